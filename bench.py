@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""AT-MGRIT hot-path benchmark (BASELINE.json metric: DOF*steps/s of batched
+Phi relaxation; AT-MGRIT time-to-tolerance).
+
+Workload (BASELINE config 5, the batch-scaling sweep): 1D heat, n = 4095
+interior points, N_t = 2^18 steps on t in [0, 1], fp64, u0 = random_state(7, n),
+two-level AT-MGRIT with m = 16, k = 8, F-relaxation, random initial guess
+(seed 20).  One "step" = one AT-MGRIT iteration: F-relaxation with the fused
+restriction tail, window exchange, 16385 truncated local coarse solves,
+correction F-relaxation with the fused C-point norm tail, norm reduction and
+its device->host read.  DOF*steps counts n x (relaxation Phi applications) =
+n x 2 x F_0 per iteration (F_0 = 245760 fine F-points).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU: launched by torchrun, one process per GPU, time shards of the
+reference rank layout; NCCL (from the C++ runtime) moves halo rows, window
+payloads and the norm squares; gloo only broadcasts the NCCL id.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(name="config5_heat1d_n4095_Nt2^18_m16_k8", n=4095, n_points=2 ** 18 + 1, m=16, k=8,
+                tf=1.0, u0_seed=7, guess_seed=20, tol=1e-10)
+# bounded CPU sample of the same workload (same n, m, k, dt-per-level shape at
+# reduced N_t): the reference's own CPU implementation on the host cores
+CPU_SAMPLE = dict(n=4095, n_points=2 ** 14 + 1, m=16, k=8, tf=1.0 / 16)
+
+
+def level0_counts(n_points, m):
+    nc = (n_points - 1) // m + 1
+    F = n_points - nc
+    n_iv = nc if (nc - 1) * m + 1 <= n_points - 1 else nc - 1
+    return F, nc, n_iv
+
+
+def dof_steps_per_iter(n, n_points, m):
+    F, _, _ = level0_counts(n_points, m)
+    return 2.0 * n * F
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.proc = None
+        self.index = index
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = max(mx, float(parts[2]))
+                except ValueError:
+                    continue
+                names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        except FileNotFoundError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_run(iters, workers=None, sample=CPU_SAMPLE):
+    """Time the compiled reference (oracle/_ref/tempo_ref) on the bounded sample."""
+    from oracle import oracle as O
+    n = sample["n"]
+    nproc = os.cpu_count() or 1
+    nc = (sample["n_points"] - 1) // sample["m"] + 1
+    workers = workers or min(nproc, nc)
+    args = dict(problem="heat1d", n=n, tf=sample["tf"], n_points=sample["n_points"], m=sample["m"],
+                k=sample["k"], manufactured=0, guess="random", seed=20, timing_iters=iters,
+                workers=workers, driver="parallel")
+    ic = O.random_state(7, n)
+    if O.ref_available():
+        res, _ = O.run_ref(args, files={"ic_file": ic}, timeout=3600)
+        kind = "reference"
+        secs = res["iteration_seconds"]
+    else:  # the C restatement, single thread
+        drv = O.Driver(dict(kind=O.HEAT1D, n=n, manufactured=0, ic=ic),
+                       dict(tf=sample["tf"], n_points=sample["n_points"], m=sample["m"], k=sample["k"]),
+                       dict(tol=1e-300, max_iters=iters, initial_guess=O.GUESS_RANDOM, seed=20))
+        drv.setup()
+        secs = []
+        for _ in range(iters):
+            t = time.perf_counter()
+            drv.cycle()
+            drv.residual_norm()
+            secs.append(time.perf_counter() - t)
+        kind, workers = "port", 1
+    per_iter = float(np.mean(secs))
+    value = dof_steps_per_iter(n, sample["n_points"], sample["m"]) / per_iter
+    desc = (f"config-5 shape (n={n}, m={sample['m']}, k={sample['k']}) at N_t={sample['n_points'] - 1}, "
+            f"{iters} iterations, reference run_parallel with {workers} threads")
+    return dict(value=value, unit="DOF*steps/s", cores=workers, kind=kind, sample=desc,
+                seconds_per_iteration=per_iter, seconds=secs)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--n-points", type=int, default=WORKLOAD["n_points"])
+    ap.add_argument("--k", type=int, default=WORKLOAD["k"])
+    ap.add_argument("--m", type=int, default=WORKLOAD["m"])
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    W = dict(WORKLOAD, n_points=args.n_points, k=args.k, m=args.m)
+    n = W["n"]
+    unit = "DOF*steps/s"
+    metric = "DOF*steps/s of batched Phi relaxation (AT-MGRIT iteration)"
+    config = {"workload": W["name"] if (args.n_points, args.k, args.m) == (WORKLOAD["n_points"], WORKLOAD["k"], WORKLOAD["m"])
+              else f"heat1d_n4095_Np{args.n_points}_m{args.m}_k{args.k}",
+              "n_dof": n, "n_points": W["n_points"], "m": W["m"], "k": W["k"], "relaxation": "F",
+              "mode": "two-level", "dtype": "f64", "global_batch": W["n_points"], "seq_len": n,
+              "parallelism": f"time-shards{world}",
+              "l2_flush": "inputs larger than L2 (8.59 GB level-0 array)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference_run(args.warmup + args.steps)
+        secs = r["seconds"][args.warmup:] or r["seconds"]
+        per = float(np.mean(secs))
+        value = dof_steps_per_iter(n, CPU_SAMPLE["n_points"], CPU_SAMPLE["m"]) / per
+        line = {"impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": dict(config, sample=r["sample"]),
+                "cpu_baseline": {"value": value, "unit": unit, "cores": r["cores"], "kind": r["kind"],
+                                 "sample": r["sample"]},
+                "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import paper_2107_09596_b200 as T
+    from oracle import oracle as O  # noqa: F401  (input generation only: random_state)
+
+    nccl_id = None
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        pg = dist
+        import ctypes as C
+        buf = (C.c_char * 128)()
+        if rank == 0:
+            assert T.lib().atm_nccl_unique_id(buf) == 0, "NCCL unavailable"
+        obj = [bytes(buf) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    ic = T.random_state(W["u0_seed"], n)
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, W["tf"], W["n_points"]), [W["m"]], W["k"])
+    cfg = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=W["tol"],
+                         max_iters=1_000_000, initial_guess=T.InitialGuess.Random, seed=W["guess_seed"])
+    app = T.Heat1D(n, manufactured_forcing=False, initial_condition=ic)
+    drv = T.CycleDriver(app, hier, cfg, device=local if world > 1 else 0, trace=True,
+                        world_size=world, rank=rank, nccl_id=nccl_id)
+    drv.setup()
+    drv.iterate(args.warmup)
+    t_before = drv.timings(with_counts=True)
+    launches = drv.last_iteration_launches()
+    if pg:
+        pg.barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.__enter__()
+    norms, ms = drv.iterate_timed(args.steps)
+    if sampler:
+        sampler.__exit__()
+    if pg:
+        import torch
+        t = torch.tensor([ms], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    t_after = drv.timings(with_counts=True)
+
+    per_iter = dof_steps_per_iter(n, W["n_points"], W["m"])
+    value = per_iter * args.steps / (ms / 1e3)
+    # dominant kernel: the correction F-sweep (fused C-point norm tail)
+    s1, c1 = t_after.get("sweep_correct", (0.0, 0))
+    s0, c0 = t_before.get("sweep_correct", (0.0, 0))
+    sweep_ms = 1e3 * (s1 - s0) / max(c1 - c0, 1)
+    F0, nc0, niv0 = level0_counts(W["n_points"], W["m"])
+    # algorithmic bytes of this rank's launch: write its F rows, read its seeds
+    rr = T.rank_ranges(hier, world, rank)
+    my_iv = rr["iv_count"][0]
+    my_F = sum(min(iv * W["m"] + W["m"] - 1, W["n_points"] - 1) - iv * W["m"]
+               for iv in range(rr["iv_first"][0], rr["iv_first"][0] + my_iv))
+    sweep_bytes = 8.0 * n * (my_F + my_iv)
+    peak, peak_src = read_peaks()
+    achieved = sweep_bytes / (sweep_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    phase_ms = {k: 1e3 * (v[0] - t_before.get(k, (0.0, 0))[0]) / args.steps for k, v in t_after.items()}
+
+    line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded splitmix64 u0 and initial guess, as the reference)",
+            "config": config,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "heat_sweep_kernel<16> (correction F-sweep + C-point norm tail)",
+                         "algorithmic_bytes_per_launch": sweep_bytes, "avg_launch_ms": sweep_ms,
+                         "peak_source": peak_src},
+            "gpu_launches": launches * args.steps,
+            "phase_ms_per_step": phase_ms,
+            "last_norm": float(norms[-1])}
+    if sampler:
+        line["clocks"] = sampler.summary()
+
+    # ---- e2e through the public API with host buffers (pinned)
+    if not args.no_e2e:
+        npts = W["n_points"]
+        if pg:
+            my_rows = None
+        guess = np.empty((npts, n), np.float64)
+        rng = np.random.default_rng(1234)
+        for i0 in range(0, npts, 16384):
+            i1 = min(npts, i0 + 16384)
+            guess[i0:i1] = rng.uniform(-1.0, 1.0, size=(i1 - i0, n))
+        guess[0] = ic
+        out = np.empty_like(guess)
+        reg = T.lib().atm_host_register(guess.ctypes.data, guess.nbytes) == 0
+        reg &= T.lib().atm_host_register(out.ctypes.data, out.nbytes) == 0
+        cfg2 = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=1e-300,
+                              max_iters=args.steps, initial_guess=T.InitialGuess.Provided,
+                              provided=guess)
+        drv2 = T.CycleDriver(app, hier, cfg2, device=local if world > 1 else 0,
+                             world_size=world, rank=rank, nccl_id=nccl_id)
+        if pg:
+            pg.barrier()
+        t0 = time.perf_counter()
+        drv2.setup()                      # H2D of the provided level-0 guess
+        rep = drv2.drive()                # K iterations, norms read back each iteration
+        drv2.get_level(0, out=out)        # D2H of the level-0 solution
+        wall = time.perf_counter() - t0
+        if pg:
+            import torch
+            t = torch.tensor([wall], dtype=torch.float64)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            wall = float(t.item())
+        h2d = guess.nbytes // max(world, 1)
+        line["e2e"] = {"value": per_iter * rep.iterations / wall, "unit": unit,
+                       "h2d_bytes_per_step": int(h2d / args.steps),
+                       "d2h_bytes_per_step": int(guess.nbytes / max(world, 1) / args.steps + 8),
+                       "wall_s": wall, "pinned": bool(reg),
+                       "what": "atm_setup(provided guess from pinned host) + atm_solve(K iterations) + atm_get_level(level 0) into pinned host"}
+        drv2.close()
+        if reg:
+            T.lib().atm_host_unregister(guess.ctypes.data)
+            T.lib().atm_host_unregister(out.ctypes.data)
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cb = cpu_reference_run(3)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "unit": unit, "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,601 @@
+"""Reference-shaped host API over the C ABI (include/atmgrit.h).
+
+Names, argument meaning and error behaviour follow the reference `tempo`
+library (/root/reference/proj/include/tempo/*.hpp) so tests read like the
+reference's own: TimeGrid.make, build_hierarchy, SolverConfig, CycleDriver
+(setup / cycle / nested_init / residual_norm / drive), solve(),
+run_parallel(), problems.Heat1D / Dahlquist, and the ScalarLinear fixture.
+All arithmetic happens in libatmgrit.so on the GPU; this module only marshals.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import lib, ptr
+
+# ---------------------------------------------------------------------------
+# errors (errors.hpp:9-42)
+
+
+class TempoError(RuntimeError):
+    pass
+
+
+class ConfigError(TempoError):
+    pass
+
+
+class DivergenceError(TempoError):
+    def __init__(self, iteration: int, what: str):
+        super().__init__(what)
+        self.iteration = iteration
+
+
+class RuntimeFault(TempoError):
+    pass
+
+
+class NonlinearSolveError(TempoError):
+    pass
+
+
+def _raise(status: int, msg: str, iteration: int = 0):
+    if status == 2:
+        raise ConfigError(msg)
+    if status == 4:
+        import re
+        m = re.search(r"iteration (\d+)", msg)
+        raise DivergenceError(int(m.group(1)) if m else iteration, msg)
+    if status == 5:
+        raise NonlinearSolveError(msg)
+    raise RuntimeFault(msg)
+
+
+# ---------------------------------------------------------------------------
+# grids (time_grid.hpp, hierarchy.hpp)
+
+
+@dataclasses.dataclass
+class TimeGrid:
+    t0: float
+    tf: float
+    n_points: int
+    dt: float
+
+    @staticmethod
+    def make(t0: float, tf: float, n_points: int) -> "TimeGrid":
+        if n_points < 2:
+            raise ConfigError("TimeGrid: need at least 2 points")
+        if not tf > t0:
+            raise ConfigError("TimeGrid: tf must exceed t0")
+        return TimeGrid(t0, tf, n_points, (tf - t0) / float(n_points - 1))
+
+    def n_steps(self):
+        return self.n_points - 1
+
+
+@dataclasses.dataclass
+class CfSplit:
+    m: int
+    c_points: list
+    intervals: list  # (c_left, first, last)
+
+
+def make_cf_split(n_points: int, m: int) -> CfSplit:
+    """hierarchy.cpp:7-22."""
+    if m < 2:
+        raise ConfigError(f"coarsening factor must exceed 1, got {m}")
+    if n_points < 2:
+        raise ConfigError("cannot split a level with fewer than 2 points")
+    last = n_points - 1
+    cps = list(range(0, last + 1, m))
+    ivs = [(c, c + 1, min(c + m - 1, last)) for c in cps if c + 1 <= min(c + m - 1, last)]
+    return CfSplit(m, cps, ivs)
+
+
+@dataclasses.dataclass
+class LocalCoarseGrid:
+    owner: int
+    lo: int
+
+    def size(self):
+        return self.owner - self.lo + 1
+
+
+class Hierarchy:
+    """build_hierarchy(fine, m, k) (hierarchy.cpp:24-50)."""
+
+    def __init__(self, fine: TimeGrid, m: Sequence[int], k: int):
+        if len(m) == 0:
+            raise ConfigError("hierarchy needs at least one coarsening factor")
+        if k < 1:
+            raise ConfigError("local-grid distance k must be at least 1")
+        self.fine = fine
+        self.m = list(m)
+        self._k = k
+        self.levels = [fine]
+        self.splits = []
+        for l, ml in enumerate(self.m):
+            cur = self.levels[-1]
+            self.splits.append(make_cf_split(cur.n_points, ml))
+            nc = (cur.n_points - 1) // ml + 1
+            if nc < 2:
+                raise ConfigError(f"coarsening exhausts the grid at level {l + 1} ({nc} points)")
+            dt = cur.dt * ml
+            self.levels.append(TimeGrid(cur.t0, cur.t0 + dt * (nc - 1), nc, dt))
+
+    def n_levels(self):
+        return len(self.levels)
+
+    def level(self, l):
+        return self.levels[l]
+
+    def k(self):
+        return self._k
+
+    def split(self, l):
+        return self.splits[l]
+
+    def coarsest(self):
+        return self.n_levels() - 1
+
+    def n_coarsest_points(self):
+        return self.levels[-1].n_points
+
+    def local_grid(self, p):
+        return LocalCoarseGrid(p, max(0, p - self._k + 1))
+
+    def is_global_coarse_grid(self):
+        return self._k >= self.n_coarsest_points()
+
+    def coarsening_factors(self):
+        return list(self.m)
+
+    def c_grid(self) -> _capi.atm_grid:
+        g = _capi.atm_grid()
+        g.t0, g.tf, g.n_points = self.fine.t0, self.fine.tf, self.fine.n_points
+        g.n_m = len(self.m)
+        for i, v in enumerate(self.m):
+            g.m[i] = v
+        g.k = self._k
+        return g
+
+
+def build_hierarchy(fine: TimeGrid, m: Sequence[int], k: int) -> Hierarchy:
+    return Hierarchy(fine, m, k)
+
+
+# ---------------------------------------------------------------------------
+# solver configuration (solver_config.hpp:14-68)
+
+
+class CycleMode(enum.IntEnum):
+    TwoLevel = 0
+    VCycle = 1
+    NestedV = 2
+
+
+class Relaxation(enum.IntEnum):
+    F = 0
+    FCF = 1
+
+
+class NormKind(enum.IntEnum):
+    ResidualL2 = 0
+    FunctionalChange = 1
+
+
+class InitialGuess(enum.IntEnum):
+    Constant = 0
+    Random = 1
+    Provided = 2
+
+
+class StopReason(enum.IntEnum):
+    Converged = 0
+    MaxIterations = 1
+    Diverged = 2
+
+
+@dataclasses.dataclass
+class SolverConfig:
+    mode: CycleMode = CycleMode.TwoLevel
+    relaxation: Relaxation = Relaxation.F
+    nu: int = 1
+    max_iters: int = 100
+    tol: float = 1e-7
+    norm: NormKind = NormKind.ResidualL2
+    functional: Optional[np.ndarray] = None  # linear functional weights w (w . u)
+    initial_guess: InitialGuess = InitialGuess.Constant
+    seed: int = 0
+    constant_value: Optional[np.ndarray] = None
+    provided: Optional[np.ndarray] = None  # [n_points, n]
+    coarse_substeps: int = 1
+
+
+@dataclasses.dataclass
+class ConvergenceReport:
+    residual_norms: list
+    iterations: int = 0
+    converged: bool = False
+    stop_reason: StopReason = StopReason.MaxIterations
+    total_seconds: float = 0.0
+    dof_steps: float = 0.0
+    timings: dict = dataclasses.field(default_factory=dict)
+
+
+# ---------------------------------------------------------------------------
+# problems (the device Phi descriptor of an Application)
+
+
+class Application:
+    kind = 0
+
+    def vector_size(self) -> int:
+        raise NotImplementedError
+
+    def forcing_folded(self) -> bool:
+        raise NotImplementedError
+
+    def c_problem(self, keep: list) -> _capi.atm_problem:
+        raise NotImplementedError
+
+
+class Heat1D(Application):
+    """problems::Heat1D (heat1d.hpp:20-76) with an optional IC override."""
+    kind = 1
+
+    def __init__(self, n_dof=1025, x0=0.0, x1=1.0, folded=False, manufactured_forcing=True,
+                 initial_condition=None):
+        if n_dof < 1:
+            raise ConfigError("heat1d: need at least one spatial unknown")
+        if not x1 > x0:
+            raise ConfigError("heat1d: x1 must exceed x0")
+        self.n_dof, self.x0, self.x1 = n_dof, x0, x1
+        self.folded = folded
+        self.manufactured_forcing = manufactured_forcing
+        self.ic = None if initial_condition is None else np.ascontiguousarray(initial_condition, np.float64)
+
+    def vector_size(self):
+        return self.n_dof
+
+    def forcing_folded(self):
+        return self.folded
+
+    def mesh_width(self):
+        return (self.x1 - self.x0) / (self.n_dof + 1)
+
+    def c_problem(self, keep):
+        p = _capi.atm_problem()
+        p.kind, p.n, p.folded = self.kind, self.n_dof, int(self.folded)
+        p.x0, p.x1, p.manufactured = self.x0, self.x1, int(self.manufactured_forcing)
+        if self.ic is not None:
+            keep.append(self.ic)
+            p.ic = ptr(self.ic)
+        return p
+
+
+class Dahlquist(Application):
+    """problems::Dahlquist (dahlquist.hpp:12-50)."""
+    kind = 2
+
+    def __init__(self, lam=-1.0, u0=1.0, folded=False):
+        self.lam, self.u0, self.folded = lam, u0, folded
+
+    def vector_size(self):
+        return 1
+
+    def forcing_folded(self):
+        return self.folded
+
+    def c_problem(self, keep):
+        p = _capi.atm_problem()
+        p.kind, p.n, p.folded, p.lam, p.u0 = self.kind, 1, int(self.folded), self.lam, self.u0
+        return p
+
+
+class ScalarLinear(Application):
+    """The reference's scalar test fixture (tests/support.hpp:19-60)."""
+    kind = 3
+
+    def __init__(self, multipliers, u0=1.0, folded=False, fine_forcing=None):
+        self.mult = list(multipliers)
+        self.u0, self.folded = u0, folded
+        self.ff = None if fine_forcing is None else np.ascontiguousarray(fine_forcing, np.float64)
+
+    def vector_size(self):
+        return 1
+
+    def forcing_folded(self):
+        return self.folded
+
+    def c_problem(self, keep):
+        p = _capi.atm_problem()
+        p.kind, p.n, p.folded, p.u0 = self.kind, 1, int(self.folded), self.u0
+        p.n_mult = len(self.mult)
+        for i, v in enumerate(self.mult):
+            p.mult[i] = v
+        if self.ff is not None and self.ff.size:
+            keep.append(self.ff)
+            p.fine_forcing, p.n_ff = ptr(self.ff), self.ff.size
+        return p
+
+
+# ---------------------------------------------------------------------------
+# the driver
+
+
+class _LevelView:
+    """Lazy per-level array view pulled from the device (space_time.hpp:20-32)."""
+
+    def __init__(self, drv, level):
+        self._d, self._l = drv, level
+
+    def _get(self, which):
+        return self._d.get_level(self._l, which)
+
+    @property
+    def u(self):
+        return self._get(0)
+
+    @property
+    def g(self):
+        return self._get(1)
+
+    @property
+    def v(self):
+        return self._get(2)
+
+    @property
+    def r(self):
+        return self._get(3)
+
+
+class _StateView:
+    def __init__(self, drv):
+        self._d = drv
+
+    def level(self, l):
+        return _LevelView(self._d, l)
+
+
+class CycleDriver:
+    """CycleDriver (solver.hpp:67-120) backed by the device engine.
+
+    `workers` > 1 drives that many time shards (the reference's rank layout,
+    layout.cpp:29-63) with device-to-device exchanges; `world_size` > 1 runs
+    one shard per process with NCCL between processes.
+    """
+
+    def __init__(self, app: Application, hier: Hierarchy, cfg: SolverConfig, workers: int = 1,
+                 device: int = 0, trace: bool = False, world_size: int = 1, rank: int = 0,
+                 nccl_id: Optional[bytes] = None):
+        self.app, self.hier, self.cfg = app, hier, cfg
+        self._keep = []
+        p = app.c_problem(self._keep)
+        g = hier.c_grid()
+        s = _capi.atm_solver()
+        s.mode, s.relaxation, s.nu = int(cfg.mode), int(cfg.relaxation), cfg.nu
+        s.max_iters, s.tol, s.norm = cfg.max_iters, cfg.tol, int(cfg.norm)
+        s.initial_guess, s.seed, s.coarse_substeps = int(cfg.initial_guess), cfg.seed, cfg.coarse_substeps
+        n = app.vector_size()
+        for field, val in (("functional_w", cfg.functional), ("constant_value", cfg.constant_value),
+                           ("provided", cfg.provided)):
+            if val is not None:
+                a = np.ascontiguousarray(val, np.float64).reshape(-1)
+                if field == "provided" and a.size != hier.level(0).n_points * n:
+                    raise ConfigError("provided initial guess has the wrong number of points")
+                self._keep.append(a)
+                setattr(s, field, ptr(a))
+        rt = _capi.atm_runtime()
+        rt.device, rt.n_shards, rt.world_size, rt.rank = device, workers, world_size, rank
+        rt.trace = int(trace)
+        if nccl_id is not None:
+            self._nid = C.create_string_buffer(bytes(nccl_id), 128)
+            rt.nccl_id = C.cast(self._nid, C.c_void_p)
+        h = C.c_void_p()
+        st = lib().atm_create(C.byref(p), C.byref(g), C.byref(s), C.byref(rt), C.byref(h))
+        if st != 0:
+            _raise(st, lib().atm_create_error().decode())
+        self._h = h
+        self.n = lib().atm_vector_size(h)
+        self.L = lib().atm_n_levels(h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().atm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, st):
+        if st not in (0, 1):
+            _raise(st, lib().atm_last_error(self._h).decode())
+        return st
+
+    # CycleDriver methods
+    def setup(self):
+        self._check(lib().atm_setup(self._h))
+
+    def cycle(self):
+        self._check(lib().atm_cycle(self._h))
+
+    def nested_init(self):
+        self._check(lib().atm_nested_init(self._h))
+
+    def residual_norm(self) -> float:
+        out = C.c_double()
+        self._check(lib().atm_residual_norm(self._h, C.byref(out)))
+        return out.value
+
+    def drive(self) -> ConvergenceReport:
+        norms = np.zeros(self.cfg.max_iters, np.float64)
+        rep = _capi.atm_report()
+        st = lib().atm_solve(self._h, C.byref(rep), ptr(norms))
+        if st == 4:
+            msg = lib().atm_last_error(self._h).decode()
+            raise DivergenceError(rep.iterations, msg)
+        self._check(st)
+        return ConvergenceReport(list(norms[: rep.iterations]), rep.iterations, bool(rep.converged),
+                                 StopReason(rep.stop_reason), rep.total_seconds, rep.dof_steps,
+                                 self.timings())
+
+    def iterate(self, count: int) -> np.ndarray:
+        norms = np.zeros(count, np.float64)
+        self._check(lib().atm_iterate(self._h, count, ptr(norms)))
+        return norms
+
+    def iterate_timed(self, count: int):
+        """`count` cycles + norms; returns (norms, device milliseconds)."""
+        norms = np.zeros(count, np.float64)
+        ms = C.c_double()
+        self._check(lib().atm_iterate_timed(self._h, count, ptr(norms), C.byref(ms)))
+        return norms, ms.value
+
+    def timings(self, with_counts: bool = False) -> dict:
+        names = C.create_string_buffer(1024)
+        secs = np.zeros(32, np.float64)
+        k = lib().atm_phase_times(self._h, names, 1024, ptr(secs), 32)
+        keys = names.value.decode().split(",") if k else []
+        if not with_counts:
+            return {key: float(secs[i]) for i, key in enumerate(keys)}
+        cnt = (C.c_int * 32)()
+        lib().atm_phase_counts(self._h, cnt, 32)
+        return {key: (float(secs[i]), int(cnt[i])) for i, key in enumerate(keys)}
+
+    def last_iteration_launches(self) -> int:
+        n = C.c_int()
+        lib().atm_last_iteration_stats(self._h, C.byref(n), None)
+        return n.value
+
+    # state access
+    def level_points(self, l):
+        return lib().atm_level_points(self._h, l)
+
+    def get_level(self, level, which=0, first=0, count=None, out=None):
+        npts = self.level_points(level)
+        count = npts - first if count is None else count
+        if out is None:
+            out = np.zeros((count, self.n), np.float64)
+        assert out.flags.c_contiguous and out.dtype == np.float64 and out.size == count * self.n
+        self._check(lib().atm_get_level(self._h, level, which, first, count, ptr(out)))
+        return out
+
+    def set_level(self, level, values, which=0, first=0):
+        a = np.ascontiguousarray(values, np.float64).reshape(-1, self.n)
+        self._check(lib().atm_set_level(self._h, level, which, first, a.shape[0], ptr(a)))
+
+    def state(self):
+        return _StateView(self)
+
+    # Application-level and kernel-level entry points
+    def apply_phi(self, level, first_index, inputs):
+        a = np.ascontiguousarray(inputs, np.float64).reshape(-1, self.n)
+        out = np.empty_like(a)
+        self._check(lib().atm_apply_phi(self._h, level, first_index, a.shape[0], ptr(a), ptr(out)))
+        return out
+
+    def forcing(self, level, first_index, count):
+        out = np.empty((count, self.n), np.float64)
+        self._check(lib().atm_forcing(self._h, level, first_index, count, ptr(out)))
+        return out
+
+    def f_relax(self, level, first_interval, count):
+        self._check(lib().atm_kernel_f_relax(self._h, level, first_interval, count))
+
+    def c_relax(self, level, first_c, count):
+        self._check(lib().atm_kernel_c_relax(self._h, level, first_c, count))
+
+    def residual(self, level, first, count):
+        out = np.empty((count, self.n), np.float64)
+        self._check(lib().atm_kernel_residual(self._h, level, first, count, ptr(out)))
+        return out
+
+
+@dataclasses.dataclass
+class SolveResult:
+    state: np.ndarray  # level-0 u, [n_points, n]
+    report: ConvergenceReport
+    driver: CycleDriver
+
+
+def solve(app: Application, hier: Hierarchy, cfg: SolverConfig, **kw) -> SolveResult:
+    """solve() (solver.hpp:134-135, solver.cpp:485-492) on the device."""
+    drv = CycleDriver(app, hier, cfg, **kw)
+    rep = drv.drive()
+    return SolveResult(drv.get_level(0), rep, drv)
+
+
+def run_parallel(app: Application, hier: Hierarchy, cfg: SolverConfig, workers: int, **kw):
+    """runtime::run_parallel (parallel.hpp:26-27): `workers` time shards."""
+    return solve(app, hier, cfg, workers=workers, **kw)
+
+
+# ---------------------------------------------------------------------------
+# host-only schedule helpers (no GPU needed)
+
+
+def random_state(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    lib().atm_random_state(C.c_uint64(seed), n, ptr(out))
+    return out
+
+
+@dataclasses.dataclass
+class RankLayout:
+    workers: int
+    fine_lo: list
+    fine_hi: list
+    coarse_lo: list
+    coarse_hi: list
+
+
+def build_layout(hier: Hierarchy, workers: int) -> RankLayout:
+    g = hier.c_grid()
+    arrs = [(C.c_int * max(workers, 1))() for _ in range(4)]
+    st = lib().atm_build_layout(C.byref(g), workers, *arrs)
+    if st != 0:
+        _raise(st, lib().atm_create_error().decode())
+    return RankLayout(workers, *[list(a) for a in arrs])
+
+
+def rank_ranges(hier: Hierarchy, workers: int, rank: int) -> dict:
+    g = hier.c_grid()
+    L = hier.n_levels()
+    arrs = [(C.c_int * L)() for _ in range(8)]
+    st = lib().atm_rank_ranges(C.byref(g), workers, rank, *arrs)
+    if st != 0:
+        _raise(st, lib().atm_create_error().decode())
+    keys = ["lo", "hi", "iv_first", "iv_count", "c_first", "c_count", "left_src", "right_dst"]
+    return {k: list(a) for k, a in zip(keys, arrs)}
+
+
+def window_recvs(hier: Hierarchy, workers: int, rank: int) -> list:
+    g = hier.c_grid()
+    buf = (C.c_int * (3 * 64))()
+    n = lib().atm_window_recvs(C.byref(g), workers, rank, buf, 64)
+    if n < 0:
+        _raise(2, lib().atm_create_error().decode())
+    return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(min(n, 64))]
+
+
+def build_comm_groups(n_coarse_points: int, k: int):
+    """layout.cpp:65-81 (kept for schedule parity tests)."""
+    if k < 1:
+        raise ConfigError("comm groups: k must be at least 1")
+    if n_coarse_points < 1:
+        raise ConfigError("comm groups: empty coarse grid")
+    first = [list(range(s, min(s + k, n_coarse_points))) for s in range(0, n_coarse_points, k)]
+    second = []
+    for s in range(k - 1, n_coarse_points, k):
+        g = list(range(s, min(s + k, n_coarse_points)))
+        if len(g) > 1:
+            second.append(g)
+    return first, second

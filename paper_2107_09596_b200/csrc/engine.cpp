@@ -1,0 +1,1447 @@
+// engine.cpp -- host runtime of the B200 AT-MGRIT path (see engine.hpp).
+//
+// Reference citations are relative to /root/reference/proj.
+#include "engine.hpp"
+
+#include <cudaTypedefs.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+namespace atm {
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+[[noreturn]] void config_error(const std::string& m) { throw Error(ATM_CONFIG_ERROR, m); }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error(ATM_RUNTIME_FAULT, std::string("CUDA error: ") + cudaGetErrorString(e) +
+                                           " in " + what);
+}
+#define CK(x) ck((x), #x)
+
+int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            throw Error(ATM_RUNTIME_FAULT, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2D view [rows * pitch/16][16 doubles], box = one point row, 128B swizzle.
+CUtensorMap make_row_map(double* ptr, int rows, int pitch) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    const cuuint64_t dims[2] = {16, static_cast<cuuint64_t>(rows) * (pitch / 16)};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(pitch / 16)};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, ptr, dims, strides, box,
+                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw Error(ATM_RUNTIME_FAULT, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return m;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded lazily so the library has no link-time NCCL dependency
+
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*ErrStr)(ncclResult_t) = nullptr;
+
+    bool load() {
+        if (h) return true;
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+#define SYM(f, n) f = reinterpret_cast<decltype(f)>(dlsym(h, n)); if (!f) return false
+        SYM(GetUniqueId, "ncclGetUniqueId");
+        SYM(CommInitRank, "ncclCommInitRank");
+        SYM(CommDestroy, "ncclCommDestroy");
+        SYM(Send, "ncclSend");
+        SYM(Recv, "ncclRecv");
+        SYM(GroupStart, "ncclGroupStart");
+        SYM(GroupEnd, "ncclGroupEnd");
+        SYM(AllReduce, "ncclAllReduce");
+        SYM(ErrStr, "ncclGetErrorString");
+#undef SYM
+        return true;
+    }
+    void check(ncclResult_t r, const char* what) const {
+        if (r != ncclSuccess)
+            throw Error(ATM_RUNTIME_FAULT, std::string("NCCL error in ") + what + ": " + ErrStr(r));
+    }
+};
+
+static NcclApi& nccl_global() {
+    static NcclApi api;
+    return api;
+}
+
+atm_status nccl_unique_id(void* out) {
+    NcclApi& api = nccl_global();
+    if (!api.load()) return ATM_RUNTIME_FAULT;
+    ncclUniqueId id;
+    if (api.GetUniqueId(&id) != ncclSuccess) return ATM_RUNTIME_FAULT;
+    std::memcpy(out, &id, sizeof(id));
+    return ATM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// hierarchy / layout / ranges (host restatements)
+
+Hier make_hier(const atm_grid& g) {
+    // TimeGrid::make (time_grid.hpp:14-23)
+    if (g.n_points < 2) config_error("TimeGrid: need at least 2 points");
+    if (!(g.tf > g.t0)) config_error("TimeGrid: tf must exceed t0");
+    // build_hierarchy (hierarchy.cpp:24-50)
+    if (g.n_m < 1 || g.n_m >= ATM_MAX_LEVELS) config_error("hierarchy needs at least one coarsening factor");
+    if (g.k < 1) config_error("local-grid distance k must be at least 1");
+    Hier h;
+    h.L = g.n_m + 1;
+    h.k = g.k;
+    h.t0 = g.t0;
+    h.np.push_back(g.n_points);
+    h.dt.push_back((g.tf - g.t0) / static_cast<double>(g.n_points - 1));
+    for (int l = 0; l < g.n_m; ++l) {
+        if (g.m[l] < 2) config_error("coarsening factor must exceed 1, got " + std::to_string(g.m[l]));
+        const int nc = (h.np.back() - 1) / g.m[l] + 1;
+        if (nc < 2)
+            config_error("coarsening exhausts the grid at level " + std::to_string(l + 1) + " (" +
+                         std::to_string(nc) + " points)");
+        h.m.push_back(g.m[l]);
+        h.np.push_back(nc);
+        h.dt.push_back(h.dt.back() * g.m[l]);
+    }
+    return h;
+}
+
+int Layout::owner_of_fine(int i) const {
+    for (int r = 0; r < workers; ++r)
+        if (i >= fine_lo[r] && i <= fine_hi[r]) return r;
+    config_error("layout: fine point " + std::to_string(i) + " is unowned");
+}
+
+int Layout::owner_of_coarse(int p) const {
+    for (int r = 0; r < workers; ++r)
+        if (p >= coarse_lo[r] && p <= coarse_hi[r]) return r;
+    config_error("layout: coarse point " + std::to_string(p) + " is unowned");
+}
+
+// layout.cpp:29-63: near-even split of coarsest C-points; fine block
+// (T_{lo-1}, T_hi], point 0 with the first rank, trailing points with the last.
+Layout build_layout(const Hier& h, int workers) {
+    const int n_coarse = h.np.back();
+    if (workers < 1) config_error("layout: need at least one worker");
+    if (workers > n_coarse)
+        config_error("layout: " + std::to_string(workers) + " workers exceed the " +
+                     std::to_string(n_coarse) + " coarsest-level points");
+    const int stride = h.stride_total();
+    const int n_fine = h.np[0];
+    Layout lay;
+    lay.workers = workers;
+    const int base = n_coarse / workers, extra = n_coarse % workers;
+    int next = 0;
+    for (int r = 0; r < workers; ++r) {
+        const int size = base + (r < extra ? 1 : 0);
+        const int lo = next, hi = next + size - 1;
+        next = hi + 1;
+        lay.coarse_lo.push_back(lo);
+        lay.coarse_hi.push_back(hi);
+        lay.fine_lo.push_back(r == 0 ? 0 : (lo - 1) * stride + 1);
+        lay.fine_hi.push_back(r == workers - 1 ? n_fine - 1 : hi * stride);
+    }
+    return lay;
+}
+
+// parallel.cpp:67-130
+Ranges compute_ranges(const Hier& h, const Layout& lay, int rank) {
+    const int L = h.L;
+    Ranges rr;
+    rr.lo.assign(L, 0);
+    rr.hi.assign(L, -1);
+    rr.iv_first.assign(L, 0);
+    rr.iv_count.assign(L, 0);
+    rr.c_first.assign(L, 0);
+    rr.c_count.assign(L, 0);
+    rr.left_src.assign(L, -1);
+    rr.right_dst.assign(L, -1);
+    const int fine_lo = lay.fine_lo[rank], fine_hi = lay.fine_hi[rank];
+    int stride = 1;
+    for (int l = 0; l < L; ++l) {
+        const int n_l = h.np[l];
+        const int lo = ceil_div(fine_lo, stride);
+        const int hi = std::min(fine_hi / stride, n_l - 1);
+        rr.lo[l] = lo;
+        rr.hi[l] = hi;
+        const bool empty = lo > hi;
+        if (!empty) {
+            if (lo > 0) rr.left_src[l] = lay.owner_of_fine((lo - 1) * stride);
+            if (hi + 1 <= n_l - 1) rr.right_dst[l] = lay.owner_of_fine((hi + 1) * stride);
+        }
+        if (l < L - 1) {
+            const int m = h.m[l];
+            if (!empty) {
+                const int cf = ceil_div(lo, m), cl = hi / m;
+                if (cf <= cl) {
+                    rr.c_first[l] = cf;
+                    rr.c_count[l] = cl - cf + 1;
+                }
+                // intervals whose first F-point lies in [lo, hi]
+                const int niv = h.n_iv(l);
+                int first = -1, count = 0;
+                for (int nI = std::max(0, (lo - 1) / m - 1); nI < niv; ++nI) {
+                    const int f = nI * m + 1;
+                    if (f > hi) break;
+                    if (f >= lo) {
+                        if (first < 0) first = nI;
+                        ++count;
+                    }
+                }
+                rr.iv_first[l] = count > 0 ? first : 0;
+                rr.iv_count[l] = count;
+            }
+            stride *= m;
+        }
+    }
+    return rr;
+}
+
+// ---------------------------------------------------------------------------
+// Engine: construction
+
+Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, const atm_runtime& rt)
+    : prob_(p), sol_(s), rt_(rt) {
+    H_ = make_hier(g);
+    if (s.coarse_substeps < 1) config_error("coarse_substeps must be at least 1");
+    kind_ = p.kind;
+    switch (kind_) {
+        case ATM_PHI_HEAT1D:
+            n_ = p.n;
+            if (n_ < 1) config_error("heat1d: need at least one spatial unknown");
+            if (!(p.x1 > p.x0)) config_error("heat1d: x1 must exceed x0");
+            if (n_ > 4096) config_error("heat1d: n > 4096 exceeds the single-CTA row kernel");
+            heat_ = true;
+            folded_ = p.folded != 0;
+            break;
+        case ATM_PHI_DAHLQUIST:
+        case ATM_PHI_SCALAR:
+            n_ = 1;
+            folded_ = p.folded != 0;
+            if (kind_ == ATM_PHI_SCALAR && p.n_mult < H_.L)
+                config_error("scalar: one multiplier per level");
+            break;
+        case ATM_PHI_ALLEN_CAHN:
+        case ATM_PHI_HEAT2D:
+            config_error("Phi family not available in this build");
+        default:
+            config_error("unknown problem kind " + std::to_string(kind_));
+    }
+    // CycleDriver::validate (solver.cpp:51-79)
+    if (!(s.tol > 0.0)) config_error("solver: tol must be positive");
+    if (s.max_iters < 1) config_error("solver: max_iters must be at least 1");
+    if (s.relaxation == ATM_RELAX_FCF && s.nu < 1) config_error("solver: FCF relaxation needs nu >= 1");
+    if (s.mode == ATM_TWO_LEVEL) {
+        if (H_.L != 2) config_error("two-level mode needs a two-level hierarchy");
+        if (folded_) config_error("two-level residual-correction mode needs explicit forcing");
+    } else if (!folded_) {
+        config_error("FAS cycles need forcing folded into the integrator");
+    }
+    if (s.norm == ATM_NORM_FUNCTIONAL && !s.functional_w)
+        config_error("functional-change stopping norm needs a functional");
+    if (s.initial_guess == ATM_GUESS_PROVIDED && !s.provided)
+        config_error("provided initial guess has the wrong number of points");
+
+    pitch_ = heat_ ? ((n_ + 15) / 16) * 16 : 1;
+    // host copies of caller-owned inputs
+    ic_.assign(n_, 0.0);
+    if (heat_) {
+        h_ = (p.x1 - p.x0) / static_cast<double>(n_ + 1);  // heat1d.cpp:16
+        sinp_.resize(n_);
+        for (int i = 0; i < n_; ++i) sinp_[i] = std::sin(kPi * (p.x0 + h_ * (i + 1)));
+        ic_ = sinp_;  // heat1d.cpp:85-91
+    } else {
+        ic_[0] = p.u0;
+    }
+    if (p.ic) ic_.assign(p.ic, p.ic + n_);
+    if (kind_ == ATM_PHI_SCALAR && p.fine_forcing && p.n_ff > 0)
+        ff_.assign(p.fine_forcing, p.fine_forcing + p.n_ff);
+    if (s.functional_w) fw_.assign(s.functional_w, s.functional_w + n_);
+    if (s.constant_value) cval_.assign(s.constant_value, s.constant_value + n_);
+    // the provided guess stays caller-owned until setup (no host copy: it can
+    // be the full level-0 array)
+    prov_ptr_ = s.provided;
+    prob_.ic = nullptr;
+    prob_.fine_forcing = nullptr;
+    prob_.source = nullptr;
+    sol_.functional_w = nullptr;
+    sol_.constant_value = nullptr;
+    sol_.provided = nullptr;
+
+    world_ = std::max(1, rt.world_size);
+    rank_ = rt.rank;
+    const int local = std::max(1, rt.n_shards);
+    if (world_ > 1 && local != 1) config_error("multi-process runs drive one shard per process");
+    G_ = world_ > 1 ? world_ : local;
+    lay_ = build_layout(H_, G_);
+    trace_ = rt.trace != 0;
+    if (const char* e = std::getenv("ATM_HEAT_L")) L_heat_ = std::atoi(e);
+    else {
+        L_heat_ = 2;
+        while (L_heat_ < 16 && pitch_ / L_heat_ > 256) L_heat_ *= 2;
+    }
+
+    CK(cudaSetDevice(rt.device));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+
+    if (world_ > 1) {
+        nccl_.reset(new NcclApi());
+        if (!nccl_->load()) throw Error(ATM_RUNTIME_FAULT, "cannot load libnccl.so.2");
+        if (!rt.nccl_id) config_error("multi-process run needs an NCCL unique id");
+        ncclUniqueId id;
+        std::memcpy(&id, rt.nccl_id, sizeof(id));
+        ncclComm_t c = nullptr;
+        nccl_->check(nccl_->CommInitRank(&c, world_, id, rank_), "ncclCommInitRank");
+        comm_ = c;
+    }
+
+    // shards driven by this process
+    if (world_ > 1) {
+        sh_.resize(1);
+        sh_[0].gid = rank_;
+    } else {
+        sh_.resize(G_);
+        for (int i = 0; i < G_; ++i) sh_[i].gid = i;
+    }
+    // global buffers
+    auto dalloc = [&](size_t bytes) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        CK(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+        gallocs_.push_back(p);
+        return static_cast<double*>(p);
+    };
+    const int np0 = H_.np[0];
+    d_sq_full_ = dalloc(sizeof(double) * np0);
+    d_sq_c_ = dalloc(sizeof(double) * np0);
+    d_norm_ = dalloc(sizeof(double) * 300);
+    d_fmax_ = dalloc(sizeof(double) * std::max(1, G_));
+    d_prevf_ = dalloc(sizeof(double) * np0);
+    d_ic_ = dalloc(sizeof(double) * pitch_);
+    d_row_ = dalloc(sizeof(double) * pitch_);
+    CK(cudaMemcpy(d_ic_, ic_.data(), sizeof(double) * n_, cudaMemcpyHostToDevice));
+    if (!fw_.empty()) {
+        d_fw_ = dalloc(sizeof(double) * n_);
+        CK(cudaMemcpy(d_fw_, fw_.data(), sizeof(double) * n_, cudaMemcpyHostToDevice));
+    }
+    if (!ff_.empty()) {
+        d_ff_ = dalloc(sizeof(double) * ff_.size());
+        CK(cudaMemcpy(d_ff_, ff_.data(), sizeof(double) * ff_.size(), cudaMemcpyHostToDevice));
+    }
+    for (Shard& s : sh_) alloc_shard(s);
+    for (Shard& s : sh_) build_coefs(s);
+}
+
+Engine::~Engine() {
+    if (st_) cudaStreamSynchronize(st_);
+    for (Shard& s : sh_)
+        for (LevelDev& L : s.lv)
+            for (void* p : L.allocs) cudaFree(p);
+    for (void* p : gallocs_) cudaFree(p);
+    for (auto& pe : pending_) {
+        cudaEventDestroy(pe.second.first);
+        cudaEventDestroy(pe.second.second);
+    }
+    for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+    if (comm_ && nccl_) nccl_->CommDestroy(static_cast<ncclComm_t>(comm_));
+    if (st_) cudaStreamDestroy(st_);
+}
+
+DArr Engine::alloc_arr(LevelDev& L, int base, int rows, bool tmap) {
+    DArr a;
+    a.base = base;
+    a.rows = std::max(rows, 0);
+    if (a.rows == 0) return a;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(a.rows) * pitch_;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    CK(cudaMemsetAsync(p, 0, bytes, st_));
+    L.allocs.push_back(p);
+    a.p = static_cast<double*>(p);
+    if (tmap && heat_) {
+        a.tm = make_row_map(a.p, a.rows, pitch_);
+        a.has_tm = true;
+    }
+    return a;
+}
+
+void Engine::alloc_shard(Shard& s) {
+    const Ranges rr = compute_ranges(H_, lay_, s.gid);
+    const int L = H_.L, lc = H_.coarsest();
+    s.lv.resize(L);
+    for (int l = 0; l < L; ++l) {
+        LevelDev& Lv = s.lv[l];
+        Lv.lo = rr.lo[l];
+        Lv.hi = rr.hi[l];
+        Lv.iv_first = rr.iv_first[l];
+        Lv.iv_count = rr.iv_count[l];
+        Lv.c_first = rr.c_first[l];
+        Lv.c_count = rr.c_count[l];
+        Lv.left = rr.left_src[l];
+        Lv.right = rr.right_dst[l];
+        if (Lv.hi < Lv.lo) continue;
+        int base = std::max(0, Lv.lo - 1);
+        if (l == lc && l >= 1) base = std::min(base, std::max(0, Lv.lo - H_.k + 1));
+        Lv.base = base;
+        const int rows = Lv.hi - base + 1;
+        Lv.u = alloc_arr(Lv, base, rows, true);
+        // g: full per-point array where forcing is stored, else point 0 only
+        bool g_full = false;
+        if (l == 0 && !folded_) {
+            const bool heat_forced = heat_ && prob_.manufactured;
+            const bool scalar_forced = (kind_ == ATM_PHI_SCALAR) && !ff_.empty();
+            g_full = heat_forced || scalar_forced;
+        }
+        if (l >= 1 && l < lc && sol_.mode != ATM_TWO_LEVEL) g_full = true;
+        Lv.g_full = g_full;
+        if (g_full) Lv.g = alloc_arr(Lv, base, rows, true);
+        else if (base == 0) Lv.g = alloc_arr(Lv, 0, 1, true);
+        if (l >= 1) {
+            Lv.v = alloc_arr(Lv, base, rows, true);
+            Lv.r = alloc_arr(Lv, base, rows, true);
+            if (l == lc && sol_.mode != ATM_TWO_LEVEL) {
+                Lv.w = alloc_arr(Lv, base, rows, true);
+                Lv.x = alloc_arr(Lv, base, rows, true);
+            }
+        }
+    }
+}
+
+void Engine::build_coefs(Shard& s) {
+    const int L = H_.L, lc = H_.coarsest();
+    for (int l = 0; l < L; ++l) {
+        LevelDev& Lv = s.lv[l];
+        const int S = (l == lc) ? sol_.coarse_substeps : 1;  // solver.cpp:39
+        const double dt = H_.dt[l];
+        const double sub_dt = dt / S;
+        auto up = [&](const std::vector<double>& v) {
+            void* p = nullptr;
+            CK(cudaMalloc(&p, sizeof(double) * std::max<size_t>(v.size(), 1)));
+            if (!v.empty())
+                CK(cudaMemcpy(p, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice));
+            Lv.allocs.push_back(p);
+            return static_cast<const double*>(p);
+        };
+        if (heat_) {
+            const HeatLevelHost hh = heat_level_host(n_, pitch_, L_heat_, sub_dt, h_, S);
+            HeatCoefDev& c = Lv.hco;
+            c.beta = up(hh.beta);
+            c.gamma = up(hh.gamma);
+            c.cneg = up(hh.cneg);
+            c.scan = up(hh.scan);
+            c.warpA = up(hh.warpA);
+            c.r = hh.r;
+            c.beta_c = hh.beta_c;
+            c.gamma_c = hh.gamma_c;
+            c.cneg_c = hh.cneg_c;
+            c.i0 = hh.i0;
+            c.n = n_;
+            c.pitch = pitch_;
+            c.nt = hh.nt;
+            c.L = hh.L;
+            c.substeps = S;
+            if (prob_.manufactured) {
+                // theta per (index, substep): heat1d.cpp:72-75 evaluated on the host
+                const int np = H_.np[l];
+                std::vector<double> th(static_cast<size_t>(np) * S, 0.0);
+                for (int i = 1; i < np; ++i)
+                    for (int ss = 1; ss <= S; ++ss) {
+                        const double t = (H_.t0 + dt * (i - 1)) + sub_dt * ss;
+                        th[static_cast<size_t>(i) * S + (ss - 1)] =
+                            sub_dt * (-(std::sin(t) - kPi * kPi * std::cos(t)));
+                    }
+                c.theta = up(th);
+                std::vector<double> prof(static_cast<size_t>(hh.nt) * hh.L, 0.0);
+                for (int i = 0; i < n_; ++i) prof[i] = sinp_[i];
+                c.prof = up(prof);
+            }
+        } else {
+            ScalarCoefDev& c = Lv.sco;
+            if (kind_ == ATM_PHI_DAHLQUIST) {
+                // dahlquist.hpp:36-42
+                const double hh = dt / S;
+                const double m = 1.0 / (1.0 - prob_.lambda * hh);
+                double out = m;
+                for (int ss = 1; ss < S; ++ss) out *= m;
+                c.mult = out;
+            } else {
+                c.mult = prob_.mult[l];
+            }
+            c.ff = (folded_ && l == 0 && d_ff_) ? d_ff_ : nullptr;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+
+int Engine::grid_for(int jobs, bool window, size_t smem) {
+    if (jobs <= 0) return 0;
+    if (!heat_) return 1;
+    const int nt = sh_[0].lv[0].hco.nt;
+    const int occ = heat_max_ctas_per_sm(L_heat_, nt, smem, window);
+    return std::max(1, std::min(jobs, sms_ * occ));
+}
+
+void Engine::check_launch(int err, const char* what) {
+    ++launches_;
+    if (err != 0)
+        throw Error(ATM_RUNTIME_FAULT, std::string("kernel launch failed (") + what + "): " +
+                                           cudaGetErrorString(static_cast<cudaError_t>(err)));
+}
+
+void Engine::phase_begin(const char* name) {
+    if (!trace_) return;
+    cudaEvent_t a, b;
+    if (ev_pool_.size() >= 2) {
+        a = ev_pool_.back(); ev_pool_.pop_back();
+        b = ev_pool_.back(); ev_pool_.pop_back();
+    } else {
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+    }
+    CK(cudaEventRecord(a, st_));
+    Pending pe;
+    pe.first = name;
+    pe.second = {a, b};
+    pending_.push_back(pe);
+}
+
+void Engine::phase_end() {
+    if (!trace_ || pending_.empty()) return;
+    // close the innermost open phase
+    for (auto it = pending_.rbegin(); it != pending_.rend(); ++it) {
+        if (!it->closed) {
+            CK(cudaEventRecord(it->second.second, st_));
+            it->closed = true;
+            break;
+        }
+    }
+}
+
+// sweep jobs [j0, j1) on one shard/level
+void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail, int m_override,
+                        double* sq, int sq_base) {
+    if (j1 <= j0) return;
+    LevelDev& Lv = s.lv[level];
+    const int m = m_override > 0 ? m_override : H_.m[level];
+    const bool add_g = Lv.g_full;
+    LevelDev* out_lv = (tail == TAIL_STORE && m_override <= 0) ? &s.lv[level + 1] : nullptr;
+    if (heat_) {
+        SweepArgs a{};
+        a.co = Lv.hco;
+        a.kind = kind;
+        a.m = m;
+        a.np = H_.np[level];
+        a.j0 = j0;
+        a.j1 = j1;
+        a.u_base = Lv.u.base;
+        a.g_base = add_g ? Lv.g.base : 0;
+        a.add_g = add_g;
+        a.forced = folded_ && prob_.manufactured;
+        a.store = 1;
+        a.tail = tail;
+        a.out_base = out_lv ? out_lv->r.base : 0;
+        a.sq = sq;
+        a.sq_base = sq_base;
+        const CUtensorMap& tg = add_g ? Lv.g.tm : Lv.u.tm;
+        const CUtensorMap& to = out_lv ? out_lv->r.tm : Lv.u.tm;
+        const int grid = grid_for(j1 - j0, false, heat_sweep_smem(a));
+        check_launch(launch_heat_sweep(a, Lv.u.tm, tg, to, grid, st_), "heat_sweep");
+    } else {
+        ScalarSweepArgs a{};
+        a.co = Lv.sco;
+        a.kind = kind;
+        a.m = m;
+        a.np = H_.np[level];
+        a.j0 = j0;
+        a.j1 = j1;
+        a.u = Lv.u.p;
+        a.u_base = Lv.u.base;
+        a.g = add_g ? Lv.g.p : nullptr;
+        a.g_base = add_g ? Lv.g.base : 0;
+        a.add_g = add_g;
+        a.store = 1;
+        a.tail = tail;
+        a.out = out_lv ? out_lv->r.p : nullptr;
+        a.out_base = out_lv ? out_lv->r.base : 0;
+        a.sq = sq;
+        a.sq_base = sq_base;
+        check_launch(launch_scalar_sweep(a, st_), "scalar_sweep");
+    }
+}
+
+void Engine::window_launch(Shard& s, int level, int kind, int pre_lo, int pre_e0, int pre_e1,
+                           int p0, int p1, const DArr& x1, const DArr& x2, const DArr& x3,
+                           const DArr& out, int out_stride, int forced, int seed_zero, int idx0,
+                           int seed_off) {
+    const bool has_pre = (kind <= WK_FORWARD) && pre_e1 >= pre_e0;
+    const int jobs = (has_pre ? 1 : 0) + std::max(0, p1 - p0 + 1);
+    if (jobs <= 0) return;
+    LevelDev& Lv = s.lv[level];
+    if (heat_) {
+        WindowArgs a{};
+        a.co = Lv.hco;
+        a.kind = kind;
+        a.k = H_.k;
+        a.pre_lo = pre_lo;
+        a.pre_e0 = pre_e0;
+        a.pre_e1 = pre_e1;
+        a.p0 = p0;
+        a.p1 = p1;
+        a.x1_base = x1.base;
+        a.x2_base = x2.base;
+        a.x3_base = x3.base;
+        a.out_base = out.base;
+        a.out_stride = out_stride;
+        a.forced = forced;
+        a.seed_zero = seed_zero;
+        a.idx0 = idx0;
+        a.seed_off = seed_off;
+        const CUtensorMap& t1 = x1.has_tm ? x1.tm : out.tm;
+        const CUtensorMap& t2 = x2.has_tm ? x2.tm : t1;
+        const CUtensorMap& t3 = x3.has_tm ? x3.tm : t1;
+        const int grid = grid_for(jobs, true, heat_window_smem(a));
+        check_launch(launch_heat_window(a, t1, t2, t3, out.tm, grid, st_), "heat_window");
+    } else {
+        ScalarWindowArgs a{};
+        a.co = Lv.sco;
+        if (forced == 0 && kind == WK_APPLY) a.co.ff = Lv.sco.ff;
+        a.kind = kind;
+        a.k = H_.k;
+        a.pre_lo = pre_lo;
+        a.pre_e0 = pre_e0;
+        a.pre_e1 = pre_e1;
+        a.p0 = p0;
+        a.p1 = p1;
+        a.x1 = x1.p;
+        a.x1_base = x1.base;
+        a.x2 = x2.p;
+        a.x2_base = x2.base;
+        a.x3 = x3.p;
+        a.x3_base = x3.base;
+        a.out = out.p;
+        a.out_base = out.base;
+        a.out_stride = out_stride;
+        a.seed_zero = seed_zero;
+        a.idx0 = idx0;
+        a.seed_off = seed_off;
+        check_launch(launch_scalar_window(a, st_), "scalar_window");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exchanges (Execution hooks, solver.hpp:40-60)
+
+void Engine::halo(int level, DArr LevelDev::*arr) {
+    // sync_left_edge (parallel.cpp:236-249): u[lo-1] <- left neighbour's u[hi]
+    if (G_ == 1) return;
+    const size_t bytes = sizeof(double) * pitch_;
+    if (world_ == 1) {
+        for (Shard& s : sh_) {
+            LevelDev& Lv = s.lv[level];
+            if (Lv.hi < Lv.lo || Lv.lo == 0 || Lv.left < 0) continue;
+            const DArr& src = sh_[Lv.left].lv[level].*arr;
+            const DArr& dst = Lv.*arr;
+            const int i = Lv.lo - 1;
+            CK(cudaMemcpyAsync(dst.p + static_cast<size_t>(i - dst.base) * pitch_,
+                               src.p + static_cast<size_t>(i - src.base) * pitch_, bytes,
+                               cudaMemcpyDeviceToDevice, st_));
+        }
+        return;
+    }
+    Shard& s = sh_[0];
+    LevelDev& Lv = s.lv[level];
+    if (Lv.hi < Lv.lo) return;
+    const DArr& a = Lv.*arr;
+    ncclComm_t c = static_cast<ncclComm_t>(comm_);
+    nccl_->check(nccl_->GroupStart(), "group");
+    if (Lv.right >= 0)
+        nccl_->check(nccl_->Send(a.p + static_cast<size_t>(Lv.hi - a.base) * pitch_, pitch_,
+                                 ncclFloat64, Lv.right, c, st_), "send halo");
+    if (Lv.lo > 0 && Lv.left >= 0)
+        nccl_->check(nccl_->Recv(a.p + static_cast<size_t>(Lv.lo - 1 - a.base) * pitch_, pitch_,
+                                 ncclFloat64, Lv.left, c, st_), "recv halo");
+    nccl_->check(nccl_->GroupEnd(), "group");
+}
+
+// Window payloads (exchange_local_windows, parallel.cpp:134-194): each shard
+// receives exactly the coarsest indices [max(0, lo-k+1), lo-1] it lacks.
+void Engine::window_exchange(int level, DArr LevelDev::*arr) {
+    if (G_ == 1) return;
+    const int k = H_.k;
+    const size_t rowb = sizeof(double) * pitch_;
+    if (world_ == 1) {
+        for (Shard& s : sh_) {
+            LevelDev& Lv = s.lv[level];
+            if (Lv.hi < Lv.lo) continue;
+            const int need_lo = std::max(0, Lv.lo - k + 1);
+            for (int j = need_lo; j < Lv.lo; ++j) {
+                const int o = lay_.owner_of_coarse(j);
+                const DArr& src = sh_[o].lv[level].*arr;
+                const DArr& dst = Lv.*arr;
+                CK(cudaMemcpyAsync(dst.p + static_cast<size_t>(j - dst.base) * pitch_,
+                                   src.p + static_cast<size_t>(j - src.base) * pitch_, rowb,
+                                   cudaMemcpyDeviceToDevice, st_));
+            }
+        }
+        return;
+    }
+    Shard& s = sh_[0];
+    LevelDev& Lv = s.lv[level];
+    const DArr& a = Lv.*arr;
+    ncclComm_t c = static_cast<ncclComm_t>(comm_);
+    nccl_->check(nccl_->GroupStart(), "group");
+    for (int q = 0; q < G_; ++q) {
+        if (q == rank_) continue;
+        const Ranges rq = compute_ranges(H_, lay_, q);
+        // what q needs from me
+        const int q_lo = rq.lo[level];
+        const int q_need_lo = std::max(0, q_lo - k + 1), q_need_hi = q_lo - 1;
+        const int a0 = std::max(q_need_lo, Lv.lo), a1 = std::min(q_need_hi, Lv.hi);
+        if (a1 >= a0 && Lv.hi >= Lv.lo)
+            nccl_->check(nccl_->Send(a.p + static_cast<size_t>(a0 - a.base) * pitch_,
+                                     static_cast<size_t>(a1 - a0 + 1) * pitch_, ncclFloat64, q, c,
+                                     st_), "send window");
+        // what I need from q
+        const int my_need_lo = std::max(0, Lv.lo - k + 1), my_need_hi = Lv.lo - 1;
+        const int b0 = std::max(my_need_lo, rq.lo[level]), b1 = std::min(my_need_hi, rq.hi[level]);
+        if (b1 >= b0 && Lv.hi >= Lv.lo)
+            nccl_->check(nccl_->Recv(a.p + static_cast<size_t>(b0 - a.base) * pitch_,
+                                     static_cast<size_t>(b1 - b0 + 1) * pitch_, ncclFloat64, q, c,
+                                     st_), "recv window");
+    }
+    nccl_->check(nccl_->GroupEnd(), "group");
+    (void)rowb;
+}
+
+double Engine::reduce_norm(double* sq, int count) {
+    if (world_ > 1)
+        nccl_->check(nccl_->AllReduce(sq, sq, count, ncclFloat64, ncclSum,
+                                      static_cast<ncclComm_t>(comm_), st_), "allreduce squares");
+    check_launch(launch_norm_from_squares(sq, count, d_norm_, st_), "norm");
+    double out = 0.0;
+    CK(cudaMemcpyAsync(&out, d_norm_, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// setup (solver.cpp:81-150)
+
+void Engine::fill_initial_guess() {
+    for (Shard& s : sh_) {
+        LevelDev& Lv = s.lv[0];
+        if (Lv.hi < Lv.lo) continue;
+        const int i0 = std::max(1, Lv.lo), i1 = Lv.hi + 1;
+        if (Lv.lo == 0)
+            check_launch(launch_fill_rows(Lv.u.p, Lv.u.base, pitch_, n_, 0, 1, d_ic_, st_), "fill ic");
+        switch (sol_.initial_guess) {
+            case ATM_GUESS_CONSTANT: {
+                double* v = d_ic_;
+                if (!cval_.empty()) {
+                    void* p = nullptr;
+                    CK(cudaMalloc(&p, sizeof(double) * n_));
+                    Lv.allocs.push_back(p);
+                    CK(cudaMemcpy(p, cval_.data(), sizeof(double) * n_, cudaMemcpyHostToDevice));
+                    v = static_cast<double*>(p);
+                }
+                check_launch(launch_fill_rows(Lv.u.p, Lv.u.base, pitch_, n_, i0, i1, v, st_), "fill const");
+                break;
+            }
+            case ATM_GUESS_RANDOM:
+                check_launch(launch_fill_random(Lv.u.p, Lv.u.base, pitch_, n_, i0, i1, sol_.seed, st_),
+                             "fill random");
+                break;
+            case ATM_GUESS_PROVIDED:
+                if (i1 > i0)
+                    CK(cudaMemcpy2DAsync(Lv.u.p + static_cast<size_t>(i0 - Lv.u.base) * pitch_,
+                                         sizeof(double) * pitch_, prov_ptr_ + static_cast<size_t>(i0) * n_,
+                                         sizeof(double) * n_, sizeof(double) * n_, i1 - i0,
+                                         cudaMemcpyHostToDevice, st_));
+                break;
+        }
+    }
+}
+
+void Engine::fill_level_rhs(int level) {
+    // g_0 = IC; g_i = 0 (folded) or forcing(level, i)  (solver.cpp:136-150)
+    for (Shard& s : sh_) {
+        LevelDev& Lv = s.lv[level];
+        if (Lv.hi < Lv.lo) continue;
+        if (Lv.g.p && Lv.g.base == 0 && Lv.lo <= 1)
+            check_launch(launch_fill_rows(Lv.g.p, Lv.g.base, pitch_, n_, 0, 1, d_ic_, st_), "g0");
+        if (!Lv.g_full) continue;
+        const int i0 = std::max(1, Lv.lo), i1 = Lv.hi;
+        if (folded_) {
+            if (i1 >= i0)
+                CK(cudaMemsetAsync(Lv.g.p + static_cast<size_t>(i0 - Lv.g.base) * pitch_, 0,
+                                   sizeof(double) * pitch_ * (i1 - i0 + 1), st_));
+        } else if (heat_) {
+            // forcing(level, i) = propagate(zero, with forcing) (heat1d.cpp:97-100)
+            window_launch(s, level, WK_APPLY, 0, 0, -1, i0, i1, Lv.g, Lv.g, Lv.g, Lv.g, 1, 1, 1, 0, 0);
+        } else {
+            // scalar fixture: forcing(0, i) = ff[i] (tests/support.hpp:43-49)
+            std::vector<double> rows(static_cast<size_t>(i1 - i0 + 1), 0.0);
+            for (int i = i0; i <= i1; ++i)
+                rows[i - i0] = (level == 0 && i < static_cast<int>(ff_.size())) ? ff_[i] : 0.0;
+            if (i1 >= i0)
+                CK(cudaMemcpyAsync(Lv.g.p + (i0 - Lv.g.base), rows.data(), sizeof(double) * rows.size(),
+                                   cudaMemcpyHostToDevice, st_));
+            CK(cudaStreamSynchronize(st_));
+        }
+    }
+}
+
+void Engine::setup() {
+    if (setup_done_) return;
+    phase_begin("setup");
+    fill_initial_guess();
+    fill_level_rhs(0);
+    if (sol_.norm == ATM_NORM_FUNCTIONAL) {
+        for (Shard& s : sh_) {
+            LevelDev& Lv = s.lv[0];
+            if (Lv.c_count > 0)
+                check_launch(launch_functional_init(Lv.u.p, Lv.u.base, H_.m[0], pitch_, n_, d_fw_,
+                                                    d_prevf_, Lv.c_first, Lv.c_first + Lv.c_count, st_),
+                             "functional init");
+        }
+    }
+    phase_end();
+    CK(cudaStreamSynchronize(st_));
+    setup_done_ = true;
+}
+
+// ---------------------------------------------------------------------------
+// cycle pieces
+
+void Engine::point0_residual(Shard& s, int level, double* r_out, double* sq_out) {
+    // r_0 = g_0 - u_0 (kernels.cpp:35-37)
+    LevelDev& Lv = s.lv[level];
+    if (Lv.lo != 0 || Lv.hi < 0) return;
+    const double* g0 = Lv.g.p;  // row 0 in both layouts (base == 0)
+    check_launch(launch_row_diff(r_out, g0, Lv.u.p, n_, sq_out, st_), "r0");
+}
+
+// F-relaxation over own intervals (kernels.cpp:7-17) with optional tail
+void Engine::f_sweep(int level, int tail, int /*out_level*/) {
+    halo(level, &LevelDev::u);
+    const char* tag = level != 0 ? nullptr : tail == TAIL_SQ ? "sweep_correct"
+                                           : tail == TAIL_STORE ? "sweep_relax" : "sweep_f";
+    if (tag) phase_begin(tag);
+    for (Shard& s : sh_) {
+        LevelDev& Lv = s.lv[level];
+        if (Lv.iv_count == 0) continue;
+        sweep_jobs(s, level, SW_F, Lv.iv_first, Lv.iv_first + Lv.iv_count, tail, 0,
+                   tail == TAIL_SQ ? d_sq_c_ : nullptr, 0);
+    }
+    if (tag) phase_end();
+}
+
+// relax_level (solver.cpp:160-172).  With F-relaxation the restriction
+// residuals are produced by the sweep's tail.
+void Engine::relax_level(int level, bool restrict_tail) {
+    if (sol_.relaxation == ATM_RELAX_F) {
+        f_sweep(level, restrict_tail ? TAIL_STORE : TAIL_NONE, level + 1);
+        return;
+    }
+    if (sol_.nu == 1) {
+        // fused F-C-F: job J chains from the old C_{J-1} through the
+        // C-relaxation of C_J into interval J (kernels.cpp:7-28)
+        halo(level, &LevelDev::u);
+        for (Shard& s : sh_) {
+            LevelDev& Lv = s.lv[level];
+            if (Lv.c_count == 0) continue;
+            int j1 = Lv.c_first + Lv.c_count;
+            sweep_jobs(s, level, SW_FCF, Lv.c_first, j1, TAIL_NONE, 0, nullptr, 0);
+        }
+        if (G_ > 1) {
+            // the first interval of a shard waits for its left neighbour's new C
+            halo(level, &LevelDev::u);
+            for (Shard& s : sh_) {
+                LevelDev& Lv = s.lv[level];
+                if (Lv.iv_count == 0 || Lv.iv_first >= Lv.c_first) continue;
+                sweep_jobs(s, level, SW_F, Lv.iv_first, Lv.iv_first + 1, TAIL_NONE, 0, nullptr, 0);
+            }
+        }
+        return;
+    }
+    f_sweep(level, TAIL_NONE, level + 1);
+    for (int it = 0; it < sol_.nu; ++it) {
+        for (Shard& s : sh_) {
+            LevelDev& Lv = s.lv[level];
+            const int j0 = std::max(1, Lv.c_first), j1 = Lv.c_first + Lv.c_count;
+            sweep_jobs(s, level, SW_CRELAX, j0, j1, TAIL_NONE, 0, nullptr, 0);
+        }
+        f_sweep(level, TAIL_NONE, level + 1);
+    }
+}
+
+// residual at own C-points of `level` into level+1 r (solver.cpp:307-314)
+void Engine::resid_c(int level) {
+    for (Shard& s : sh_) {
+        LevelDev& Lv = s.lv[level];
+        if (Lv.c_count == 0) continue;
+        const int j0 = std::max(1, Lv.c_first), j1 = Lv.c_first + Lv.c_count;
+        sweep_jobs(s, level, SW_RESID, j0, j1, TAIL_STORE, 0, nullptr, 0);
+    }
+}
+
+void Engine::restrict_to(int level) {
+    // solver.cpp:194-222
+    const int lc = H_.coarsest();
+    const int m = H_.m[level];
+    const bool relaxed = (level + 1) != lc;
+    if (sol_.relaxation != ATM_RELAX_F) resid_c(level);
+    if (sol_.relaxation != ATM_RELAX_F && G_ > 1) halo(level, &LevelDev::u);
+    for (Shard& s : sh_) {
+        LevelDev& F = s.lv[level];
+        LevelDev& C = s.lv[level + 1];
+        if (F.c_count == 0) continue;
+        const int j0 = F.c_first, cnt = F.c_count;
+        // injection: coarse u = coarse v = fine u at C-points (kernels.cpp:45-51)
+        const size_t rowb = sizeof(double) * pitch_;
+        const double* src = F.u.p + static_cast<size_t>(j0 * m - F.u.base) * pitch_;
+        for (DArr* dst : {&C.u, &C.v})
+            CK(cudaMemcpy2DAsync(dst->p + static_cast<size_t>(j0 - dst->base) * pitch_, rowb, src,
+                                 rowb * m, rowb, cnt, cudaMemcpyDeviceToDevice, st_));
+        if (j0 > 0 && C.v.valid(j0 - 1) && F.u.valid((j0 - 1) * m))
+            CK(cudaMemcpyAsync(C.v.p + static_cast<size_t>(j0 - 1 - C.v.base) * pitch_,
+                               F.u.p + static_cast<size_t>((j0 - 1) * m - F.u.base) * pitch_, rowb,
+                               cudaMemcpyDeviceToDevice, st_));
+        if (j0 == 0) point0_residual(s, level, C.r.p, nullptr);
+        if (relaxed) {
+            // g_j = (v_j - Psi_j(v_{j-1})) + r_j, j >= 1; g_0 = v_0 + r_0
+            const int p0 = std::max(1, j0), p1 = j0 + cnt - 1;
+            window_launch(s, level + 1, WK_FAS_RHS, 0, 0, -1, p0, p1, C.v, C.v, C.r, C.g, 1,
+                          folded_ && prob_.manufactured, 0, 0, 0);
+            if (j0 == 0)
+                check_launch(launch_row_sum(C.g.p, C.v.p, C.r.p, n_, st_), "g0 fas");
+        }
+    }
+}
+
+void Engine::windows(int kind) {
+    // coarsest_linear / coarsest_fas / nested forward (solver.cpp:224-279, :347-356)
+    const int lc = H_.coarsest();
+    const int k = H_.k;
+    for (Shard& s : sh_) {
+        LevelDev& C = s.lv[lc];
+        if (C.hi < C.lo) continue;
+        const int plo = C.lo, phi = C.hi;
+        // windows with lo = 0 (p <= k-1) share one prefix chain
+        const int pre_e0 = plo, pre_e1 = std::min(k - 1, phi);
+        const int p0 = std::max(plo, k), p1 = phi;
+        const int forced = folded_ && prob_.manufactured;
+        if (kind == WK_LINEAR) {
+            LevelDev& F = s.lv[0];
+            window_launch(s, lc, WK_LINEAR, 0, pre_e0, pre_e1, p0, p1, C.r, C.r, C.r, F.u, H_.m[0],
+                          forced, 0, 0, 0);
+        } else if (kind == WK_FAS) {
+            // Psi(v_{j-1}) once per coarse point, shared by every window
+            const int a0 = std::max(1, C.base + 1);
+            window_launch(s, lc, WK_APPLY, 0, 0, -1, a0, phi, C.v, C.v, C.v, C.w, 1, forced, 0, 0, -1);
+            window_launch(s, lc, WK_FAS, 0, pre_e0, pre_e1, p0, p1, C.r, C.v, C.w, C.u, 1, forced,
+                          0, 0, 0);
+        } else {
+            window_launch(s, lc, WK_FORWARD, 0, pre_e0, pre_e1, p0, p1, C.x, C.x, C.x, C.u, 1,
+                          forced, 0, 0, 0);
+        }
+    }
+}
+
+void Engine::coarsest_linear() {
+    phase_begin("exchange");
+    window_exchange(1, &LevelDev::r);
+    phase_end();
+    phase_begin("coarse");
+    windows(WK_LINEAR);
+    phase_end();
+}
+
+void Engine::coarsest_fas() {
+    const int lc = H_.coarsest();
+    phase_begin("exchange");
+    window_exchange(lc, &LevelDev::v);
+    window_exchange(lc, &LevelDev::r);
+    phase_end();
+    phase_begin("coarse");
+    windows(WK_FAS);
+    phase_end();
+}
+
+void Engine::correct_from(int level) {
+    // solver.cpp:281-292
+    const int m = H_.m[level];
+    for (Shard& s : sh_) {
+        LevelDev& F = s.lv[level];
+        LevelDev& C = s.lv[level + 1];
+        if (F.c_count == 0) continue;
+        check_launch(launch_c_correct(F.u.p, F.u.base, m, C.u.p, C.v.p, C.u.base, pitch_, n_,
+                                      F.c_first, F.c_first + F.c_count, st_), "c_correct");
+    }
+    f_sweep(level, level == 0 ? TAIL_SQ : TAIL_NONE, level + 1);
+    if (level == 0)
+        for (Shard& s : sh_) point0_residual(s, 0, d_row_, d_sq_c_);
+}
+
+void Engine::v_cycle(int level) {
+    // solver.cpp:294-303
+    if (level == H_.coarsest()) {
+        coarsest_fas();
+        return;
+    }
+    phase_begin("relax");
+    relax_level(level, sol_.relaxation == ATM_RELAX_F);
+    phase_end();
+    phase_begin("restrict");
+    restrict_to(level);
+    phase_end();
+    v_cycle(level + 1);
+    phase_begin("correct");
+    correct_from(level);
+    phase_end();
+}
+
+void Engine::two_level_cycle() {
+    // solver.cpp:305-320
+    phase_begin("relax");
+    relax_level(0, sol_.relaxation == ATM_RELAX_F);
+    phase_end();
+    phase_begin("restrict");
+    if (sol_.relaxation != ATM_RELAX_F) resid_c(0);
+    for (Shard& s : sh_) point0_residual(s, 0, s.lv[1].r.p, nullptr);
+    phase_end();
+    coarsest_linear();
+    phase_begin("correct");
+    f_sweep(0, TAIL_SQ, 1);
+    for (Shard& s : sh_) point0_residual(s, 0, d_row_, d_sq_c_);
+    phase_end();
+}
+
+void Engine::cycle() {
+    setup();
+    launches_ = 0;
+    if (sol_.mode == ATM_TWO_LEVEL) two_level_cycle();
+    else v_cycle(0);
+    last_launches_ = launches_;
+}
+
+void Engine::nested_init() {
+    // solver.cpp:331-368
+    setup();
+    const int lc = H_.coarsest();
+    for (int l = 0; l < lc; ++l) {
+        const int m = H_.m[l];
+        for (Shard& s : sh_) {
+            LevelDev& F = s.lv[l];
+            LevelDev& C = s.lv[l + 1];
+            if (F.c_count == 0) continue;
+            const size_t rowb = sizeof(double) * pitch_;
+            CK(cudaMemcpy2DAsync(C.u.p + static_cast<size_t>(F.c_first - C.u.base) * pitch_, rowb,
+                                 F.u.p + static_cast<size_t>(F.c_first * m - F.u.base) * pitch_,
+                                 rowb * m, rowb, F.c_count, cudaMemcpyDeviceToDevice, st_));
+        }
+        fill_level_rhs(l + 1);
+    }
+    const int forced = folded_ && prob_.manufactured;
+    if (H_.k >= H_.np[lc]) {
+        // chain_forward: sequential across shards (parallel.cpp:257-277)
+        for (size_t si = 0; si < sh_.size(); ++si) {
+            Shard& s = sh_[si];
+            LevelDev& C = s.lv[lc];
+            if (C.hi < C.lo) continue;
+            if (world_ == 1 && C.lo > 0) {
+                const DArr& src = sh_[C.left].lv[lc].u;
+                CK(cudaMemcpyAsync(C.u.p + static_cast<size_t>(C.lo - 1 - C.u.base) * pitch_,
+                                   src.p + static_cast<size_t>(C.lo - 1 - src.base) * pitch_,
+                                   sizeof(double) * pitch_, cudaMemcpyDeviceToDevice, st_));
+            } else if (world_ > 1 && C.lo > 0) {
+                nccl_->check(nccl_->Recv(C.u.p + static_cast<size_t>(C.lo - 1 - C.u.base) * pitch_,
+                                         pitch_, ncclFloat64, C.left, static_cast<ncclComm_t>(comm_), st_),
+                             "chain recv");
+            }
+            const int from = std::max(0, C.lo - 1);
+            window_launch(s, lc, WK_FORWARD, from, std::max(1, C.lo), C.hi, 1, 0, C.u, C.u, C.u,
+                          C.u, 1, forced, 0, 0, 0);
+            if (world_ > 1 && C.right >= 0)
+                nccl_->check(nccl_->Send(C.u.p + static_cast<size_t>(C.hi - C.u.base) * pitch_, pitch_,
+                                         ncclFloat64, C.right, static_cast<ncclComm_t>(comm_), st_),
+                             "chain send");
+        }
+    } else {
+        for (Shard& s : sh_) {
+            LevelDev& C = s.lv[lc];
+            if (C.hi < C.lo) continue;
+            CK(cudaMemcpyAsync(C.x.p + static_cast<size_t>(C.lo - C.x.base) * pitch_,
+                               C.u.p + static_cast<size_t>(C.lo - C.u.base) * pitch_,
+                               sizeof(double) * pitch_ * (C.hi - C.lo + 1), cudaMemcpyDeviceToDevice, st_));
+        }
+        window_exchange(lc, &LevelDev::x);
+        windows(WK_FORWARD);
+    }
+    for (int l = lc - 1; l >= 0; --l) {
+        const int m = H_.m[l];
+        for (Shard& s : sh_) {
+            LevelDev& F = s.lv[l];
+            LevelDev& C = s.lv[l + 1];
+            if (F.c_count == 0) continue;
+            const size_t rowb = sizeof(double) * pitch_;
+            CK(cudaMemcpy2DAsync(F.u.p + static_cast<size_t>(F.c_first * m - F.u.base) * pitch_,
+                                 rowb * m, C.u.p + static_cast<size_t>(F.c_first - C.u.base) * pitch_,
+                                 rowb, rowb, F.c_count, cudaMemcpyDeviceToDevice, st_));
+        }
+        f_sweep(l, TAIL_NONE, l + 1);
+        if (l >= 1) v_cycle(l);
+    }
+    CK(cudaStreamSynchronize(st_));
+}
+
+double Engine::residual_norm() {
+    // full residual over all level-0 points (solver.cpp:370-378), m = 1 jobs
+    setup();
+    phase_begin("norm");
+    halo(0, &LevelDev::u);
+    for (Shard& s : sh_) {
+        LevelDev& Lv = s.lv[0];
+        if (Lv.hi < Lv.lo) continue;
+        sweep_jobs(s, 0, SW_RESID, std::max(1, Lv.lo), Lv.hi + 1, TAIL_SQ, 1, d_sq_full_, 0);
+        point0_residual(s, 0, d_row_, d_sq_full_);
+    }
+    const double v = reduce_norm(d_sq_full_, H_.np[0]);
+    phase_end();
+    return v;
+}
+
+double Engine::functional_change() {
+    double mx = 0.0;
+    for (size_t i = 0; i < sh_.size(); ++i) {
+        LevelDev& Lv = sh_[i].lv[0];
+        if (Lv.c_count == 0) continue;
+        check_launch(launch_functional_change(Lv.u.p, Lv.u.base, H_.m[0], pitch_, n_, d_fw_,
+                                              d_prevf_, Lv.c_first, Lv.c_first + Lv.c_count,
+                                              d_fmax_ + i, st_), "functional");
+    }
+    if (world_ > 1)
+        nccl_->check(nccl_->AllReduce(d_fmax_, d_fmax_, 1, ncclFloat64, ncclMax,
+                                      static_cast<ncclComm_t>(comm_), st_), "allreduce max");
+    std::vector<double> h(sh_.size(), 0.0);
+    CK(cudaMemcpyAsync(h.data(), d_fmax_, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    for (double v : h) mx = std::max(mx, v);
+    return mx;
+}
+
+double Engine::stopping_norm_after_cycle() {
+    // stopping_norm (solver.cpp:380-396).  After a cycle every F-point
+    // residual is bitwise zero (the last operation on each F-point is the
+    // correction F-relaxation from its predecessor), so the C-point squares
+    // written by the correction sweep's tail are the full per-point array.
+    if (sol_.norm == ATM_NORM_FUNCTIONAL) return functional_change();
+    phase_begin("norm");
+    const double v = reduce_norm(d_sq_c_, H_.np[0]);
+    phase_end();
+    return v;
+}
+
+double Engine::iterate_timed(int count, double* norms) {
+    setup();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaStreamSynchronize(st_));
+    CK(cudaEventRecord(a, st_));
+    for (int i = 0; i < count; ++i) {
+        cycle();
+        const double v = stopping_norm_after_cycle();
+        if (norms) norms[i] = v;
+    }
+    CK(cudaEventRecord(b, st_));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
+}
+
+void Engine::iterate(int count, double* norms) {
+    setup();
+    for (int i = 0; i < count; ++i) {
+        cycle();
+        const double v = stopping_norm_after_cycle();
+        if (norms) norms[i] = v;
+    }
+}
+
+int Engine::solve(atm_report* rep, double* norms) {
+    // drive (solver.cpp:398-435)
+    const auto t0 = std::chrono::steady_clock::now();
+    setup();
+    if (sol_.mode == ATM_NESTED_V) nested_init();
+    atm_report r{};
+    r.stop_reason = 1;
+    double dof_steps = 0.0;
+    int status = ATM_NOT_CONVERGED;
+    for (int it = 1; it <= sol_.max_iters; ++it) {
+        cycle();
+        const double v = stopping_norm_after_cycle();
+        if (norms) norms[it - 1] = v;
+        r.iterations = it;
+        // relaxation Phi applications: every F-point twice per level visit
+        for (int l = 0; l + 1 < H_.L; ++l) {
+            const double F = static_cast<double>(H_.np[l] - H_.n_c(l));
+            double per = 2.0 * F;
+            if (sol_.relaxation == ATM_RELAX_FCF) per += sol_.nu * (F + H_.n_c(l) - 1);
+            dof_steps += per * n_;
+        }
+        if (!std::isfinite(v)) {
+            r.stop_reason = 2;
+            r.total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            r.dof_steps = dof_steps;
+            if (rep) *rep = r;
+            throw Error(ATM_DIVERGED, "non-finite residual norm at iteration " + std::to_string(it));
+        }
+        if (v <= sol_.tol) {
+            r.converged = 1;
+            r.stop_reason = 0;
+            status = ATM_OK;
+            break;
+        }
+    }
+    CK(cudaStreamSynchronize(st_));
+    r.total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    r.dof_steps = dof_steps;
+    if (rep) *rep = r;
+    return status;
+}
+
+// ---------------------------------------------------------------------------
+// state access and kernel-level entry points
+
+static LevelDev* owner_level(std::vector<Shard>& sh, int level, int i) {
+    for (Shard& s : sh) {
+        LevelDev& Lv = s.lv[level];
+        if (i >= Lv.lo && i <= Lv.hi) return &Lv;
+    }
+    return nullptr;
+}
+
+// copy [first, first+count) of one array kind between host and device,
+// one 2D copy per owning shard
+void Engine::xfer_level(int level, int which, int first, int count, double* host, bool to_host) {
+    if (level < 0 || level >= H_.L) config_error("level out of range");
+    if (count < 0 || first < 0 || first + count > H_.np[level]) config_error("point range out of range");
+    if (!to_host) setup();
+    CK(cudaStreamSynchronize(st_));
+    if (to_host) std::fill(host, host + static_cast<size_t>(count) * n_, 0.0);
+    for (Shard& s : sh_) {
+        LevelDev& Lv = s.lv[level];
+        DArr* a = which == 0 ? &Lv.u : which == 1 ? &Lv.g : which == 2 ? &Lv.v : &Lv.r;
+        if (!a->p) continue;
+        // owned points (plus, for writes, any allocated row such as halos)
+        int lo = to_host ? std::max(Lv.lo, a->base) : a->base;
+        int hi = to_host ? std::min(Lv.hi, a->base + a->rows - 1) : a->base + a->rows - 1;
+        lo = std::max(lo, first);
+        hi = std::min(hi, first + count - 1);
+        if (hi < lo) continue;
+        double* h = host + static_cast<size_t>(lo - first) * n_;
+        double* d = a->p + static_cast<size_t>(lo - a->base) * pitch_;
+        if (to_host)
+            CK(cudaMemcpy2DAsync(h, sizeof(double) * n_, d, sizeof(double) * pitch_,
+                                 sizeof(double) * n_, hi - lo + 1, cudaMemcpyDeviceToHost, st_));
+        else
+            CK(cudaMemcpy2DAsync(d, sizeof(double) * pitch_, h, sizeof(double) * n_,
+                                 sizeof(double) * n_, hi - lo + 1, cudaMemcpyHostToDevice, st_));
+    }
+    CK(cudaStreamSynchronize(st_));
+}
+
+void Engine::get_level(int level, int which, int first, int count, double* out) {
+    xfer_level(level, which, first, count, out, true);
+}
+
+void Engine::set_level(int level, int which, int first, int count, const double* in) {
+    xfer_level(level, which, first, count, const_cast<double*>(in), false);
+}
+
+void Engine::apply_phi(int level, int first, int count, const double* in, double* out,
+                       bool forcing) {
+    if (level < 0 || level >= H_.L) config_error("level out of range");
+    if (count <= 0) return;
+    if (first < 1 || first + count > H_.np[level]) config_error("step index out of range");
+    Shard& s = sh_[0];
+    LevelDev tmp;
+    DArr x = alloc_arr(tmp, 0, count, true);
+    DArr y = alloc_arr(tmp, 0, count, true);
+    if (!forcing)
+        CK(cudaMemcpy2DAsync(x.p, sizeof(double) * pitch_, in, sizeof(double) * n_,
+                             sizeof(double) * n_, count, cudaMemcpyHostToDevice, st_));
+    const int forced = forcing ? 1 : (folded_ && prob_.manufactured);
+    LevelDev save = s.lv[level];
+    if (!heat_ && !forcing) {
+        // scalar: folded fine forcing indexes ff by step index
+    }
+    if (!heat_ && forcing) {
+        // scalar forcing(level, i): ff[i] on level 0 explicit, else zero
+        std::vector<double> h(count, 0.0);
+        for (int j = 0; j < count; ++j) {
+            const int i = first + j;
+            h[j] = (!folded_ && level == 0 && i < static_cast<int>(ff_.size())) ? ff_[i] : 0.0;
+        }
+        std::memcpy(out, h.data(), sizeof(double) * count);
+    } else {
+        window_launch(s, level, WK_APPLY, 0, 0, -1, 0, count - 1, x, x, x, y, 1, forced,
+                      forcing ? 1 : 0, first, 0);
+        CK(cudaMemcpy2DAsync(out, sizeof(double) * n_, y.p, sizeof(double) * pitch_,
+                             sizeof(double) * n_, count, cudaMemcpyDeviceToHost, st_));
+    }
+    CK(cudaStreamSynchronize(st_));
+    (void)save;
+    for (void* p : tmp.allocs) cudaFree(p);
+}
+
+void Engine::kernel_f_relax(int level, int first_iv, int count) {
+    if (G_ != 1) config_error("kernel-level entry points need a single shard");
+    setup();
+    sweep_jobs(sh_[0], level, SW_F, first_iv, first_iv + count, TAIL_NONE, 0, nullptr, 0);
+    CK(cudaStreamSynchronize(st_));
+}
+
+void Engine::kernel_c_relax(int level, int first_c, int count) {
+    if (G_ != 1) config_error("kernel-level entry points need a single shard");
+    setup();
+    sweep_jobs(sh_[0], level, SW_CRELAX, std::max(1, first_c), first_c + count, TAIL_NONE, 0,
+               nullptr, 0);
+    CK(cudaStreamSynchronize(st_));
+}
+
+void Engine::kernel_residual(int level, int first, int count, double* out) {
+    if (G_ != 1) config_error("kernel-level entry points need a single shard");
+    setup();
+    Shard& s = sh_[0];
+    LevelDev tmp;
+    DArr r = alloc_arr(tmp, first, count, true);
+    LevelDev& Lv = s.lv[level];
+    if (heat_) {
+        SweepArgs a{};
+        a.co = Lv.hco;
+        a.kind = SW_RESID;
+        a.m = 1;
+        a.np = H_.np[level];
+        a.j0 = std::max(1, first);
+        a.j1 = first + count;
+        a.u_base = Lv.u.base;
+        a.add_g = Lv.g_full;
+        a.g_base = Lv.g_full ? Lv.g.base : 0;
+        a.forced = folded_ && prob_.manufactured;
+        a.store = 1;
+        a.tail = TAIL_STORE;
+        a.out_base = first;
+        const int grid = grid_for(a.j1 - a.j0, false, heat_sweep_smem(a));
+        if (a.j1 > a.j0)
+            check_launch(launch_heat_sweep(a, Lv.u.tm, Lv.g_full ? Lv.g.tm : Lv.u.tm, r.tm, grid, st_),
+                         "resid");
+    } else {
+        ScalarSweepArgs a{};
+        a.co = Lv.sco;
+        a.kind = SW_RESID;
+        a.m = 1;
+        a.np = H_.np[level];
+        a.j0 = std::max(1, first);
+        a.j1 = first + count;
+        a.u = Lv.u.p;
+        a.u_base = Lv.u.base;
+        a.g = Lv.g_full ? Lv.g.p : nullptr;
+        a.g_base = Lv.g_full ? Lv.g.base : 0;
+        a.add_g = Lv.g_full;
+        a.store = 1;
+        a.tail = TAIL_STORE;
+        a.out = r.p;
+        a.out_base = first;
+        check_launch(launch_scalar_sweep(a, st_), "resid");
+    }
+    if (first == 0 && Lv.g.p) check_launch(launch_row_diff(r.p, Lv.g.p, Lv.u.p, n_, nullptr, st_), "r0");
+    CK(cudaMemcpy2DAsync(out, sizeof(double) * n_, r.p, sizeof(double) * pitch_, sizeof(double) * n_,
+                         count, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    for (void* p : tmp.allocs) cudaFree(p);
+}
+
+int Engine::phase_times(char* names, int cap_names, double* secs, int cap, int* counts) const {
+    // resolve pending events (const_cast: bookkeeping only)
+    Engine* self = const_cast<Engine*>(this);
+    if (!pending_.empty()) {
+        cudaStreamSynchronize(st_);
+        for (auto& pe : self->pending_) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, pe.second.first, pe.second.second) == cudaSuccess) {
+                self->phase_sec_[pe.first] += ms * 1e-3;
+                self->phase_cnt_[pe.first] += 1;
+            }
+            self->ev_pool_.push_back(pe.second.first);
+            self->ev_pool_.push_back(pe.second.second);
+        }
+        self->pending_.clear();
+    }
+    std::string csv;
+    int i = 0;
+    for (const auto& kv : phase_sec_) {
+        if (i >= cap) break;
+        if (counts) {
+            auto it = phase_cnt_.find(kv.first);
+            counts[i] = it == phase_cnt_.end() ? 0 : it->second;
+        }
+        secs[i++] = kv.second;
+        csv += (csv.empty() ? "" : ",") + kv.first;
+    }
+    if (names && cap_names > 0) {
+        std::strncpy(names, csv.c_str(), cap_names - 1);
+        names[cap_names - 1] = 0;
+    }
+    return i;
+}
+
+}  // namespace atm

@@ -1,0 +1,99 @@
+// heat_kernels.cuh -- host/device interface of the Heat1D Phi kernels.
+//
+// Phi for problems::Heat1D (reference heat1d.cpp:47-100) is a backward-Euler
+// step: S sub-steps of a constant-coefficient tridiagonal solve
+// (I + sub_dt L) x = rhs, optionally preceded by the manufactured forcing
+// x += theta(t) * sin(pi x).  The reference runs the Thomas recurrences
+// serially per vector; here one CTA owns one state vector (one time point)
+// in registers, in a blocked arrangement (thread t holds elements
+// [t*L, t*L+L)), and each recurrence is evaluated as
+//   local chunk recurrence  ->  warp/CTA scan of affine carries  ->  fix-up.
+// The chunk/warp carry multipliers depend only on the level's coefficients
+// and are precomputed on the host (HeatLevelHost).
+#pragma once
+
+#include <cuda.h>
+#include <cstdint>
+#include <vector>
+
+namespace atm {
+
+constexpr int kMaxThreads = 512;
+constexpr int kMaxWarps = kMaxThreads / 32;
+constexpr int kScanPerThread = 12;  // Mf[5], Pf_ex, Mb[5], Pb_ex
+
+// Device view of one level's Phi coefficients.
+struct HeatCoefDev {
+    const double* beta;    // [nt*L] 1/den_i   (0 beyond n)
+    const double* gamma;   // [nt*L] r/den_i   (0 beyond n)
+    const double* cneg;    // [nt*L] -c'_i     (0 beyond n)
+    const double* scan;    // [nt][12]
+    const double* warpA;   // [2][kMaxWarps] forward / backward warp products
+    const double* theta;   // [np*S] forcing amplitude per (index, substep) or null
+    const double* prof;    // [pitch] forcing profile sin(pi x_i) or null
+    double r;              // sub_dt / h^2
+    double beta_c, gamma_c, cneg_c;  // converged coefficients (chunks >= i0)
+    int i0;                // first chunk start using constants (multiple of L)
+    int n, pitch, nt, L;
+    int substeps;
+};
+
+// Host-side construction of a level's coefficients (heat1d.cpp:24-45).
+struct HeatLevelHost {
+    std::vector<double> beta, gamma, cneg, scan, warpA;
+    double r = 0, beta_c = 0, gamma_c = 0, cneg_c = 0;
+    int i0 = 0, n = 0, pitch = 0, nt = 0, L = 0, substeps = 1;
+};
+HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, int substeps);
+
+// Job kinds of the sweep kernel (one job per C-point index J of a level).
+enum SweepKind { SW_F = 0, SW_FCF = 1, SW_CRELAX = 2, SW_RESID = 3 };
+enum TailKind { TAIL_NONE = 0, TAIL_STORE = 1, TAIL_SQ = 2 };
+
+struct SweepArgs {
+    HeatCoefDev co;
+    int kind;          // SweepKind
+    int m, np;         // level CF split
+    int j0, j1;        // job range [j0, j1)
+    int u_base;        // global index of row 0 of the u array
+    int g_base;        // global index of row 0 of the g array
+    int add_g;         // u_i = Phi(u_{i-1}) + g_i with g stored per point
+    int forced;        // Phi includes forcing (folded manufactured)
+    int store;         // store produced points (full storage)
+    int tail;          // TailKind, residual at c_{J+1}
+    int out_base;      // global (coarse) index of row 0 of the tail target
+    double* sq;        // per-point squares (TAIL_SQ), indexed by tail point - sq_base
+    int sq_base;
+};
+
+enum WindowKind { WK_LINEAR = 0, WK_FAS = 1, WK_FORWARD = 2, WK_APPLY = 3, WK_FAS_RHS = 4 };
+
+struct WindowArgs {
+    HeatCoefDev co;
+    int kind;
+    int k;             // window distance
+    int pre_lo, pre_e0, pre_e1;  // prefix job (chain from pre_lo) emitting [pre_e0, pre_e1]; pre_e1 < pre_e0 => none
+    int p0, p1;        // individual windows p in [p0, p1]
+    int x1_base, x2_base, x3_base, out_base;
+    int out_stride;    // emit row for p: out index p*out_stride (linear: fine m)
+    int forced;        // Phi includes forcing theta*prof
+    int seed_zero;     // WK_APPLY: seed is the zero vector (forcing computation)
+    int idx0;          // WK_APPLY: step index offset (job p applies Phi_{idx0+p})
+    int seed_off;      // WK_APPLY: seed row is p + seed_off
+};
+
+struct Maps {
+    CUtensorMap a, b, c, d, e;
+};
+
+// Launchers (stream-ordered).  Return cudaError_t as int.
+int launch_heat_sweep(const SweepArgs& args, const CUtensorMap& tm_u, const CUtensorMap& tm_g,
+                      const CUtensorMap& tm_out, int grid, cudaStream_t s);
+int launch_heat_window(const WindowArgs& args, const CUtensorMap& tm_x1, const CUtensorMap& tm_x2,
+                       const CUtensorMap& tm_x3, const CUtensorMap& tm_out, int grid,
+                       cudaStream_t s);
+size_t heat_sweep_smem(const SweepArgs& a);
+size_t heat_window_smem(const WindowArgs& a);
+int heat_max_ctas_per_sm(int L, int nt, size_t smem, bool window);
+
+}  // namespace atm
