@@ -471,8 +471,11 @@ void Engine::build_coefs(Shard& s) {
             c.gamma = up(hh.gamma);
             c.cneg = up(hh.cneg);
             c.scan = up(hh.scan);
-            c.warpA = up(hh.warpA);
-            c.r = hh.r;
+            c.pf = up(hh.pf);
+            c.pb = up(hh.pb);
+            c.wf = up(hh.wf);
+            c.wb = up(hh.wb);
+            c.powc = up(hh.powc);
             c.beta_c = hh.beta_c;
             c.gamma_c = hh.gamma_c;
             c.cneg_c = hh.cneg_c;
@@ -517,12 +520,19 @@ void Engine::build_coefs(Shard& s) {
 // ---------------------------------------------------------------------------
 // launch helpers
 
-int Engine::grid_for(int jobs, bool window, size_t smem) {
+// output staging: double-buffered unless a single buffer buys occupancy
+static int choose_n_out(SweepArgs a) {
+    if (const char* e = std::getenv("ATM_NOUT")) return std::atoi(e) == 1 ? 1 : 2;
+    a.n_out = 2;
+    const int o2 = heat_sweep_occupancy(a);
+    a.n_out = 1;
+    const int o1 = heat_sweep_occupancy(a);
+    return o1 > o2 ? 1 : 2;
+}
+
+int Engine::grid_for(int jobs, int occ) {
     if (jobs <= 0) return 0;
-    if (!heat_) return 1;
-    const int nt = sh_[0].lv[0].hco.nt;
-    const int occ = heat_max_ctas_per_sm(L_heat_, nt, smem, window);
-    return std::max(1, std::min(jobs, sms_ * occ));
+    return std::max(1, std::min(jobs, sms_ * std::max(1, occ)));
 }
 
 void Engine::check_launch(int err, const char* what) {
@@ -588,7 +598,9 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.sq_base = sq_base;
         const CUtensorMap& tg = add_g ? Lv.g.tm : Lv.u.tm;
         const CUtensorMap& to = out_lv ? out_lv->r.tm : Lv.u.tm;
-        const int grid = grid_for(j1 - j0, false, heat_sweep_smem(a));
+        a.n_out = choose_n_out(a);
+        int grid = grid_for(j1 - j0, heat_sweep_occupancy(a));
+        if (const char* e = std::getenv("ATM_GRID_SWEEP")) grid = std::min(grid, std::atoi(e));
         check_launch(launch_heat_sweep(a, Lv.u.tm, tg, to, grid, st_), "heat_sweep");
     } else {
         ScalarSweepArgs a{};
@@ -643,7 +655,8 @@ void Engine::window_launch(Shard& s, int level, int kind, int pre_lo, int pre_e0
         const CUtensorMap& t1 = x1.has_tm ? x1.tm : out.tm;
         const CUtensorMap& t2 = x2.has_tm ? x2.tm : t1;
         const CUtensorMap& t3 = x3.has_tm ? x3.tm : t1;
-        const int grid = grid_for(jobs, true, heat_window_smem(a));
+        int grid = grid_for(jobs, heat_window_occupancy(a));
+        if (const char* e = std::getenv("ATM_GRID_WINDOW")) grid = std::min(grid, std::atoi(e));
         check_launch(launch_heat_window(a, t1, t2, t3, out.tm, grid, st_), "heat_window");
     } else {
         ScalarWindowArgs a{};
@@ -964,6 +977,7 @@ void Engine::restrict_to(int level) {
 }
 
 void Engine::windows(int kind) {
+    if (std::getenv("ATM_SYNC_PHASES")) CK(cudaDeviceSynchronize());
     // coarsest_linear / coarsest_fas / nested forward (solver.cpp:224-279, :347-356)
     const int lc = H_.coarsest();
     const int k = H_.k;
@@ -977,8 +991,24 @@ void Engine::windows(int kind) {
         const int forced = folded_ && prob_.manufactured;
         if (kind == WK_LINEAR) {
             LevelDev& F = s.lv[0];
+            const char* dump = std::getenv("ATM_DEBUG_DUMP");
+            auto dump_rows = [&](const char* tag) {
+                CK(cudaStreamSynchronize(st_));
+                std::vector<double> h(static_cast<size_t>(C.r.rows) * pitch_);
+                CK(cudaMemcpy(h.data(), C.r.p, h.size() * 8, cudaMemcpyDeviceToHost));
+                FILE* f = std::fopen((std::string(dump) + "_r_" + tag).c_str(), "wb");
+                std::fwrite(h.data(), 8, h.size(), f);
+                std::fclose(f);
+                std::vector<double> u(static_cast<size_t>(F.u.rows) * pitch_);
+                CK(cudaMemcpy(u.data(), F.u.p, u.size() * 8, cudaMemcpyDeviceToHost));
+                f = std::fopen((std::string(dump) + "_u_" + tag).c_str(), "wb");
+                std::fwrite(u.data(), 8, u.size(), f);
+                std::fclose(f);
+            };
+            if (dump) dump_rows("before");
             window_launch(s, lc, WK_LINEAR, 0, pre_e0, pre_e1, p0, p1, C.r, C.r, C.r, F.u, H_.m[0],
                           forced, 0, 0, 0);
+            if (dump) dump_rows("after");
         } else if (kind == WK_FAS) {
             // Psi(v_{j-1}) once per coarse point, shared by every window
             const int a0 = std::max(1, C.base + 1);
@@ -1380,7 +1410,8 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
         a.store = 1;
         a.tail = TAIL_STORE;
         a.out_base = first;
-        const int grid = grid_for(a.j1 - a.j0, false, heat_sweep_smem(a));
+        a.n_out = choose_n_out(a);
+        const int grid = grid_for(a.j1 - a.j0, heat_sweep_occupancy(a));
         if (a.j1 > a.j0)
             check_launch(launch_heat_sweep(a, Lv.u.tm, Lv.g_full ? Lv.g.tm : Lv.u.tm, r.tm, grid, st_),
                          "resid");

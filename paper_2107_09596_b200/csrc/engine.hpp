@@ -162,7 +162,7 @@ private:
                        int p0, int p1, const DArr& x1, const DArr& x2, const DArr& x3,
                        const DArr& out, int out_stride, int forced, int seed_zero, int idx0,
                        int seed_off);
-    int grid_for(int jobs, bool window, size_t smem);
+    int grid_for(int jobs, int occ);
     // timing
     void phase_begin(const char* name);
     void phase_end();

@@ -6,10 +6,11 @@
 // x += theta(t) * sin(pi x).  The reference runs the Thomas recurrences
 // serially per vector; here one CTA owns one state vector (one time point)
 // in registers, in a blocked arrangement (thread t holds elements
-// [t*L, t*L+L)), and each recurrence is evaluated as
-//   local chunk recurrence  ->  warp/CTA scan of affine carries  ->  fix-up.
-// The chunk/warp carry multipliers depend only on the level's coefficients
-// and are precomputed on the host (HeatLevelHost).
+// [t*L, t*L+L)), and each first-order recurrence is evaluated as
+//   local chunk recurrence  ->  warp shuffle scan + cross-warp carry  ->
+//   fix-up with precomputed multiplier products (independent FMAs).
+// Every multiplier depends only on the level's coefficients and the CTA
+// shape, so it is precomputed once on the host (HeatLevelHost).
 #pragma once
 
 #include <cuda.h>
@@ -20,18 +21,22 @@ namespace atm {
 
 constexpr int kMaxThreads = 512;
 constexpr int kMaxWarps = kMaxThreads / 32;
+constexpr int kMaxL = 16;
 constexpr int kScanPerThread = 12;  // Mf[5], Pf_ex, Mb[5], Pb_ex
 
 // Device view of one level's Phi coefficients.
 struct HeatCoefDev {
-    const double* beta;    // [nt*L] 1/den_i   (0 beyond n)
-    const double* gamma;   // [nt*L] r/den_i   (0 beyond n)
-    const double* cneg;    // [nt*L] -c'_i     (0 beyond n)
-    const double* scan;    // [nt][12]
-    const double* warpA;   // [2][kMaxWarps] forward / backward warp products
+    const double* beta;    // [nt*L] 1/den_i        (0 beyond n)
+    const double* gamma;   // [nt*L] r/den_i        (0 beyond n)
+    const double* cneg;    // [nt*L] -c'_i          (0 beyond n and at n-1)
+    const double* pf;      // [nt*L] forward fix-up products  prod_{j=s..e} gamma_j
+    const double* pb;      // [nt*L] backward fix-up products prod_{j=e..s+L-1} cneg_j
+    const double* scan;    // [nt][12] warp-scan multipliers
+    const double* wf;      // [kMaxWarps][kMaxWarps] cross-warp carry weights (forward)
+    const double* wb;      // [kMaxWarps][kMaxWarps] (backward)
+    const double* powc;    // [2][kMaxL] fix-up products for constant-coefficient threads
     const double* theta;   // [np*S] forcing amplitude per (index, substep) or null
-    const double* prof;    // [pitch] forcing profile sin(pi x_i) or null
-    double r;              // sub_dt / h^2
+    const double* prof;    // [nt*L] forcing profile sin(pi x_i) or null
     double beta_c, gamma_c, cneg_c;  // converged coefficients (chunks >= i0)
     int i0;                // first chunk start using constants (multiple of L)
     int n, pitch, nt, L;
@@ -40,7 +45,7 @@ struct HeatCoefDev {
 
 // Host-side construction of a level's coefficients (heat1d.cpp:24-45).
 struct HeatLevelHost {
-    std::vector<double> beta, gamma, cneg, scan, warpA;
+    std::vector<double> beta, gamma, cneg, pf, pb, scan, wf, wb, powc;
     double r = 0, beta_c = 0, gamma_c = 0, cneg_c = 0;
     int i0 = 0, n = 0, pitch = 0, nt = 0, L = 0, substeps = 1;
 };
@@ -53,17 +58,18 @@ enum TailKind { TAIL_NONE = 0, TAIL_STORE = 1, TAIL_SQ = 2 };
 struct SweepArgs {
     HeatCoefDev co;
     int kind;          // SweepKind
-    int m, np;         // level CF split
+    int m, np;         // level CF split (m = 1 => every point is a job)
     int j0, j1;        // job range [j0, j1)
     int u_base;        // global index of row 0 of the u array
     int g_base;        // global index of row 0 of the g array
     int add_g;         // u_i = Phi(u_{i-1}) + g_i with g stored per point
     int forced;        // Phi includes forcing (folded manufactured)
     int store;         // store produced points (full storage)
-    int tail;          // TailKind, residual at c_{J+1}
+    int tail;          // TailKind: residual at the next C-point
     int out_base;      // global (coarse) index of row 0 of the tail target
     double* sq;        // per-point squares (TAIL_SQ), indexed by tail point - sq_base
     int sq_base;
+    int n_out;         // output staging buffers (1 or 2)
 };
 
 enum WindowKind { WK_LINEAR = 0, WK_FAS = 1, WK_FORWARD = 2, WK_APPLY = 3, WK_FAS_RHS = 4 };
@@ -82,10 +88,6 @@ struct WindowArgs {
     int seed_off;      // WK_APPLY: seed row is p + seed_off
 };
 
-struct Maps {
-    CUtensorMap a, b, c, d, e;
-};
-
 // Launchers (stream-ordered).  Return cudaError_t as int.
 int launch_heat_sweep(const SweepArgs& args, const CUtensorMap& tm_u, const CUtensorMap& tm_g,
                       const CUtensorMap& tm_out, int grid, cudaStream_t s);
@@ -94,6 +96,8 @@ int launch_heat_window(const WindowArgs& args, const CUtensorMap& tm_x1, const C
                        cudaStream_t s);
 size_t heat_sweep_smem(const SweepArgs& a);
 size_t heat_window_smem(const WindowArgs& a);
-int heat_max_ctas_per_sm(int L, int nt, size_t smem, bool window);
+// max resident CTAs per SM for the kernel that would serve these args
+int heat_sweep_occupancy(const SweepArgs& a);
+int heat_window_occupancy(const WindowArgs& a);
 
 }  // namespace atm

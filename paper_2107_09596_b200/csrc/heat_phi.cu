@@ -1,23 +1,28 @@
-// heat_kernels.cu -- Heat1D Phi chains for sm_100a.
+// heat_phi.cu -- Heat1D Phi chains for sm_100a.
 //
 // One CTA owns one state vector (a time point) in registers, blocked
 // (thread t holds elements [t*L, t*L+L)).  Rows move HBM <-> smem by TMA
 // (cp.async.bulk.tensor, 128B-swizzled so the blocked register view reads
-// and writes smem conflict-free); produced rows leave through a double-
-// buffered TMA-store staging area so stores overlap the next Phi.
+// and writes smem conflict-free); produced rows leave through TMA-store
+// staging so stores overlap the next Phi.  The kernels are persistent: each
+// CTA walks a contiguous range of jobs, so the row that closes job J (the
+// residual's C-point) is the seed of job J+1 and is loaded once.
 //
 // Reference semantics restated (file:line under /root/reference/proj):
 //   Phi / step          heat1d.cpp:47-60 (Thomas), :66-83 (sub-steps, forcing)
 //   F-relaxation        kernels.cpp:7-17      -> SW_F jobs
 //   C-relaxation        kernels.cpp:19-28     -> SW_CRELAX jobs / fused SW_FCF
 //   residual / restrict kernels.cpp:30-43, solver.cpp:174-185 -> tails, SW_RESID
-//   window solves       kernels.cpp:53-88     -> heat_window_kernel
+//   window solves       kernels.cpp:53-88     -> heat_window_*_kernel
 //   point squares       kernels.cpp:90-95     -> TAIL_SQ (fixed-order tree)
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "heat_kernels.cuh"
 #include "tma.cuh"
@@ -25,7 +30,7 @@
 namespace atm {
 
 // --------------------------------------------------------------------------
-// host: coefficients and scan multipliers
+// host: coefficients and scan / carry multipliers
 
 HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, int substeps) {
     HeatLevelHost H;
@@ -58,13 +63,11 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
         H.cneg[i] = (i == n - 1) ? 0.0 : -cpr[i];
     }
     // converged tail: the c' recurrence is a contraction; past i0 the
-    // coefficients agree with their limit to <= 2 ulp and are held in registers
-    H.i0 = n;
+    // coefficients agree with their limit to <= 2 ulp and live in registers
+    H.i0 = ((n + L - 1) / L) * L;
     if (n >= 3) {
         const double bc = beta[n - 2], cc = -cpr[n - 2];
-        auto close = [](double x, double y) {
-            return std::fabs(x - y) <= 4.5e-16 * std::fabs(y);
-        };
+        auto close = [](double x, double y) { return std::fabs(x - y) <= 4.5e-16 * std::fabs(y); };
         int last_diff = -1;
         for (int i = 0; i < n - 1; ++i)
             if (!close(beta[i], bc) || !close(-cpr[i], cc)) last_diff = i;
@@ -73,7 +76,7 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
         H.gamma_c = H.r * bc;
         H.cneg_c = cc;
     }
-    // effective per-element coefficients as the device will use them
+    // effective per-element coefficients exactly as the device uses them
     std::vector<double> eg(npad), ec(npad);
     for (int t = 0; t < nt; ++t) {
         const int s = t * L;
@@ -83,20 +86,47 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
             ec[s + e] = cst ? H.cneg_c : H.cneg[s + e];
         }
     }
-    std::vector<double> Af(nt, 1.0), Ab(nt, 1.0);
+    // per-thread fix-up products and chunk products
+    H.pf.assign(npad, 0.0);
+    H.pb.assign(npad, 0.0);
+    std::vector<double> Af(nt), Ab(nt);
     for (int t = 0; t < nt; ++t) {
-        for (int e = 0; e < L; ++e) Af[t] *= eg[t * L + e];
-        for (int e = L - 1; e >= 0; --e) Ab[t] *= ec[t * L + e];
+        double p = 1.0;
+        for (int e = 0; e < L; ++e) {
+            p *= eg[t * L + e];
+            H.pf[t * L + e] = p;
+        }
+        Af[t] = p;
+        p = 1.0;
+        for (int e = L - 1; e >= 0; --e) {
+            p *= ec[t * L + e];
+            H.pb[t * L + e] = p;
+        }
+        Ab[t] = p;
     }
+    H.powc.assign(2 * kMaxL, 0.0);
+    {
+        double p = 1.0;
+        for (int e = 0; e < L; ++e) {
+            p *= H.gamma_c;
+            H.powc[e] = p;
+        }
+        p = 1.0;
+        for (int e = L - 1; e >= 0; --e) {
+            p *= H.cneg_c;
+            H.powc[kMaxL + e] = p;
+        }
+    }
+    // warp scan multipliers (Hillis-Steele over lanes) and warp products
     H.scan.assign(static_cast<size_t>(nt) * kScanPerThread, 0.0);
-    H.warpA.assign(2 * kMaxWarps, 0.0);
     const int nw = nt / 32;
+    std::vector<double> AWf(nw), AWb(nw);
     for (int w = 0; w < nw; ++w) {
         double pf = 1.0, pb = 1.0;
         for (int l = 0; l < 32; ++l) pf *= Af[32 * w + l];
         for (int l = 31; l >= 0; --l) pb *= Ab[32 * w + l];
-        H.warpA[w] = pf;
-        H.warpA[kMaxWarps + w] = pb;
+        AWf[w] = pf;
+        AWb[w] = pb;
         for (int l = 0; l < 32; ++l) {
             double* sc = &H.scan[static_cast<size_t>(32 * w + l) * kScanPerThread];
             for (int d = 0; d < 5; ++d) {
@@ -121,11 +151,26 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
             sc[11] = exb;
         }
     }
+    // cross-warp carry weights: carry_w = sum_{v<w} (prod_{u=v+1}^{w-1} AWf_u) T_v
+    H.wf.assign(kMaxWarps * kMaxWarps, 0.0);
+    H.wb.assign(kMaxWarps * kMaxWarps, 0.0);
+    for (int w = 0; w < nw; ++w) {
+        for (int v = 0; v < w; ++v) {
+            double p = 1.0;
+            for (int u = v + 1; u <= w - 1; ++u) p *= AWf[u];
+            H.wf[w * kMaxWarps + v] = p;
+        }
+        for (int v = w + 1; v < nw; ++v) {
+            double p = 1.0;
+            for (int u = w + 1; u <= v - 1; ++u) p *= AWb[u];
+            H.wb[w * kMaxWarps + v] = p;
+        }
+    }
     return H;
 }
 
 // --------------------------------------------------------------------------
-// device: per-thread state and the tridiagonal solve
+// device: per-thread state, shared tables and the tridiagonal solve
 
 template <int L>
 struct Lane {
@@ -152,34 +197,46 @@ __device__ __forceinline__ void lane_init(Lane<L>& ln, const HeatCoefDev& co) {
     ln.Pbex = __ldg(sc + 11);
 }
 
-struct Slots {            // small shared scratch
+struct Tabs {              // per-CTA copy of the level's small tables
+    double wf[kMaxWarps * kMaxWarps];
+    double wb[kMaxWarps * kMaxWarps];
+    double powc[2 * kMaxL];
+};
+
+struct Slots {             // small shared scratch
     double swf[kMaxWarps];
     double swb[kMaxWarps];
-    double wAf[kMaxWarps];
-    double wAb[kMaxWarps];
     double red[kMaxWarps];
     uint64_t bar[4];
 };
 
+__device__ __forceinline__ void tabs_init(Tabs& tb, const HeatCoefDev& co) {
+    for (int i = threadIdx.x; i < kMaxWarps * kMaxWarps; i += blockDim.x) {
+        tb.wf[i] = co.wf[i];
+        tb.wb[i] = co.wb[i];
+    }
+    for (int i = threadIdx.x; i < 2 * kMaxL; i += blockDim.x) tb.powc[i] = co.powc[i];
+}
+
 // (I + sub_dt L) x = x, in place, over the CTA (heat1d.cpp:47-60).
 template <int L>
 __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
-                                          const Lane<L>& ln, Slots& sl) {
-    const double r = co.r;
-    // forward: y_i = (x_i + r y_{i-1}) / den_i, local with zero carry-in
+                                          const Lane<L>& ln, const Tabs& tb, Slots& sl) {
+    // forward  y_i = beta_i x_i + gamma_i y_{i-1}   (local: zero carry-in)
     double y = 0.0;
     if (ln.cst) {
-        const double b = co.beta_c;
+        const double bb = co.beta_c, gg = co.gamma_c;
 #pragma unroll
         for (int e = 0; e < L; ++e) {
-            y = fma(r, y, x[e]) * b;
+            y = fma(gg, y, bb * x[e]);
             x[e] = y;
         }
     } else {
         const double* bt = co.beta + ln.s;
+        const double* gt = co.gamma + ln.s;
 #pragma unroll
         for (int e = 0; e < L; ++e) {
-            y = fma(r, y, x[e]) * __ldg(bt + e);
+            y = fma(__ldg(gt + e), y, __ldg(bt + e) * x[e]);
             x[e] = y;
         }
     }
@@ -193,31 +250,32 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     if (ln.lane == 0) ex = 0.0;
     if (ln.lane == 31) sl.swf[ln.warp] = B;
     __syncthreads();
-    double cw = 0.0;
-    for (int v = 0; v < ln.warp; ++v) cw = fma(sl.wAf[v], cw, sl.swf[v]);
-    double p = fma(ln.Pfex, cw, ex);
-    if (ln.cst) {
-        const double g = co.gamma_c;
-#pragma unroll
-        for (int e = 0; e < L; ++e) {
-            p *= g;
-            x[e] += p;
+    {
+        const double* wr = tb.wf + ln.warp * kMaxWarps;
+        double c0 = 0.0, c1 = 0.0;
+        int v = 0;
+        for (; v + 1 < ln.warp; v += 2) {
+            c0 = fma(wr[v], sl.swf[v], c0);
+            c1 = fma(wr[v + 1], sl.swf[v + 1], c1);
         }
-    } else {
-        const double* gt = co.gamma + ln.s;
+        if (v < ln.warp) c0 = fma(wr[v], sl.swf[v], c0);
+        const double carry = fma(ln.Pfex, c0 + c1, ex);
+        if (ln.cst) {
 #pragma unroll
-        for (int e = 0; e < L; ++e) {
-            p *= __ldg(gt + e);
-            x[e] += p;
+            for (int e = 0; e < L; ++e) x[e] = fma(carry, tb.powc[e], x[e]);
+        } else {
+            const double* pt = co.pf + ln.s;
+#pragma unroll
+            for (int e = 0; e < L; ++e) x[e] = fma(carry, __ldg(pt + e), x[e]);
         }
     }
-    // backward: x_i = y_i - c'_i x_{i+1}, local with zero carry-in
+    // backward  x_i = y_i - c'_i x_{i+1}   (local: zero carry-in)
     double z = 0.0;
     if (ln.cst) {
-        const double c = co.cneg_c;
+        const double cc = co.cneg_c;
 #pragma unroll
         for (int e = L - 1; e >= 0; --e) {
-            z = fma(c, z, x[e]);
+            z = fma(cc, z, x[e]);
             x[e] = z;
         }
     } else {
@@ -238,22 +296,23 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     if (ln.lane == 31) ex = 0.0;
     if (ln.lane == 0) sl.swb[ln.warp] = B;
     __syncthreads();
-    cw = 0.0;
-    for (int v = ln.nw - 1; v > ln.warp; --v) cw = fma(sl.wAb[v], cw, sl.swb[v]);
-    p = fma(ln.Pbex, cw, ex);
-    if (ln.cst) {
-        const double c = co.cneg_c;
-#pragma unroll
-        for (int e = L - 1; e >= 0; --e) {
-            p *= c;
-            x[e] += p;
+    {
+        const double* wr = tb.wb + ln.warp * kMaxWarps;
+        double c0 = 0.0, c1 = 0.0;
+        int v = ln.warp + 1;
+        for (; v + 1 < ln.nw; v += 2) {
+            c0 = fma(wr[v], sl.swb[v], c0);
+            c1 = fma(wr[v + 1], sl.swb[v + 1], c1);
         }
-    } else {
-        const double* ct = co.cneg + ln.s;
+        if (v < ln.nw) c0 = fma(wr[v], sl.swb[v], c0);
+        const double carry = fma(ln.Pbex, c0 + c1, ex);
+        if (ln.cst) {
 #pragma unroll
-        for (int e = L - 1; e >= 0; --e) {
-            p *= __ldg(ct + e);
-            x[e] += p;
+            for (int e = 0; e < L; ++e) x[e] = fma(carry, tb.powc[kMaxL + e], x[e]);
+        } else {
+            const double* pt = co.pb + ln.s;
+#pragma unroll
+            for (int e = 0; e < L; ++e) x[e] = fma(carry, __ldg(pt + e), x[e]);
         }
     }
 }
@@ -262,14 +321,14 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
 // when `forced` (heat1d.cpp:66-83).
 template <int L>
 __device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, const Lane<L>& ln,
-                                    Slots& sl, int index, int forced) {
+                                    const Tabs& tb, Slots& sl, int index, int forced) {
     for (int s = 0; s < co.substeps; ++s) {
         if (forced) {
             const double th = __ldg(co.theta + static_cast<size_t>(index) * co.substeps + s);
 #pragma unroll
             for (int e = 0; e < L; ++e) x[e] = fma(th, __ldg(co.prof + ln.s + e), x[e]);
         }
-        tri_solve<L>(x, co, ln, sl);
+        tri_solve<L>(x, co, ln, tb, sl);
     }
 }
 
@@ -306,7 +365,7 @@ __device__ __forceinline__ void row_store(char* buf, const double (&x)[L], int s
     }
 }
 
-// x = x + row  (sign = +1) or x = x - row (sign = -1)
+// x = x + row, or x = x - row
 template <int L>
 __device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], int s, int pitch,
                                         bool sub) {
@@ -326,7 +385,8 @@ __device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], int s, 
     }
 }
 
-// y = row + x (row first operand, matches u.add(e) ordering is commutative anyway)
+// fixed-order CTA reduction of sum x_e^2 (thread order, then warp xor tree,
+// then warps in order): depends only on the CTA shape
 template <int L>
 __device__ __forceinline__ double cta_sum_squares(const double (&x)[L], const Lane<L>& ln,
                                                   Slots& sl) {
@@ -350,9 +410,10 @@ __host__ __device__ inline int row_bytes_al(int pitch) { return ((pitch * 8) + 1
 
 // --------------------------------------------------------------------------
 // sweep kernel: F / fused FCF / C-relax / residual jobs over C-point indices
+// smem: [S seed/tail][O0][O1 if n_out=2][A if add_g][Tabs][Slots]
 
-template <int L>
-__global__ void __launch_bounds__(kMaxThreads)
+template <int L, int NTMAX, int MINB>
+__global__ void __launch_bounds__(NTMAX, MINB)
     heat_sweep_kernel(const __grid_constant__ SweepArgs a, const __grid_constant__ CUtensorMap tm_u,
                       const __grid_constant__ CUtensorMap tm_g,
                       const __grid_constant__ CUtensorMap tm_out) {
@@ -360,10 +421,13 @@ __global__ void __launch_bounds__(kMaxThreads)
     char* base = align1k(smem_raw);
     const int pitch = a.co.pitch;
     const int rb = row_bytes_al(pitch);
-    char* bufO[2] = {base, base + rb};
-    char* bufS = base + 2 * rb;
-    char* bufA = base + 3 * rb;
-    Slots& sl = *reinterpret_cast<Slots*>(base + (a.add_g ? 4 : 3) * rb);
+    const int nob = a.n_out;
+    char* bufS = base;
+    char* bufO[2] = {base + rb, base + (nob == 2 ? 2 : 1) * rb};
+    char* bufA = base + (1 + nob) * rb;
+    char* tl = base + (1 + nob + (a.add_g ? 1 : 0)) * rb;
+    Tabs& tb = *reinterpret_cast<Tabs*>(tl);
+    Slots& sl = *reinterpret_cast<Slots*>(tl + sizeof(Tabs));
     uint64_t* barS = &sl.bar[0];
     uint64_t* barA = &sl.bar[1];
     const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
@@ -372,10 +436,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     Lane<L> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
-    if (t < ln.nw) {
-        sl.wAf[t] = a.co.warpA[t];
-        sl.wAb[t] = a.co.warpA[kMaxWarps + t];
-    }
+    tabs_init(tb, a.co);
     if (t == 0) {
         mbar_init(barS, 1);
         mbar_init(barA, 1);
@@ -392,6 +453,20 @@ __global__ void __launch_bounds__(kMaxThreads)
     const int m = a.m, last = a.np - 1;
     bool seed_ready = false;
     double x[L];
+
+    // stage x into an output buffer and TMA-store it; the store that last
+    // read that buffer was waited for (bulk_wait_read) before the Phi
+    auto stage_out = [&](int row, const CUtensorMap* map) {
+        char* o = bufO[ob];
+        row_store<L>(o, x, ln.s, pitch);
+        fence_proxy_async();
+        __syncthreads();
+        if (t == 0) {
+            tma_store_2d(map, 0, row * R, o);
+            bulk_commit();
+        }
+        ob = (nob == 2) ? ob ^ 1 : 0;
+    };
 
     for (int J = jb; J < je; ++J) {
         const int c = J * m;
@@ -432,6 +507,9 @@ __global__ void __launch_bounds__(kMaxThreads)
             phS ^= 1;
         }
         row_load<L>(bufS, x, ln.s, pitch);
+        // WAR across proxies: our generic reads of S must be ordered before
+        // the TMA (async proxy) write that refills it
+        fence_proxy_async();
         __syncthreads();
         seed_ready = false;
         if (tail_i >= 0 && t == 0) {
@@ -445,24 +523,20 @@ __global__ void __launch_bounds__(kMaxThreads)
                 mbar_expect_tx(barA, bytes);
                 tma_load_2d(bufA, &tm_g, 0, (i - a.g_base) * R, barA);
             }
-            if (t == 0) bulk_wait_read<1>();
-            phi<L>(x, a.co, ln, sl, i, a.forced);
+            if (t == 0) {
+                if (nob == 2) bulk_wait_read<1>();
+                else bulk_wait_read<0>();
+            }
+            phi<L>(x, a.co, ln, tb, sl, i, a.forced);
             if (a.add_g) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
                 row_acc<L>(bufA, x, ln.s, pitch, false);
             }
             if (a.store && i >= store_from) {
-                char* o = bufO[ob];
-                row_store<L>(o, x, ln.s, pitch);
-                fence_proxy_async();
-                __syncthreads();
-                if (t == 0) {
-                    tma_store_2d(&tm_u, 0, (i - a.u_base) * R, o);
-                    bulk_commit();
-                }
-                ob ^= 1;
+                stage_out(i - a.u_base, &tm_u);
             } else if (a.add_g) {
+                fence_proxy_async();
                 __syncthreads();  // bufA consumed before the next load
             }
         }
@@ -473,8 +547,11 @@ __global__ void __launch_bounds__(kMaxThreads)
                 mbar_expect_tx(barA, bytes);
                 tma_load_2d(bufA, &tm_g, 0, (tail_i - a.g_base) * R, barA);
             }
-            if (t == 0) bulk_wait_read<1>();
-            phi<L>(x, a.co, ln, sl, tail_i, a.forced);
+            if (t == 0) {
+                if (nob == 2) bulk_wait_read<1>();
+                else bulk_wait_read<0>();
+            }
+            phi<L>(x, a.co, ln, tb, sl, tail_i, a.forced);
             if (a.add_g) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
@@ -484,17 +561,8 @@ __global__ void __launch_bounds__(kMaxThreads)
             phS ^= 1;
             row_acc<L>(bufS, x, ln.s, pitch, true);
             if (a.kind == SW_F && J + 1 < je) seed_ready = true;  // S holds u[c_{J+1}]
-            const int ci = tail_i / m;
             if (a.tail == TAIL_STORE) {
-                char* o = bufO[ob];
-                row_store<L>(o, x, ln.s, pitch);
-                fence_proxy_async();
-                __syncthreads();
-                if (t == 0) {
-                    tma_store_2d(&tm_out, 0, (ci - a.out_base) * R, o);
-                    bulk_commit();
-                }
-                ob ^= 1;
+                stage_out(tail_i / m - a.out_base, &tm_out);
             } else {
                 const double tot = cta_sum_squares<L>(x, ln, sl);
                 if (t == 0) a.sq[tail_i - a.sq_base] = tot;
@@ -505,11 +573,142 @@ __global__ void __launch_bounds__(kMaxThreads)
 }
 
 // --------------------------------------------------------------------------
-// window kernel: truncated local coarse grids (kernels.cpp:53-88) and
-// batched single-step applications
+// linear window kernel (kernels.cpp:53-61 + solver.cpp:271-278):
+// e = r_lo, e = Psi_s(e) + r_s, fine u[c_p] += e.  The r rows of every job of
+// the CTA form one stream, double-buffered two rows ahead; the fine C-point
+// row is fetched into S ahead of its emit, updated in place and stored back.
+// smem: [A0][A1][S][Tabs][Slots]
 
-template <int L>
-__global__ void __launch_bounds__(kMaxThreads)
+template <int L, int NTMAX, int MINB>
+__global__ void __launch_bounds__(NTMAX, MINB)
+    heat_window_linear_kernel(const __grid_constant__ WindowArgs a,
+                              const __grid_constant__ CUtensorMap tm_r,
+                              const __grid_constant__ CUtensorMap tm_fine) {
+    extern __shared__ unsigned char smem_raw[];
+    char* base = align1k(smem_raw);
+    const int pitch = a.co.pitch;
+    const int rb = row_bytes_al(pitch);
+    char* bufA[2] = {base, base + rb};
+    char* bufS = base + 2 * rb;
+    Tabs& tb = *reinterpret_cast<Tabs*>(base + 3 * rb);
+    Slots& sl = *reinterpret_cast<Slots*>(base + 3 * rb + sizeof(Tabs));
+    uint64_t* barA = &sl.bar[0];  // two barriers: bar[0], bar[1]
+    uint64_t* barS = &sl.bar[2];
+    const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
+    const int R = pitch >> 4;
+
+    Lane<L> ln;
+    lane_init<L>(ln, a.co);
+    const int t = ln.t;
+    tabs_init(tb, a.co);
+    if (t == 0) {
+        mbar_init(&barA[0], 1);
+        mbar_init(&barA[1], 1);
+        mbar_init(barS, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    uint32_t phA[2] = {0, 0}, phS = 0;
+
+    const bool has_pre = a.pre_e1 >= a.pre_e0;
+    const int n_ind = max(0, a.p1 - a.p0 + 1);
+    const long long Nj = (has_pre ? 1 : 0) + n_ind;
+    const int jb = static_cast<int>(Nj * blockIdx.x / gridDim.x);
+    const int je = static_cast<int>(Nj * (blockIdx.x + 1) / gridDim.x);
+    if (jb >= je) return;
+
+    auto job_range = [&](int q, int& lo, int& e0, int& e1) {
+        if (has_pre && q == 0) {
+            lo = a.pre_lo;
+            e0 = a.pre_e0;
+            e1 = a.pre_e1;
+        } else {
+            const int p = a.p0 + q - (has_pre ? 1 : 0);
+            lo = max(0, p - a.k + 1);
+            e0 = e1 = p;
+        }
+    };
+    // issue stream: (iq, is_) = next r row to load
+    int iq = jb, is_, ilo, ie0, ie1;
+    job_range(iq, ilo, ie0, ie1);
+    is_ = ilo;
+    auto issue_next = [&](int buf) {  // thread 0 only
+        if (iq >= je) return;
+        mbar_expect_tx(&barA[buf], bytes);
+        tma_load_2d(bufA[buf], &tm_r, 0, (is_ - a.x1_base) * R, &barA[buf]);
+        if (++is_ > ie1) {
+            if (++iq < je) {
+                job_range(iq, ilo, ie0, ie1);
+                is_ = ilo;
+            }
+        }
+    };
+    if (t == 0) {
+        issue_next(0);
+        issue_next(1);
+    }
+    int cb = 0;  // buffer of the next row to consume
+    double x[L];
+    auto consume = [&](bool add) {
+        mbar_wait(&barA[cb], phA[cb]);
+        phA[cb] ^= 1;
+        if (add) row_acc<L>(bufA[cb], x, ln.s, pitch, false);
+        else row_load<L>(bufA[cb], x, ln.s, pitch);
+        fence_proxy_async();  // generic reads before the TMA refill (WAR)
+        __syncthreads();
+        if (t == 0) issue_next(cb);
+        cb ^= 1;
+    };
+
+    for (int q = jb; q < je; ++q) {
+        int lo, e0, e1;
+        job_range(q, lo, e0, e1);
+        consume(false);  // e = r_lo
+        if (t == 0) {
+            bulk_wait_read<0>();  // S free again
+            mbar_expect_tx(barS, bytes);
+            tma_load_2d(bufS, &tm_fine, 0, (max(e0, lo) * a.out_stride - a.out_base) * R, barS);
+        }
+        for (int s = lo; s <= e1; ++s) {
+            if (s > lo) {
+                phi<L>(x, a.co, ln, tb, sl, s, a.forced);
+                consume(true);  // e = Psi(e) + r_s
+            }
+            if (s >= e0) {
+                // fine.u[c_s] += e
+                mbar_wait(barS, phS);
+                phS ^= 1;
+                double y[L];
+                row_load<L>(bufS, y, ln.s, pitch);
+#pragma unroll
+                for (int e = 0; e < L; ++e) y[e] += x[e];
+                row_store<L>(bufS, y, ln.s, pitch);
+                fence_proxy_async();
+                __syncthreads();
+                if (t == 0) {
+                    tma_store_2d(&tm_fine, 0, (s * a.out_stride - a.out_base) * R, bufS);
+                    bulk_commit();
+                    if (s + 1 <= e1) {
+                        bulk_wait_read<0>();
+                        mbar_expect_tx(barS, bytes);
+                        tma_load_2d(bufS, &tm_fine, 0, ((s + 1) * a.out_stride - a.out_base) * R,
+                                    barS);
+                    }
+                }
+            }
+        }
+    }
+    if (t == 0) bulk_wait<0>();
+}
+
+// --------------------------------------------------------------------------
+// generic window kernel: FAS windows (kernels.cpp:63-77), nested forward
+// windows (kernels.cpp:79-88), batched single-step applications (Phi of
+// given rows, forcing, Psi(v_{j-1})) and the FAS coarse right-hand side
+// (solver.cpp:214-218).  smem: [O0][O1][A1][A2][A3][Tabs][Slots]
+
+template <int L, int NTMAX, int MINB>
+__global__ void __launch_bounds__(NTMAX, MINB)
     heat_window_kernel(const __grid_constant__ WindowArgs a,
                        const __grid_constant__ CUtensorMap tm_x1,
                        const __grid_constant__ CUtensorMap tm_x2,
@@ -520,13 +719,13 @@ __global__ void __launch_bounds__(kMaxThreads)
     const int pitch = a.co.pitch;
     const int rb = row_bytes_al(pitch);
     char* bufO[2] = {base, base + rb};
-    char* bufS = base + 2 * rb;
-    char* bufA1 = base + 3 * rb;
-    char* bufA2 = base + 4 * rb;
-    char* bufA3 = base + 5 * rb;
+    char* bufA1 = base + 2 * rb;
+    char* bufA2 = base + 3 * rb;
+    char* bufA3 = base + 4 * rb;
     const bool three = (a.kind == WK_FAS || a.kind == WK_FAS_RHS);
-    Slots& sl = *reinterpret_cast<Slots*>(base + (three ? 6 : 4) * rb);
-    uint64_t* barS = &sl.bar[0];
+    char* tl = base + (three ? 5 : 3) * rb;
+    Tabs& tb = *reinterpret_cast<Tabs*>(tl);
+    Slots& sl = *reinterpret_cast<Slots*>(tl + sizeof(Tabs));
     uint64_t* barA = &sl.bar[1];
     const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
     const int R = pitch >> 4;
@@ -534,20 +733,16 @@ __global__ void __launch_bounds__(kMaxThreads)
     Lane<L> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
-    if (t < ln.nw) {
-        sl.wAf[t] = a.co.warpA[t];
-        sl.wAb[t] = a.co.warpA[kMaxWarps + t];
-    }
+    tabs_init(tb, a.co);
     if (t == 0) {
-        mbar_init(barS, 1);
         mbar_init(barA, 1);
         mbar_fence_init();
     }
     __syncthreads();
-    uint32_t phS = 0, phA = 0;
+    uint32_t phA = 0;
     int ob = 0;
 
-    const bool has_pre = (a.kind <= WK_FORWARD) && (a.pre_e1 >= a.pre_e0);
+    const bool has_pre = (a.kind == WK_FAS || a.kind == WK_FORWARD) && (a.pre_e1 >= a.pre_e0);
     const int n_ind = max(0, a.p1 - a.p0 + 1);
     const long long Nj = (has_pre ? 1 : 0) + n_ind;
     const int jb = static_cast<int>(Nj * blockIdx.x / gridDim.x);
@@ -570,18 +765,17 @@ __global__ void __launch_bounds__(kMaxThreads)
         if (a.kind == WK_APPLY || a.kind == WK_FAS_RHS) {
             const int p = a.p0 + q;
             const int src = (a.kind == WK_FAS_RHS) ? p - 1 : p + a.seed_off;
-            if (t == 0) {
-                const uint32_t nb = a.seed_zero ? 0u : bytes;
-                const uint32_t extra = (a.kind == WK_FAS_RHS) ? 2 * bytes : 0u;
-                if (nb + extra) mbar_expect_tx(barA, nb + extra);
+            const uint32_t nb = a.seed_zero ? 0u : bytes;
+            const uint32_t extra = (a.kind == WK_FAS_RHS) ? 2 * bytes : 0u;
+            if (t == 0 && nb + extra) {
+                mbar_expect_tx(barA, nb + extra);
                 if (!a.seed_zero) tma_load_2d(bufA1, &tm_x1, 0, (src - a.x1_base) * R, barA);
                 if (a.kind == WK_FAS_RHS) {
                     tma_load_2d(bufA2, &tm_x2, 0, (p - a.x2_base) * R, barA);
                     tma_load_2d(bufA3, &tm_x3, 0, (p - a.x3_base) * R, barA);
                 }
             }
-            const bool waited = !(a.seed_zero && a.kind == WK_APPLY);
-            if (waited) {
+            if (nb + extra) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
             }
@@ -592,7 +786,7 @@ __global__ void __launch_bounds__(kMaxThreads)
                 row_load<L>(bufA1, x, ln.s, pitch);
             }
             if (t == 0) bulk_wait_read<1>();
-            phi<L>(x, a.co, ln, sl, a.idx0 + p, a.forced);
+            phi<L>(x, a.co, ln, tb, sl, a.idx0 + p, a.forced);
             if (a.kind == WK_FAS_RHS) {
                 // g_j = (v_j - Psi_j(v_{j-1})) + r_j  (solver.cpp:214-218)
                 double y[L];
@@ -617,81 +811,44 @@ __global__ void __launch_bounds__(kMaxThreads)
             lo = max(0, p - a.k + 1);
             e0 = e1 = p;
         }
-        // ---- seed: r_lo (linear), v_lo + r_lo (FAS), u_lo (forward)
+        // ---- seed: v_lo + r_lo (FAS), u_lo (forward)
+        const bool fas = (a.kind == WK_FAS);
         if (t == 0) {
-            const bool fas = (a.kind == WK_FAS);
             mbar_expect_tx(barA, fas ? 2 * bytes : bytes);
             tma_load_2d(bufA1, &tm_x1, 0, (lo - a.x1_base) * R, barA);
             if (fas) tma_load_2d(bufA2, &tm_x2, 0, (lo - a.x2_base) * R, barA);
         }
         mbar_wait(barA, phA);
         phA ^= 1;
-        if (a.kind == WK_FAS) {
-            row_load<L>(bufA2, x, ln.s, pitch);   // v_lo
+        if (fas) {
+            row_load<L>(bufA2, x, ln.s, pitch);        // v_lo
             row_acc<L>(bufA1, x, ln.s, pitch, false);  // + r_lo
         } else {
             row_load<L>(bufA1, x, ln.s, pitch);
         }
+        fence_proxy_async();
         __syncthreads();
-        int next_emit = max(e0, lo);
-        if (a.kind == WK_LINEAR && t == 0) {
-            mbar_expect_tx(barS, bytes);
-            tma_load_2d(bufS, &tm_out, 0, (next_emit * a.out_stride - a.out_base) * R, barS);
-        }
-        auto emit = [&](int p) {
-            if (a.kind == WK_LINEAR) {
-                // fine.u[c_p] += e  (solver.cpp:277)
-                mbar_wait(barS, phS);
-                phS ^= 1;
-                double y[L];
-                row_load<L>(bufS, y, ln.s, pitch);
-#pragma unroll
-                for (int e = 0; e < L; ++e) y[e] += x[e];
-                char* o = bufO[ob];
-                row_store<L>(o, y, ln.s, pitch);
-                fence_proxy_async();
-                __syncthreads();
-                if (t == 0) {
-                    tma_store_2d(&tm_out, 0, (p * a.out_stride - a.out_base) * R, o);
-                    bulk_commit();
-                    if (p + 1 <= e1) {
-                        mbar_expect_tx(barS, bytes);
-                        tma_load_2d(bufS, &tm_out, 0, ((p + 1) * a.out_stride - a.out_base) * R,
-                                    barS);
-                    }
-                }
-                ob ^= 1;
-            } else {
-                emit_store(p);
-            }
-        };
-        if (lo >= e0) emit(lo);
+        if (lo >= e0) emit_store(lo);
         for (int s = lo + 1; s <= e1; ++s) {
-            if (t == 0 && a.kind != WK_FORWARD) {
-                const bool fas = (a.kind == WK_FAS);
-                mbar_expect_tx(barA, fas ? 3 * bytes : bytes);
+            if (t == 0 && fas) {
+                mbar_expect_tx(barA, 3 * bytes);
                 tma_load_2d(bufA1, &tm_x1, 0, (s - a.x1_base) * R, barA);
-                if (fas) {
-                    tma_load_2d(bufA2, &tm_x2, 0, (s - a.x2_base) * R, barA);
-                    tma_load_2d(bufA3, &tm_x3, 0, (s - a.x3_base) * R, barA);
-                }
+                tma_load_2d(bufA2, &tm_x2, 0, (s - a.x2_base) * R, barA);
+                tma_load_2d(bufA3, &tm_x3, 0, (s - a.x3_base) * R, barA);
             }
             if (t == 0) bulk_wait_read<1>();
-            phi<L>(x, a.co, ln, sl, s, a.forced);
-            if (a.kind != WK_FORWARD) {
+            phi<L>(x, a.co, ln, tb, sl, s, a.forced);
+            if (fas) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
-                if (a.kind == WK_FAS) {
-                    // next = Psi(u) + v_s - Psi(v_{s-1}) + r_s  (kernels.cpp:69-74)
-                    row_acc<L>(bufA2, x, ln.s, pitch, false);
-                    row_acc<L>(bufA3, x, ln.s, pitch, true);
-                    row_acc<L>(bufA1, x, ln.s, pitch, false);
-                } else {
-                    row_acc<L>(bufA1, x, ln.s, pitch, false);  // e = Psi(e) + r_s
-                }
+                // next = Psi(u) + v_s - Psi(v_{s-1}) + r_s  (kernels.cpp:69-74)
+                row_acc<L>(bufA2, x, ln.s, pitch, false);
+                row_acc<L>(bufA3, x, ln.s, pitch, true);
+                row_acc<L>(bufA1, x, ln.s, pitch, false);
+                fence_proxy_async();
                 __syncthreads();
             }
-            if (s >= e0) emit(s);
+            if (s >= e0) emit_store(s);
         }
     }
     if (t == 0) bulk_wait<0>();
@@ -701,69 +858,106 @@ __global__ void __launch_bounds__(kMaxThreads)
 // host launchers
 
 size_t heat_sweep_smem(const SweepArgs& a) {
-    return 1024 + static_cast<size_t>(a.add_g ? 4 : 3) * row_bytes_al(a.co.pitch) + sizeof(Slots);
+    const int rows = 1 + a.n_out + (a.add_g ? 1 : 0);
+    return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) + sizeof(Slots);
 }
 
 size_t heat_window_smem(const WindowArgs& a) {
-    const bool three = (a.kind == WK_FAS || a.kind == WK_FAS_RHS);
-    return 1024 + static_cast<size_t>(three ? 6 : 4) * row_bytes_al(a.co.pitch) + sizeof(Slots);
+    int rows;
+    if (a.kind == WK_LINEAR) rows = 3;
+    else rows = (a.kind == WK_FAS || a.kind == WK_FAS_RHS) ? 5 : 3;
+    size_t pad = 0;
+    if (const char* e = std::getenv("ATM_WIN_PAD")) pad = static_cast<size_t>(std::atoi(e)) * 1024;
+    return pad + 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) + sizeof(Slots);
 }
 
-template <int L>
-static int launch_sweep_L(const SweepArgs& a, const CUtensorMap& u, const CUtensorMap& g,
-                          const CUtensorMap& o, int grid, cudaStream_t s) {
-    const size_t smem = heat_sweep_smem(a);
-    cudaFuncSetAttribute(heat_sweep_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    heat_sweep_kernel<L><<<grid, a.co.nt, smem, s>>>(a, u, g, o);
-    return static_cast<int>(cudaGetLastError());
+namespace {
+
+struct KernelPtrs {
+    const void* sweep;
+    const void* wlin;
+    const void* win;
+};
+
+template <int L, int NT, int MB>
+KernelPtrs kptrs() {
+    return {reinterpret_cast<const void*>(heat_sweep_kernel<L, NT, MB>),
+            reinterpret_cast<const void*>(heat_window_linear_kernel<L, NT, MB>),
+            reinterpret_cast<const void*>(heat_window_kernel<L, NT, MB>)};
 }
 
-template <int L>
-static int launch_window_L(const WindowArgs& a, const CUtensorMap& x1, const CUtensorMap& x2,
-                           const CUtensorMap& x3, const CUtensorMap& o, int grid, cudaStream_t s) {
-    const size_t smem = heat_window_smem(a);
-    cudaFuncSetAttribute(heat_window_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    heat_window_kernel<L><<<grid, a.co.nt, smem, s>>>(a, x1, x2, x3, o);
-    return static_cast<int>(cudaGetLastError());
+// L=16 serves 2048 < n <= 4096 with 256 threads; smaller L use up to 512
+KernelPtrs select(int L) {
+    switch (L) {
+        case 2: return kptrs<2, 512, 1>();
+        case 4: return kptrs<4, 512, 1>();
+        case 8: return kptrs<8, 512, 1>();
+        default: return kptrs<16, 256, 2>();
+    }
+}
+
+void prepare(const void* fn) {
+    static std::mutex mu;
+    static std::map<const void*, bool> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[fn]) return;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    done[fn] = true;
+}
+
+int occupancy(const void* fn, int nt, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t>, int> cache;
+    prepare(fn);
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(fn, nt, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, nt, smem) != cudaSuccess) n = 1;
+    n = std::max(1, n);
+    cache[key] = n;
+    return n;
+}
+
+int launch(const void* fn, int grid, int nt, size_t smem, cudaStream_t s, void** args) {
+    prepare(fn);
+    return static_cast<int>(cudaLaunchKernel(fn, dim3(grid), dim3(nt), args, smem, s));
+}
+
+}  // namespace
+
+int heat_sweep_occupancy(const SweepArgs& a) {
+    return occupancy(select(a.co.L).sweep, a.co.nt, heat_sweep_smem(a));
+}
+
+int heat_window_occupancy(const WindowArgs& a) {
+    const KernelPtrs k = select(a.co.L);
+    return occupancy(a.kind == WK_LINEAR ? k.wlin : k.win, a.co.nt, heat_window_smem(a));
 }
 
 int launch_heat_sweep(const SweepArgs& a, const CUtensorMap& u, const CUtensorMap& g,
                       const CUtensorMap& o, int grid, cudaStream_t s) {
-    switch (a.co.L) {
-        case 2: return launch_sweep_L<2>(a, u, g, o, grid, s);
-        case 4: return launch_sweep_L<4>(a, u, g, o, grid, s);
-        case 8: return launch_sweep_L<8>(a, u, g, o, grid, s);
-        case 16: return launch_sweep_L<16>(a, u, g, o, grid, s);
-    }
-    return static_cast<int>(cudaErrorInvalidValue);
+    if (grid <= 0) return 0;
+    SweepArgs aa = a;
+    CUtensorMap tu = u, tg = g, to = o;
+    void* args[] = {&aa, &tu, &tg, &to};
+    return launch(select(a.co.L).sweep, grid, a.co.nt, heat_sweep_smem(a), s, args);
 }
 
 int launch_heat_window(const WindowArgs& a, const CUtensorMap& x1, const CUtensorMap& x2,
                        const CUtensorMap& x3, const CUtensorMap& o, int grid, cudaStream_t s) {
-    switch (a.co.L) {
-        case 2: return launch_window_L<2>(a, x1, x2, x3, o, grid, s);
-        case 4: return launch_window_L<4>(a, x1, x2, x3, o, grid, s);
-        case 8: return launch_window_L<8>(a, x1, x2, x3, o, grid, s);
-        case 16: return launch_window_L<16>(a, x1, x2, x3, o, grid, s);
+    if (grid <= 0) return 0;
+    WindowArgs aa = a;
+    CUtensorMap t1 = x1, t2 = x2, t3 = x3, to = o;
+    const KernelPtrs k = select(a.co.L);
+    if (a.kind == WK_LINEAR) {
+        void* args[] = {&aa, &t1, &to};
+        return launch(k.wlin, grid, a.co.nt, heat_window_smem(a), s, args);
     }
-    return static_cast<int>(cudaErrorInvalidValue);
-}
-
-int heat_max_ctas_per_sm(int L, int nt, size_t smem, bool window) {
-    int n = 0;
-    const void* fn = nullptr;
-    switch (L) {
-        case 2: fn = window ? (const void*)heat_window_kernel<2> : (const void*)heat_sweep_kernel<2>; break;
-        case 4: fn = window ? (const void*)heat_window_kernel<4> : (const void*)heat_sweep_kernel<4>; break;
-        case 8: fn = window ? (const void*)heat_window_kernel<8> : (const void*)heat_sweep_kernel<8>; break;
-        case 16: fn = window ? (const void*)heat_window_kernel<16> : (const void*)heat_sweep_kernel<16>; break;
-        default: return 1;
-    }
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, nt, smem) != cudaSuccess) return 1;
-    return std::max(1, n);
+    void* args[] = {&aa, &t1, &t2, &t3, &to};
+    return launch(k.win, grid, a.co.nt, heat_window_smem(a), s, args);
 }
 
 }  // namespace atm

@@ -39,6 +39,22 @@ def test_phi_matches_oracle(n, level):
     assert rel_l2(got, want) <= PHI_RTOL
 
 
+@pytest.mark.parametrize("n", [63, 257, 1025, 4095])
+@pytest.mark.parametrize("tf", [1.0 / 64, 1.0 / 4, 4.0])
+def test_phi_small_r_uses_converged_coefficients(n, tf):
+    # small dt/h^2 makes the Thomas coefficients converge inside the vector,
+    # exercising the register-constant path next to the table path
+    args = dict(_heat_case(n, n_points=4097, m=16, k=8), tf=tf)
+    app, hier, cfg = device_objects(args)
+    drv = T.CycleDriver(app, hier, cfg)
+    orc = oracle_driver(args)
+    x = np.stack([O.random_state(300 + j, n) for j in range(3)])
+    for level in (0, 1):
+        got = drv.apply_phi(level, 1, x)
+        want = np.stack([orc.step(level, 1 + j, x[j]) for j in range(3)])
+        assert rel_l2(got, want) <= PHI_RTOL, level
+
+
 @pytest.mark.parametrize("n", [17, 1025])
 def test_forced_phi_and_forcing_match_oracle(n):
     for folded in (0, 1):
