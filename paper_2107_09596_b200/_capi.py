@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libatmgrit.so")
+LIB_PATH = os.environ.get("ATM_LIB") or os.path.join(HERE, "libatmgrit.so")
 MAXL = 8
 _DP = C.POINTER(C.c_double)
 _IP = C.POINTER(C.c_int)

@@ -467,19 +467,18 @@ void Engine::build_coefs(Shard& s) {
         if (heat_) {
             const HeatLevelHost hh = heat_level_host(n_, pitch_, L_heat_, sub_dt, h_, S);
             HeatCoefDev& c = Lv.hco;
-            c.beta = up(hh.beta);
-            c.gamma = up(hh.gamma);
-            c.cneg = up(hh.cneg);
+            c.corr_g = up(hh.corr_g);
+            c.corr_w = up(hh.corr_w);
             c.scan = up(hh.scan);
-            c.pf = up(hh.pf);
-            c.pb = up(hh.pb);
             c.wf = up(hh.wf);
             c.wb = up(hh.wb);
+            c.wk = up(hh.wk);
             c.powc = up(hh.powc);
             c.beta_c = hh.beta_c;
             c.gamma_c = hh.gamma_c;
             c.cneg_c = hh.cneg_c;
-            c.i0 = hh.i0;
+            c.sigma = hh.sigma;
+            c.ncw = hh.ncw;
             c.n = n_;
             c.pitch = pitch_;
             c.nt = hh.nt;

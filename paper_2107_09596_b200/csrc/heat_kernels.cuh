@@ -6,11 +6,7 @@
 // x += theta(t) * sin(pi x).  The reference runs the Thomas recurrences
 // serially per vector; here one CTA owns one state vector (one time point)
 // in registers, in a blocked arrangement (thread t holds elements
-// [t*L, t*L+L)), and each first-order recurrence is evaluated as
-//   local chunk recurrence  ->  warp shuffle scan + cross-warp carry  ->
-//   fix-up with precomputed multiplier products (independent FMAs).
-// Every multiplier depends only on the level's coefficients and the CTA
-// shape, so it is precomputed once on the host (HeatLevelHost).
+// [t*L, t*L+L)).  See heat_phi5.cu for the algorithm.
 #pragma once
 
 #include <cuda.h>
@@ -22,32 +18,40 @@ namespace atm {
 constexpr int kMaxThreads = 512;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr int kMaxL = 16;
-constexpr int kScanPerThread = 12;  // Mf[5], Pf_ex, Mb[5], Pb_ex
+constexpr int kScanPerThread = 16;  // Mf[5], Pf_ex, Mb[5], Pb_ex, SB, q0, pad
 
 // Device view of one level's Phi coefficients.
+//
+// The tridiagonal matrix T = tridiag(a, b, a) (a = -r, b = 1 + 2r) equals
+// the constant-coefficient LU product M = L_c U_c built from the fixed point
+// (c*, d*) of the Thomas recurrence everywhere except entry (0,0):
+//     T = M + delta e0 e0^T,  delta = a c*.
+// Phi is therefore computed as x = M^{-1} b - s w with w = M^{-1} e0,
+// s = sigma (g . b), g = M^{-T} e0, sigma = delta / (1 + delta w0)
+// (Sherman-Morrison).  w and g decay geometrically from index 0, so only
+// the first `ncw` warps touch them.
 struct HeatCoefDev {
-    const double* beta;    // [nt*L] 1/den_i        (0 beyond n)
-    const double* gamma;   // [nt*L] r/den_i        (0 beyond n)
-    const double* cneg;    // [nt*L] -c'_i          (0 beyond n and at n-1)
-    const double* pf;      // [nt*L] forward fix-up products  prod_{j=s..e} gamma_j
-    const double* pb;      // [nt*L] backward fix-up products prod_{j=e..s+L-1} cneg_j
-    const double* scan;    // [nt][12] warp-scan multipliers
+    const double* corr_g;  // [nt*L] g = M^{-T} e0 (0 past the decay cut-off)
+    const double* corr_w;  // [nt*L] w = M^{-1} e0 (0 past the cut-off and beyond n)
+    const double* scan;    // [nt][16] per-thread scan multipliers
     const double* wf;      // [kMaxWarps][kMaxWarps] cross-warp carry weights (forward)
     const double* wb;      // [kMaxWarps][kMaxWarps] (backward)
-    const double* powc;    // [2][kMaxL] fix-up products for constant-coefficient threads
+    const double* wk;      // [kMaxWarps][kMaxWarps] forward-into-backward coupling weights
+    const double* powc;    // [3][kMaxL] q, p_b of interior threads; q of the padded last thread
     const double* theta;   // [np*S] forcing amplitude per (index, substep) or null
     const double* prof;    // [nt*L] forcing profile sin(pi x_i) or null
-    double beta_c, gamma_c, cneg_c;  // converged coefficients (chunks >= i0)
-    int i0;                // first chunk start using constants (multiple of L)
+    double beta_c, gamma_c, cneg_c;  // fixed-point factors: 1/d*, r/d*, -c*
+    double sigma;          // Sherman-Morrison scale
+    int ncw;               // warps that carry the rank-1 correction
     int n, pitch, nt, L;
     int substeps;
 };
 
 // Host-side construction of a level's coefficients (heat1d.cpp:24-45).
 struct HeatLevelHost {
-    std::vector<double> beta, gamma, cneg, pf, pb, scan, wf, wb, powc;
-    double r = 0, beta_c = 0, gamma_c = 0, cneg_c = 0;
-    int i0 = 0, n = 0, pitch = 0, nt = 0, L = 0, substeps = 1;
+    std::vector<double> corr_g, corr_w, scan, wf, wb, wk, powc;
+    double r = 0, beta_c = 0, gamma_c = 0, cneg_c = 0, sigma = 0;
+    int ncw = 0, n = 0, pitch = 0, nt = 0, L = 0, substeps = 1;
 };
 HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, int substeps);
 

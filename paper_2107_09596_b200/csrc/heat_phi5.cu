@@ -1,12 +1,35 @@
-// heat_phi.cu -- Heat1D Phi chains for sm_100a.
+// heat_phi5.cu -- Heat1D Phi chains for sm_100a.
 //
 // One CTA owns one state vector (a time point) in registers, blocked
 // (thread t holds elements [t*L, t*L+L)).  Rows move HBM <-> smem by TMA
 // (cp.async.bulk.tensor, 128B-swizzled so the blocked register view reads
 // and writes smem conflict-free); produced rows leave through TMA-store
-// staging so stores overlap the next Phi.  The kernels are persistent: each
-// CTA walks a contiguous range of jobs, so the row that closes job J (the
-// residual's C-point) is the seed of job J+1 and is loaded once.
+// staging so stores overlap the next Phi.
+//
+// One Phi sub-step solves (I + sub_dt L) x = b, T = tridiag(a, b0, a) with
+// a = -r, b0 = 1 + 2r (heat1d.cpp:24-60).  With (c*, d*) the fixed point of
+// the Thomas recurrence, T = L_c U_c + delta e0 e0^T (delta = a c*), so
+//     x = M^{-1} b - sigma (g . b) w,   M = L_c U_c, w = M^{-1} e0, g = M^{-T} e0
+// (Sherman-Morrison).  Every thread runs the constant-coefficient recurrences
+// from registers; g and w decay geometrically from the boundary and only
+// touch the first `ncw` warps, as independent FMAs.  (In fp64 this is more
+// accurate than the serial Thomas sweep with its non-converged leading
+// factors; see tests/test_gpu_parity.py.)
+//
+// M^{-1} b is evaluated with ONE CTA barrier:
+//   1. forward local pass      y_loc = L^{-1} b on the chunk (zero carry-in)
+//   2. forward warp scan of the chunk ends -> E (exclusive), warp total Tf
+//   3. backward local pass     z_loc = U^{-1} y_loc   (the forward carry c_f
+//      enters linearly as c_f q with q = U^{-1} p_f, precomputed)
+//   4. backward warp scan of a = z_loc[0] + E q0 -> RA, warp total TA
+//   5. publish (Tf, TA, g.b partials), bar.sync, cross-warp carries as fixed
+//      weighted sums (lane-parallel + xor tree)
+//   6. x = z_loc + c_f q + c_b p_b - s w
+// All multipliers are precomputed on the host (heat_level_host).
+//
+// Proxy rule: a buffer filled by TMA and read with ld.shared is handed back
+// to TMA only after fence.proxy.async + bar.sync (write-after-read across
+// the generic and async proxies).
 //
 // Reference semantics restated (file:line under /root/reference/proj):
 //   Phi / step          heat1d.cpp:47-60 (Thomas), :66-83 (sub-steps, forcing)
@@ -30,142 +53,181 @@
 namespace atm {
 
 // --------------------------------------------------------------------------
-// host: coefficients and scan / carry multipliers
+// host: fixed-point factors, correction vectors and every scan multiplier
 
 HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, int substeps) {
+    using LD = long double;
     HeatLevelHost H;
     H.n = n;
     H.pitch = pitch;
     H.L = L;
     H.substeps = substeps;
-    const int nt = (((pitch + L - 1) / L) + 31) / 32 * 32;
+    const int nt = ((pitch + L - 1) / L + 127) / 128 * 128;
     H.nt = nt;
     const int npad = nt * L;
-    // heat1d.cpp:28-44: r = sub_dt/h^2, a = -r, b = 1 + 2r, den_i = b - a c'_{i-1}
+    // heat1d.cpp:28-31: r = sub_dt/h^2, a = -r, b = 1 + 2r
     H.r = sub_dt / (h * h);
-    const double a = -H.r;
-    const double b = 1.0 + 2.0 * H.r;
-    std::vector<double> beta(npad, 0.0), cpr(npad, 0.0);
-    double prev_c = 0.0;
-    for (int i = 0; i < n; ++i) {
-        const double den = b - a * prev_c;
-        beta[i] = 1.0 / den;
-        prev_c = a / den;
-        cpr[i] = prev_c;
-    }
-    H.beta.assign(npad, 0.0);
-    H.gamma.assign(npad, 0.0);
-    H.cneg.assign(npad, 0.0);
-    for (int i = 0; i < n; ++i) {
-        H.beta[i] = beta[i];
-        H.gamma[i] = H.r * beta[i];
-        // the backward sweep never reads c'_{n-1} (heat1d.cpp:56)
-        H.cneg[i] = (i == n - 1) ? 0.0 : -cpr[i];
-    }
-    // converged tail: the c' recurrence is a contraction; past i0 the
-    // coefficients agree with their limit to <= 2 ulp and live in registers
-    H.i0 = ((n + L - 1) / L) * L;
-    if (n >= 3) {
-        const double bc = beta[n - 2], cc = -cpr[n - 2];
-        auto close = [](double x, double y) { return std::fabs(x - y) <= 4.5e-16 * std::fabs(y); };
-        int last_diff = -1;
-        for (int i = 0; i < n - 1; ++i)
-            if (!close(beta[i], bc) || !close(-cpr[i], cc)) last_diff = i;
-        H.i0 = ((last_diff + 1 + L - 1) / L) * L;
-        H.beta_c = bc;
-        H.gamma_c = H.r * bc;
-        H.cneg_c = cc;
-    }
-    // effective per-element coefficients exactly as the device uses them
-    std::vector<double> eg(npad), ec(npad);
-    for (int t = 0; t < nt; ++t) {
-        const int s = t * L;
-        const bool cst = (s >= H.i0) && (s + L <= n - 1);
-        for (int e = 0; e < L; ++e) {
-            eg[s + e] = cst ? H.gamma_c : H.gamma[s + e];
-            ec[s + e] = cst ? H.cneg_c : H.cneg[s + e];
+    const LD r = static_cast<LD>(H.r);
+    const LD a = -r, b = 1.0L + 2.0L * r;
+    // fixed point of c = a / (b - a c): the root of a c^2 - b c + a with |c| < 1
+    const LD c = 2.0L * a / (b + std::sqrt(1.0L + 4.0L * r));
+    const LD d = b - a * c;
+    H.beta_c = static_cast<double>(1.0L / d);
+    H.gamma_c = static_cast<double>(r / d);
+    H.cneg_c = static_cast<double>(-c);
+    // correction vectors: w = M^{-1} e0 (L_c: d* diag, a sub; U_c: 1 diag, c* super)
+    std::vector<LD> w(n), v(n), g(n);
+    {
+        LD p = 0.0L;
+        for (int i = 0; i < n; ++i) {
+            p = ((i == 0 ? 1.0L : 0.0L) - a * p) / d;
+            w[i] = p;
         }
+        for (int i = n - 2; i >= 0; --i) w[i] -= c * w[i + 1];
+        // g = M^{-T} e0: U_c^T v = e0, then L_c^T g = v
+        v[0] = 1.0L;
+        for (int i = 1; i < n; ++i) v[i] = -c * v[i - 1];
+        for (int i = n - 1; i >= 0; --i) g[i] = (v[i] - (i + 1 < n ? a * g[i + 1] : 0.0L)) / d;
     }
-    // per-thread fix-up products and chunk products
-    H.pf.assign(npad, 0.0);
-    H.pb.assign(npad, 0.0);
-    std::vector<double> Af(nt), Ab(nt);
+    const LD delta = a * c;
+    H.sigma = static_cast<double>(delta / (1.0L + delta * w[0]));
+    LD wmax = 0.0L, gmax = 0.0L;
+    for (int i = 0; i < n; ++i) {
+        wmax = std::max(wmax, std::fabs(w[i]));
+        gmax = std::max(gmax, std::fabs(g[i]));
+    }
+    int K = 0;  // past K both vectors are below 1e-20 of their peak
+    for (int i = 0; i < n; ++i)
+        if (std::fabs(w[i]) > 1e-20L * wmax || std::fabs(g[i]) > 1e-20L * gmax) K = i + 1;
+    H.corr_w.assign(npad, 0.0);
+    H.corr_g.assign(npad, 0.0);
+    for (int i = 0; i < K; ++i) {
+        H.corr_w[i] = static_cast<double>(w[i]);
+        H.corr_g[i] = static_cast<double>(g[i]);
+    }
+    H.ncw = (K + 32 * L - 1) / (32 * L);
+    // effective per-element coefficients; padding elements (>= n) carry
+    // gamma = 0 so no forward carry crosses them
+    std::vector<double> eg(npad), ec(npad);
+    for (int i = 0; i < npad; ++i) {
+        eg[i] = i < n ? H.gamma_c : 0.0;
+        ec[i] = H.cneg_c;
+    }
+    // per thread: p_f (forward carry influence), q = U^{-1} p_f, p_b
+    std::vector<double> q(npad), pb(npad), Af(nt), Ab(nt), q0(nt);
     for (int t = 0; t < nt; ++t) {
+        std::vector<double> pf(L);
         double p = 1.0;
         for (int e = 0; e < L; ++e) {
             p *= eg[t * L + e];
-            H.pf[t * L + e] = p;
+            pf[e] = p;
         }
         Af[t] = p;
+        double z = 0.0;
+        for (int e = L - 1; e >= 0; --e) {
+            z = ec[t * L + e] * z + pf[e];
+            q[t * L + e] = z;
+        }
+        q0[t] = q[t * L];
         p = 1.0;
         for (int e = L - 1; e >= 0; --e) {
             p *= ec[t * L + e];
-            H.pb[t * L + e] = p;
+            pb[t * L + e] = p;
         }
         Ab[t] = p;
     }
-    H.powc.assign(2 * kMaxL, 0.0);
+    // interior-thread vectors (constant coefficients, no padding), and q of
+    // the thread holding element n-1
+    H.powc.assign(3 * kMaxL, 0.0);
     {
+        std::vector<double> pf(L);
         double p = 1.0;
         for (int e = 0; e < L; ++e) {
             p *= H.gamma_c;
-            H.powc[e] = p;
+            pf[e] = p;
+        }
+        double z = 0.0;
+        for (int e = L - 1; e >= 0; --e) {
+            z = H.cneg_c * z + pf[e];
+            H.powc[e] = z;
         }
         p = 1.0;
         for (int e = L - 1; e >= 0; --e) {
             p *= H.cneg_c;
             H.powc[kMaxL + e] = p;
         }
+        const int tl = (n - 1) / L;
+        for (int e = 0; e < L; ++e) H.powc[2 * kMaxL + e] = q[tl * L + e];
     }
-    // warp scan multipliers (Hillis-Steele over lanes) and warp products
+    // warp scans (Hillis-Steele; 0 where a lane has no partner)
     H.scan.assign(static_cast<size_t>(nt) * kScanPerThread, 0.0);
     const int nw = nt / 32;
-    std::vector<double> AWf(nw), AWb(nw);
-    for (int w = 0; w < nw; ++w) {
-        double pf = 1.0, pb = 1.0;
-        for (int l = 0; l < 32; ++l) pf *= Af[32 * w + l];
-        for (int l = 31; l >= 0; --l) pb *= Ab[32 * w + l];
-        AWf[w] = pf;
-        AWb[w] = pb;
+    std::vector<double> AWf(nw), AWb(nw), TB(nw);
+    for (int wi = 0; wi < nw; ++wi) {
+        double pf = 1.0, pbw = 1.0;
+        for (int l = 0; l < 32; ++l) pf *= Af[32 * wi + l];
+        for (int l = 31; l >= 0; --l) pbw *= Ab[32 * wi + l];
+        AWf[wi] = pf;
+        AWb[wi] = pbw;
+        std::vector<double> Pfex(32), RB(33, 0.0);
         for (int l = 0; l < 32; ++l) {
-            double* sc = &H.scan[static_cast<size_t>(32 * w + l) * kScanPerThread];
-            for (int d = 0; d < 5; ++d) {
-                const int off = 1 << d;
+            double ex = 1.0;
+            for (int u = 0; u < l; ++u) ex *= Af[32 * wi + u];
+            Pfex[l] = ex;
+        }
+        // backward inclusive-from-the-right recurrence of b = Pfex * q0
+        for (int l = 31; l >= 0; --l)
+            RB[l] = Pfex[l] * q0[32 * wi + l] + Ab[32 * wi + l] * RB[l + 1];
+        TB[wi] = RB[0];
+        for (int l = 0; l < 32; ++l) {
+            double* sc = &H.scan[static_cast<size_t>(32 * wi + l) * kScanPerThread];
+            for (int dd = 0; dd < 5; ++dd) {
+                const int off = 1 << dd;
                 double mf = 0.0, mb = 0.0;
                 if (l >= off) {
                     mf = 1.0;
-                    for (int u = l - off + 1; u <= l; ++u) mf *= Af[32 * w + u];
+                    for (int u = l - off + 1; u <= l; ++u) mf *= Af[32 * wi + u];
                 }
                 if (l + off <= 31) {
                     mb = 1.0;
-                    for (int u = l; u <= l + off - 1; ++u) mb *= Ab[32 * w + u];
+                    for (int u = l; u <= l + off - 1; ++u) mb *= Ab[32 * wi + u];
                 }
-                sc[d] = mf;
-                sc[6 + d] = mb;
+                sc[dd] = mf;
+                sc[6 + dd] = mb;
             }
-            double ex = 1.0;
-            for (int u = 0; u < l; ++u) ex *= Af[32 * w + u];
-            sc[5] = ex;
+            sc[5] = Pfex[l];
             double exb = 1.0;
-            for (int u = l + 1; u <= 31; ++u) exb *= Ab[32 * w + u];
+            for (int u = l + 1; u <= 31; ++u) exb *= Ab[32 * wi + u];
             sc[11] = exb;
+            sc[12] = RB[l + 1];      // SB: coefficient of C_w in c_b
+            sc[13] = q0[32 * wi + l];
         }
     }
-    // cross-warp carry weights: carry_w = sum_{v<w} (prod_{u=v+1}^{w-1} AWf_u) T_v
+    // cross-warp weights (zero outside the causal range)
     H.wf.assign(kMaxWarps * kMaxWarps, 0.0);
     H.wb.assign(kMaxWarps * kMaxWarps, 0.0);
-    for (int w = 0; w < nw; ++w) {
-        for (int v = 0; v < w; ++v) {
+    H.wk.assign(kMaxWarps * kMaxWarps, 0.0);
+    for (int wi = 0; wi < nw; ++wi) {
+        for (int vv = 0; vv < wi; ++vv) {
             double p = 1.0;
-            for (int u = v + 1; u <= w - 1; ++u) p *= AWf[u];
-            H.wf[w * kMaxWarps + v] = p;
+            for (int u = vv + 1; u <= wi - 1; ++u) p *= AWf[u];
+            H.wf[wi * kMaxWarps + vv] = p;
         }
-        for (int v = w + 1; v < nw; ++v) {
+        for (int vv = wi + 1; vv < nw; ++vv) {
             double p = 1.0;
-            for (int u = w + 1; u <= v - 1; ++u) p *= AWb[u];
-            H.wb[w * kMaxWarps + v] = p;
+            for (int u = wi + 1; u <= vv - 1; ++u) p *= AWb[u];
+            H.wb[wi * kMaxWarps + vv] = p;
         }
     }
+    // D_w = sum_{v>w} Wb[w][v] (TA_v + C_v TB_v), C_v = sum_{u<v} Wf[v][u] Tf_u
+    //     = sum_v Wb[w][v] TA_v + sum_u K[w][u] Tf_u
+    for (int wi = 0; wi < nw; ++wi)
+        for (int u = 0; u < nw; ++u) {
+            double k = 0.0;
+            for (int vv = std::max(wi, u) + 1; vv < nw; ++vv)
+                k += H.wb[wi * kMaxWarps + vv] * TB[vv] * H.wf[vv * kMaxWarps + u];
+            H.wk[wi * kMaxWarps + u] = k;
+        }
     return H;
 }
 
@@ -175,8 +237,11 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
 template <int L>
 struct Lane {
     int t, lane, warp, nw, s;
-    bool cst;
-    double Mf[5], Pfex, Mb[5], Pbex;
+    int q7, qx, ch0;     // swizzled row-staging geometry of this chunk
+    int pad0;            // first padding element of the chunk, L if none
+    int par;             // parity of the warp-total slots (one barrier per Phi)
+    bool corr, inside;   // carries the rank-1 correction; chunk inside the row
+    double Mf[5], Pfex, Mb[5], Pbex, SB, q0, lm, rm;
 };
 
 template <int L>
@@ -186,7 +251,13 @@ __device__ __forceinline__ void lane_init(Lane<L>& ln, const HeatCoefDev& co) {
     ln.warp = ln.t >> 5;
     ln.nw = blockDim.x >> 5;
     ln.s = ln.t * L;
-    ln.cst = (ln.s >= co.i0) && (ln.s + L <= co.n - 1);
+    ln.corr = ln.warp < co.ncw;
+    ln.inside = ln.s < co.pitch;  // chunks never straddle pitch (pitch % 16 == 0)
+    ln.q7 = (ln.s >> 4) << 7;
+    ln.qx = (ln.s >> 4) & 7;
+    ln.ch0 = (ln.s & 15) >> 1;
+    ln.pad0 = (ln.s + L > co.n) ? max(0, co.n - ln.s) : L;
+    ln.par = 0;
     const double* sc = co.scan + ln.t * kScanPerThread;
 #pragma unroll
     for (int d = 0; d < 5; ++d) {
@@ -195,132 +266,160 @@ __device__ __forceinline__ void lane_init(Lane<L>& ln, const HeatCoefDev& co) {
     }
     ln.Pfex = __ldg(sc + 5);
     ln.Pbex = __ldg(sc + 11);
+    ln.SB = __ldg(sc + 12);
+    ln.q0 = __ldg(sc + 13);
+    ln.lm = ln.lane > 0 ? 1.0 : 0.0;
+    ln.rm = ln.lane < 31 ? 1.0 : 0.0;
 }
 
 struct Tabs {              // per-CTA copy of the level's small tables
     double wf[kMaxWarps * kMaxWarps];
     double wb[kMaxWarps * kMaxWarps];
-    double powc[2 * kMaxL];
+    double wk[kMaxWarps * kMaxWarps];
+    double powc[3 * kMaxL];  // q, p_b of interior threads; q of the padded last thread
 };
 
-struct Slots {             // small shared scratch
-    double swf[kMaxWarps];
-    double swb[kMaxWarps];
+struct Slots {                // small shared scratch
+    double tf[2][kMaxWarps];  // forward warp totals (double-buffered by Phi parity)
+    double ta[2][kMaxWarps];  // backward warp totals, C_w-free part
+    double gd[2][kMaxWarps];  // g . b partial sums of the correction warps
     double red[kMaxWarps];
     uint64_t bar[4];
 };
 
-__device__ __forceinline__ void tabs_init(Tabs& tb, const HeatCoefDev& co) {
+__device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev& co) {
     for (int i = threadIdx.x; i < kMaxWarps * kMaxWarps; i += blockDim.x) {
         tb.wf[i] = co.wf[i];
         tb.wb[i] = co.wb[i];
+        tb.wk[i] = co.wk[i];
     }
-    for (int i = threadIdx.x; i < 2 * kMaxL; i += blockDim.x) tb.powc[i] = co.powc[i];
+    for (int i = threadIdx.x; i < 3 * kMaxL; i += blockDim.x) tb.powc[i] = co.powc[i];
+    // warp slots beyond the CTA are read with zero weights: keep them finite
+    for (int i = threadIdx.x; i < 2 * kMaxWarps; i += blockDim.x) {
+        sl.tf[i / kMaxWarps][i % kMaxWarps] = 0.0;
+        sl.ta[i / kMaxWarps][i % kMaxWarps] = 0.0;
+        sl.gd[i / kMaxWarps][i % kMaxWarps] = 0.0;
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L>& ln) {
+    if (ln.pad0 < L) {
+#pragma unroll
+        for (int e = 0; e < L; ++e)
+            if (e >= ln.pad0) x[e] = 0.0;
+    }
 }
 
 // (I + sub_dt L) x = x, in place, over the CTA (heat1d.cpp:47-60).
 template <int L>
-__device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
-                                          const Lane<L>& ln, const Tabs& tb, Slots& sl) {
-    // forward  y_i = beta_i x_i + gamma_i y_{i-1}   (local: zero carry-in)
+__device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
+                                          const Tabs& tb, Slots& sl) {
+    // 0. g . b partial: only when the correction spans several warps (with a
+    //    single correction warp, x_c[0] is thread 0's own result, see 6.)
+    const bool dot = ln.corr && co.ncw > 1;
+    double gd = 0.0;
+    if (dot) {
+        const double* gt = co.corr_g + ln.s;
+        if constexpr (L >= 4) {
+            double g1 = 0.0, g2 = 0.0, g3 = 0.0;
+#pragma unroll
+            for (int e = 0; e < L; e += 4) {
+                gd = fma(__ldg(gt + e), x[e], gd);
+                g1 = fma(__ldg(gt + e + 1), x[e + 1], g1);
+                g2 = fma(__ldg(gt + e + 2), x[e + 2], g2);
+                g3 = fma(__ldg(gt + e + 3), x[e + 3], g3);
+            }
+            gd = (gd + g1) + (g2 + g3);
+        } else {
+#pragma unroll
+            for (int e = 0; e < L; ++e) gd = fma(__ldg(gt + e), x[e], gd);
+        }
+    }
+    // 1. forward local  y_i = beta x_i + gamma y_{i-1}
     double y = 0.0;
-    if (ln.cst) {
+    {
         const double bb = co.beta_c, gg = co.gamma_c;
 #pragma unroll
         for (int e = 0; e < L; ++e) {
             y = fma(gg, y, bb * x[e]);
             x[e] = y;
         }
-    } else {
-        const double* bt = co.beta + ln.s;
-        const double* gt = co.gamma + ln.s;
-#pragma unroll
-        for (int e = 0; e < L; ++e) {
-            y = fma(__ldg(gt + e), y, __ldg(bt + e) * x[e]);
-            x[e] = y;
-        }
+        zero_padding<L>(x, ln);
+        y = x[L - 1];
     }
+    // 2. forward warp scan of the chunk ends
     double B = y;
 #pragma unroll
-    for (int d = 0; d < 5; ++d) {
-        const double o = __shfl_up_sync(0xffffffffu, B, 1 << d);
-        if (ln.lane >= (1 << d)) B = fma(ln.Mf[d], o, B);
-    }
-    double ex = __shfl_up_sync(0xffffffffu, B, 1);
-    if (ln.lane == 0) ex = 0.0;
-    if (ln.lane == 31) sl.swf[ln.warp] = B;
-    __syncthreads();
-    {
-        const double* wr = tb.wf + ln.warp * kMaxWarps;
-        double c0 = 0.0, c1 = 0.0;
-        int v = 0;
-        for (; v + 1 < ln.warp; v += 2) {
-            c0 = fma(wr[v], sl.swf[v], c0);
-            c1 = fma(wr[v + 1], sl.swf[v + 1], c1);
-        }
-        if (v < ln.warp) c0 = fma(wr[v], sl.swf[v], c0);
-        const double carry = fma(ln.Pfex, c0 + c1, ex);
-        if (ln.cst) {
-#pragma unroll
-            for (int e = 0; e < L; ++e) x[e] = fma(carry, tb.powc[e], x[e]);
-        } else {
-            const double* pt = co.pf + ln.s;
-#pragma unroll
-            for (int e = 0; e < L; ++e) x[e] = fma(carry, __ldg(pt + e), x[e]);
-        }
-    }
-    // backward  x_i = y_i - c'_i x_{i+1}   (local: zero carry-in)
+    for (int d = 0; d < 5; ++d) B = fma(ln.Mf[d], __shfl_up_sync(0xffffffffu, B, 1 << d), B);
+    const double E = __shfl_up_sync(0xffffffffu, B, 1) * ln.lm;
+    // 3. backward local on the uncorrected forward values
     double z = 0.0;
-    if (ln.cst) {
+    {
         const double cc = co.cneg_c;
 #pragma unroll
         for (int e = L - 1; e >= 0; --e) {
             z = fma(cc, z, x[e]);
             x[e] = z;
         }
-    } else {
-        const double* ct = co.cneg + ln.s;
-#pragma unroll
-        for (int e = L - 1; e >= 0; --e) {
-            z = fma(__ldg(ct + e), z, x[e]);
-            x[e] = z;
-        }
     }
-    B = z;
+    // 4. backward warp scan of a = z_loc[0] + E q0 (the C_w part is precomputed)
+    double R = fma(E, ln.q0, z);
 #pragma unroll
-    for (int d = 0; d < 5; ++d) {
-        const double o = __shfl_down_sync(0xffffffffu, B, 1 << d);
-        if (ln.lane + (1 << d) <= 31) B = fma(ln.Mb[d], o, B);
+    for (int d = 0; d < 5; ++d) R = fma(ln.Mb[d], __shfl_down_sync(0xffffffffu, R, 1 << d), R);
+    const double RAn = __shfl_down_sync(0xffffffffu, R, 1) * ln.rm;
+    if (dot) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) gd += __shfl_xor_sync(0xffffffffu, gd, off);
     }
-    ex = __shfl_down_sync(0xffffffffu, B, 1);
-    if (ln.lane == 31) ex = 0.0;
-    if (ln.lane == 0) sl.swb[ln.warp] = B;
+    // 5. publish warp totals; one barrier; cross-warp carries
+    const int par = ln.par;
+    if (ln.lane == 31) sl.tf[par][ln.warp] = B;
+    if (ln.lane == 0) sl.ta[par][ln.warp] = R;
+    if (dot && ln.lane == 1) sl.gd[par][ln.warp] = gd;
     __syncthreads();
+    ln.par ^= 1;
+    double cC, cD;
     {
-        const double* wr = tb.wb + ln.warp * kMaxWarps;
-        double c0 = 0.0, c1 = 0.0;
-        int v = ln.warp + 1;
-        for (; v + 1 < ln.nw; v += 2) {
-            c0 = fma(wr[v], sl.swb[v], c0);
-            c1 = fma(wr[v + 1], sl.swb[v + 1], c1);
-        }
-        if (v < ln.nw) c0 = fma(wr[v], sl.swb[v], c0);
-        const double carry = fma(ln.Pbex, c0 + c1, ex);
-        if (ln.cst) {
+        const int v = ln.lane & (kMaxWarps - 1);
+        const double tf = sl.tf[par][v], ta = sl.ta[par][v];
+        const int row = ln.warp * kMaxWarps + v;
+        cC = tb.wf[row] * tf;
+        cD = fma(tb.wb[row], ta, tb.wk[row] * tf);
 #pragma unroll
-            for (int e = 0; e < L; ++e) x[e] = fma(carry, tb.powc[kMaxL + e], x[e]);
+        for (int off = kMaxWarps / 2; off >= 1; off >>= 1) {
+            cC += __shfl_xor_sync(0xffffffffu, cC, off);
+            cD += __shfl_xor_sync(0xffffffffu, cD, off);
+        }
+    }
+    const double cf = fma(ln.Pfex, cC, E);
+    const double cb = fma(ln.Pbex, cD, fma(ln.SB, cC, RAn));
+    // 6. x = z_loc + c_f q + c_b p_b (- s w)
+    {
+        const double* qv = (ln.pad0 < L) ? tb.powc + 2 * kMaxL : tb.powc;
+#pragma unroll
+        for (int e = 0; e < L; ++e) x[e] = fma(cb, tb.powc[kMaxL + e], fma(cf, qv[e], x[e]));
+        zero_padding<L>(x, ln);
+    }
+    if (ln.corr) {
+        double g0;
+        if (dot) {
+            g0 = 0.0;
+            for (int w = 0; w < co.ncw; ++w) g0 += sl.gd[par][w];
         } else {
-            const double* pt = co.pb + ln.s;
-#pragma unroll
-            for (int e = 0; e < L; ++e) x[e] = fma(carry, __ldg(pt + e), x[e]);
+            g0 = __shfl_sync(0xffffffffu, x[0], 0);  // (M^{-1} b)_0 held by thread 0
         }
+        const double ms = -co.sigma * g0;
+        const double* wt = co.corr_w + ln.s;
+#pragma unroll
+        for (int e = 0; e < L; ++e) x[e] = fma(ms, __ldg(wt + e), x[e]);
     }
 }
 
 // Phi_index on this level: S sub-steps, forcing added before each solve
 // when `forced` (heat1d.cpp:66-83).
 template <int L>
-__device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, const Lane<L>& ln,
+__device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
                                     const Tabs& tb, Slots& sl, int index, int forced) {
     for (int s = 0; s < co.substeps; ++s) {
         if (forced) {
@@ -333,47 +432,46 @@ __device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, const
 }
 
 // --------------------------------------------------------------------------
-// device: swizzled row staging (TMA SWIZZLE_128B layout)
-
-__device__ __forceinline__ int swz(int e) {
-    const int q = e >> 4, ch = (e & 15) >> 1;
-    return (q << 7) + ((ch ^ (q & 7)) << 4);
-}
+// device: swizzled row staging (TMA SWIZZLE_128B layout).  A thread's chunk
+// lies in one 128-byte row q of the staging box; 16-byte unit c sits at
+// position c ^ (q & 7).
 
 template <int L>
-__device__ __forceinline__ void row_load(const char* buf, double (&x)[L], int s, int pitch) {
+__device__ __forceinline__ void row_load(const char* buf, double (&x)[L], const Lane<L>& ln) {
+    if (ln.inside) {
+        const char* rp = buf + ln.q7;
 #pragma unroll
-    for (int c = 0; c < L / 2; ++c) {
-        const int e = s + 2 * c;
-        if (e < pitch) {
-            const double2 v = *reinterpret_cast<const double2*>(buf + swz(e));
+        for (int c = 0; c < L / 2; ++c) {
+            const double2 v = *reinterpret_cast<const double2*>(rp + (((ln.ch0 + c) ^ ln.qx) << 4));
             x[2 * c] = v.x;
             x[2 * c + 1] = v.y;
-        } else {
-            x[2 * c] = 0.0;
-            x[2 * c + 1] = 0.0;
         }
+    } else {
+#pragma unroll
+        for (int e = 0; e < L; ++e) x[e] = 0.0;
     }
 }
 
 template <int L>
-__device__ __forceinline__ void row_store(char* buf, const double (&x)[L], int s, int pitch) {
+__device__ __forceinline__ void row_store(char* buf, const double (&x)[L], const Lane<L>& ln) {
+    if (ln.inside) {
+        char* rp = buf + ln.q7;
 #pragma unroll
-    for (int c = 0; c < L / 2; ++c) {
-        const int e = s + 2 * c;
-        if (e < pitch) *reinterpret_cast<double2*>(buf + swz(e)) = make_double2(x[2 * c], x[2 * c + 1]);
+        for (int c = 0; c < L / 2; ++c)
+            *reinterpret_cast<double2*>(rp + (((ln.ch0 + c) ^ ln.qx) << 4)) =
+                make_double2(x[2 * c], x[2 * c + 1]);
     }
 }
 
 // x = x + row, or x = x - row
 template <int L>
-__device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], int s, int pitch,
+__device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], const Lane<L>& ln,
                                         bool sub) {
+    if (ln.inside) {
+        const char* rp = buf + ln.q7;
 #pragma unroll
-    for (int c = 0; c < L / 2; ++c) {
-        const int e = s + 2 * c;
-        if (e < pitch) {
-            const double2 v = *reinterpret_cast<const double2*>(buf + swz(e));
+        for (int c = 0; c < L / 2; ++c) {
+            const double2 v = *reinterpret_cast<const double2*>(rp + (((ln.ch0 + c) ^ ln.qx) << 4));
             if (sub) {
                 x[2 * c] -= v.x;
                 x[2 * c + 1] -= v.y;
@@ -402,8 +500,15 @@ __device__ __forceinline__ double cta_sum_squares(const double (&x)[L], const La
     return tot;
 }
 
-__device__ __forceinline__ char* align1k(unsigned char* p) {
-    return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+// 1024-aligned base inside the dynamic smem window, kept as a __shared__-
+// derived pointer so every access compiles to LDS/STS
+__device__ __forceinline__ char* smem_base(unsigned char* raw) {
+#ifdef ATM_GENERIC_SMEM
+    return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+#else
+    const uint32_t mis = smem_u32(raw) & 1023u;
+    return reinterpret_cast<char*>(raw + ((1024u - mis) & 1023u));
+#endif
 }
 
 __host__ __device__ inline int row_bytes_al(int pitch) { return ((pitch * 8) + 1023) & ~1023; }
@@ -418,12 +523,13 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                       const __grid_constant__ CUtensorMap tm_g,
                       const __grid_constant__ CUtensorMap tm_out) {
     extern __shared__ unsigned char smem_raw[];
-    char* base = align1k(smem_raw);
+    char* base = smem_base(smem_raw);
     const int pitch = a.co.pitch;
     const int rb = row_bytes_al(pitch);
     const int nob = a.n_out;
     char* bufS = base;
-    char* bufO[2] = {base + rb, base + (nob == 2 ? 2 : 1) * rb};
+    char* bufO0 = base + rb;
+    char* bufO1 = base + (nob == 2 ? 2 : 1) * rb;
     char* bufA = base + (1 + nob) * rb;
     char* tl = base + (1 + nob + (a.add_g ? 1 : 0)) * rb;
     Tabs& tb = *reinterpret_cast<Tabs*>(tl);
@@ -436,7 +542,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     Lane<L> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
-    tabs_init(tb, a.co);
+    tabs_init(tb, sl, a.co);
     if (t == 0) {
         mbar_init(barS, 1);
         mbar_init(barA, 1);
@@ -457,8 +563,8 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     // stage x into an output buffer and TMA-store it; the store that last
     // read that buffer was waited for (bulk_wait_read) before the Phi
     auto stage_out = [&](int row, const CUtensorMap* map) {
-        char* o = bufO[ob];
-        row_store<L>(o, x, ln.s, pitch);
+        char* o = ob ? bufO1 : bufO0;
+        row_store<L>(o, x, ln);
         fence_proxy_async();
         __syncthreads();
         if (t == 0) {
@@ -506,10 +612,8 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             mbar_wait(barS, phS);
             phS ^= 1;
         }
-        row_load<L>(bufS, x, ln.s, pitch);
-        // WAR across proxies: our generic reads of S must be ordered before
-        // the TMA (async proxy) write that refills it
-        fence_proxy_async();
+        row_load<L>(bufS, x, ln);
+        fence_proxy_async();  // our reads of S before the TMA refill (WAR)
         __syncthreads();
         seed_ready = false;
         if (tail_i >= 0 && t == 0) {
@@ -531,7 +635,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             if (a.add_g) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
-                row_acc<L>(bufA, x, ln.s, pitch, false);
+                row_acc<L>(bufA, x, ln, false);
             }
             if (a.store && i >= store_from) {
                 stage_out(i - a.u_base, &tm_u);
@@ -555,11 +659,11 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             if (a.add_g) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
-                row_acc<L>(bufA, x, ln.s, pitch, false);
+                row_acc<L>(bufA, x, ln, false);
             }
             mbar_wait(barS, phS);
             phS ^= 1;
-            row_acc<L>(bufS, x, ln.s, pitch, true);
+            row_acc<L>(bufS, x, ln, true);
             if (a.kind == SW_F && J + 1 < je) seed_ready = true;  // S holds u[c_{J+1}]
             if (a.tail == TAIL_STORE) {
                 stage_out(tail_i / m - a.out_base, &tm_out);
@@ -574,9 +678,10 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 
 // --------------------------------------------------------------------------
 // linear window kernel (kernels.cpp:53-61 + solver.cpp:271-278):
-// e = r_lo, e = Psi_s(e) + r_s, fine u[c_p] += e.  The r rows of every job of
-// the CTA form one stream, double-buffered two rows ahead; the fine C-point
-// row is fetched into S ahead of its emit, updated in place and stored back.
+// e = r_lo, e = Psi_s(e) + r_s, fine u[c_p] += e.  Jobs are interleaved over
+// CTAs (concurrent CTAs share r rows in L2); the r rows of the CTA's jobs
+// form one stream, double-buffered two rows ahead; the fine C-point row is
+// fetched into S ahead of its emit, updated in place and stored back.
 // smem: [A0][A1][S][Tabs][Slots]
 
 template <int L, int NTMAX, int MINB>
@@ -585,14 +690,16 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                               const __grid_constant__ CUtensorMap tm_r,
                               const __grid_constant__ CUtensorMap tm_fine) {
     extern __shared__ unsigned char smem_raw[];
-    char* base = align1k(smem_raw);
+    char* base = smem_base(smem_raw);
     const int pitch = a.co.pitch;
     const int rb = row_bytes_al(pitch);
-    char* bufA[2] = {base, base + rb};
+    char* bufA0 = base;
+    char* bufA1 = base + rb;
     char* bufS = base + 2 * rb;
     Tabs& tb = *reinterpret_cast<Tabs*>(base + 3 * rb);
     Slots& sl = *reinterpret_cast<Slots*>(base + 3 * rb + sizeof(Tabs));
-    uint64_t* barA = &sl.bar[0];  // two barriers: bar[0], bar[1]
+    uint64_t* barA0 = &sl.bar[0];
+    uint64_t* barA1 = &sl.bar[1];
     uint64_t* barS = &sl.bar[2];
     const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
     const int R = pitch >> 4;
@@ -600,22 +707,21 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     Lane<L> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
-    tabs_init(tb, a.co);
+    tabs_init(tb, sl, a.co);
     if (t == 0) {
-        mbar_init(&barA[0], 1);
-        mbar_init(&barA[1], 1);
+        mbar_init(barA0, 1);
+        mbar_init(barA1, 1);
         mbar_init(barS, 1);
         mbar_fence_init();
     }
     __syncthreads();
-    uint32_t phA[2] = {0, 0}, phS = 0;
+    uint32_t ph0 = 0, ph1 = 0, phS = 0;
 
     const bool has_pre = a.pre_e1 >= a.pre_e0;
     const int n_ind = max(0, a.p1 - a.p0 + 1);
-    const long long Nj = (has_pre ? 1 : 0) + n_ind;
-    const int jb = static_cast<int>(Nj * blockIdx.x / gridDim.x);
-    const int je = static_cast<int>(Nj * (blockIdx.x + 1) / gridDim.x);
-    if (jb >= je) return;
+    const int Nj = (has_pre ? 1 : 0) + n_ind;
+    const int G = gridDim.x;
+    if (static_cast<int>(blockIdx.x) >= Nj) return;
 
     auto job_range = [&](int q, int& lo, int& e0, int& e1) {
         if (has_pre && q == 0) {
@@ -628,16 +734,18 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             e0 = e1 = p;
         }
     };
-    // issue stream: (iq, is_) = next r row to load
-    int iq = jb, is_, ilo, ie0, ie1;
+    // issue stream (thread 0): (iq, is_) = next r row to load
+    int iq = blockIdx.x, is_ = 0, ilo = 0, ie0 = 0, ie1 = -1;
     job_range(iq, ilo, ie0, ie1);
     is_ = ilo;
-    auto issue_next = [&](int buf) {  // thread 0 only
-        if (iq >= je) return;
-        mbar_expect_tx(&barA[buf], bytes);
-        tma_load_2d(bufA[buf], &tm_r, 0, (is_ - a.x1_base) * R, &barA[buf]);
+    auto issue_next = [&](int buf) {
+        if (iq >= Nj) return;
+        uint64_t* bar = buf ? barA1 : barA0;
+        mbar_expect_tx(bar, bytes);
+        tma_load_2d(buf ? bufA1 : bufA0, &tm_r, 0, (is_ - a.x1_base) * R, bar);
         if (++is_ > ie1) {
-            if (++iq < je) {
+            iq += G;
+            if (iq < Nj) {
                 job_range(iq, ilo, ie0, ie1);
                 is_ = ilo;
             }
@@ -650,17 +758,23 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     int cb = 0;  // buffer of the next row to consume
     double x[L];
     auto consume = [&](bool add) {
-        mbar_wait(&barA[cb], phA[cb]);
-        phA[cb] ^= 1;
-        if (add) row_acc<L>(bufA[cb], x, ln.s, pitch, false);
-        else row_load<L>(bufA[cb], x, ln.s, pitch);
+        if (cb) {
+            mbar_wait(barA1, ph1);
+            ph1 ^= 1;
+        } else {
+            mbar_wait(barA0, ph0);
+            ph0 ^= 1;
+        }
+        const char* buf = cb ? bufA1 : bufA0;
+        if (add) row_acc<L>(buf, x, ln, false);
+        else row_load<L>(buf, x, ln);
         fence_proxy_async();  // generic reads before the TMA refill (WAR)
         __syncthreads();
         if (t == 0) issue_next(cb);
         cb ^= 1;
     };
 
-    for (int q = jb; q < je; ++q) {
+    for (int q = blockIdx.x; q < Nj; q += G) {
         int lo, e0, e1;
         job_range(q, lo, e0, e1);
         consume(false);  // e = r_lo
@@ -679,10 +793,10 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 mbar_wait(barS, phS);
                 phS ^= 1;
                 double y[L];
-                row_load<L>(bufS, y, ln.s, pitch);
+                row_load<L>(bufS, y, ln);
 #pragma unroll
                 for (int e = 0; e < L; ++e) y[e] += x[e];
-                row_store<L>(bufS, y, ln.s, pitch);
+                row_store<L>(bufS, y, ln);
                 fence_proxy_async();
                 __syncthreads();
                 if (t == 0) {
@@ -715,10 +829,11 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                        const __grid_constant__ CUtensorMap tm_x3,
                        const __grid_constant__ CUtensorMap tm_out) {
     extern __shared__ unsigned char smem_raw[];
-    char* base = align1k(smem_raw);
+    char* base = smem_base(smem_raw);
     const int pitch = a.co.pitch;
     const int rb = row_bytes_al(pitch);
-    char* bufO[2] = {base, base + rb};
+    char* bufO0 = base;
+    char* bufO1 = base + rb;
     char* bufA1 = base + 2 * rb;
     char* bufA2 = base + 3 * rb;
     char* bufA3 = base + 4 * rb;
@@ -733,7 +848,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     Lane<L> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
-    tabs_init(tb, a.co);
+    tabs_init(tb, sl, a.co);
     if (t == 0) {
         mbar_init(barA, 1);
         mbar_fence_init();
@@ -744,14 +859,12 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 
     const bool has_pre = (a.kind == WK_FAS || a.kind == WK_FORWARD) && (a.pre_e1 >= a.pre_e0);
     const int n_ind = max(0, a.p1 - a.p0 + 1);
-    const long long Nj = (has_pre ? 1 : 0) + n_ind;
-    const int jb = static_cast<int>(Nj * blockIdx.x / gridDim.x);
-    const int je = static_cast<int>(Nj * (blockIdx.x + 1) / gridDim.x);
+    const int Nj = (has_pre ? 1 : 0) + n_ind;
     double x[L];
 
     auto emit_store = [&](int row) {
-        char* o = bufO[ob];
-        row_store<L>(o, x, ln.s, pitch);
+        char* o = ob ? bufO1 : bufO0;
+        row_store<L>(o, x, ln);
         fence_proxy_async();
         __syncthreads();
         if (t == 0) {
@@ -761,7 +874,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         ob ^= 1;
     };
 
-    for (int q = jb; q < je; ++q) {
+    for (int q = blockIdx.x; q < Nj; q += gridDim.x) {
         if (a.kind == WK_APPLY || a.kind == WK_FAS_RHS) {
             const int p = a.p0 + q;
             const int src = (a.kind == WK_FAS_RHS) ? p - 1 : p + a.seed_off;
@@ -783,21 +896,21 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 #pragma unroll
                 for (int e = 0; e < L; ++e) x[e] = 0.0;
             } else {
-                row_load<L>(bufA1, x, ln.s, pitch);
+                row_load<L>(bufA1, x, ln);
             }
             if (t == 0) bulk_wait_read<1>();
             phi<L>(x, a.co, ln, tb, sl, a.idx0 + p, a.forced);
             if (a.kind == WK_FAS_RHS) {
                 // g_j = (v_j - Psi_j(v_{j-1})) + r_j  (solver.cpp:214-218)
                 double y[L];
-                row_load<L>(bufA2, y, ln.s, pitch);
+                row_load<L>(bufA2, y, ln);
 #pragma unroll
                 for (int e = 0; e < L; ++e) y[e] -= x[e];
-                row_acc<L>(bufA3, y, ln.s, pitch, false);
+                row_acc<L>(bufA3, y, ln, false);
 #pragma unroll
                 for (int e = 0; e < L; ++e) x[e] = y[e];
             }
-            emit_store(p);
+            emit_store(p);  // its fence + barrier also release bufA*
             continue;
         }
 
@@ -821,10 +934,10 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         mbar_wait(barA, phA);
         phA ^= 1;
         if (fas) {
-            row_load<L>(bufA2, x, ln.s, pitch);        // v_lo
-            row_acc<L>(bufA1, x, ln.s, pitch, false);  // + r_lo
+            row_load<L>(bufA2, x, ln);         // v_lo
+            row_acc<L>(bufA1, x, ln, false);   // + r_lo
         } else {
-            row_load<L>(bufA1, x, ln.s, pitch);
+            row_load<L>(bufA1, x, ln);
         }
         fence_proxy_async();
         __syncthreads();
@@ -842,9 +955,9 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 mbar_wait(barA, phA);
                 phA ^= 1;
                 // next = Psi(u) + v_s - Psi(v_{s-1}) + r_s  (kernels.cpp:69-74)
-                row_acc<L>(bufA2, x, ln.s, pitch, false);
-                row_acc<L>(bufA3, x, ln.s, pitch, true);
-                row_acc<L>(bufA1, x, ln.s, pitch, false);
+                row_acc<L>(bufA2, x, ln, false);
+                row_acc<L>(bufA3, x, ln, true);
+                row_acc<L>(bufA1, x, ln, false);
                 fence_proxy_async();
                 __syncthreads();
             }
@@ -866,9 +979,7 @@ size_t heat_window_smem(const WindowArgs& a) {
     int rows;
     if (a.kind == WK_LINEAR) rows = 3;
     else rows = (a.kind == WK_FAS || a.kind == WK_FAS_RHS) ? 5 : 3;
-    size_t pad = 0;
-    if (const char* e = std::getenv("ATM_WIN_PAD")) pad = static_cast<size_t>(std::atoi(e)) * 1024;
-    return pad + 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) + sizeof(Slots);
+    return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) + sizeof(Slots);
 }
 
 namespace {
