@@ -264,3 +264,34 @@ def test_config5_shape_reduced_single_iteration():
         want.append(orc.residual_norm())
     assert np.allclose(got, want, rtol=1e-9, atol=0)
     assert rel_l2(drv.get_level(0), orc.array(0)) <= SOLVE_RTOL
+
+
+@pytest.mark.parametrize("k", [2, 4, 8, 12, 64, 128])
+def test_heat_k_study_iteration_counts(k):
+    # acceptance.cpp:158-201 (criterion 3), counts 45/24/14/14/14/14
+    _golden_solve(f"kstudy_k{k}")
+
+
+@pytest.mark.parametrize("k", [4, 8, 1025])
+def test_config5_shape_iteration_counts(k):
+    # BASELINE config 5 discretisation (n=4095, m=16) at N_t = 2^14, tol 1e-10:
+    # same iteration count as the compiled reference and history within 1e-9
+    _golden_solve(f"config5r_k{k}")
+
+
+def test_config5_shape_bitwise_across_shard_counts():
+    case = golden_cases()["config5r_k8"]
+    ic = golden_array("config5r_k8", "ic")
+    args = dict(case["args"], max_iters=6, tol=1e-300)
+    base = None
+    for workers in (1, 2, 4, 8):
+        app, hier, cfg = device_objects(args, ic=ic)
+        drv = T.CycleDriver(app, hier, cfg, workers=workers)
+        drv.setup()
+        norms = drv.iterate(6)
+        u = drv.get_level(0, first=16000, count=385)
+        if base is None:
+            base = (norms, u)
+            continue
+        assert np.array_equal(norms, base[0]), workers
+        assert np.array_equal(u, base[1]), workers
