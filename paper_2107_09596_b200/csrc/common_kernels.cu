@@ -119,27 +119,53 @@ int launch_row_sum(double* g, const double* v, const double* r, int n, cudaStrea
     return static_cast<int>(cudaGetLastError());
 }
 
-// Fixed association: thread t sums the contiguous chunk t of 1024 chunks in
-// index order, then a fixed binary tree.  Depends only on `count`, so every
-// shard decomposition yields the same bits (cf. parallel.cpp:279-295).
-__global__ void norm_kernel(const double* sq, int count, double* out) {
-    __shared__ double part[1024];
+// Fixed association in two stages: block b sums slice b of 256 equal slices
+// (thread t takes elements t, t+256, ... of the slice in order, then a fixed
+// binary tree), the last block to finish sums the 256 partials the same way.
+// Depends only on `count`, so every shard decomposition yields the same bits
+// (the reference sums in point order for the same reason, parallel.cpp:279-295).
+constexpr int kNormBlocks = 256;
+
+__device__ double block_tree_sum(double s, double* part) {
     const int t = threadIdx.x;
-    const long long lo = static_cast<long long>(count) * t / 1024;
-    const long long hi = static_cast<long long>(count) * (t + 1) / 1024;
-    double s = 0.0;
-    for (long long i = lo; i < hi; ++i) s += sq[i];
     part[t] = s;
     __syncthreads();
-    for (int w = 512; w >= 1; w >>= 1) {
+    for (int w = blockDim.x / 2; w >= 1; w >>= 1) {
         if (t < w) part[t] = part[t] + part[t + w];
         __syncthreads();
     }
-    if (t == 0) out[0] = sqrt(part[0]);
+    return part[0];
+}
+
+__global__ void norm_kernel(const double* sq, int count, double* partials, unsigned* ticket,
+                            double* out) {
+    __shared__ double part[256];
+    __shared__ bool last;
+    const long long lo = static_cast<long long>(count) * blockIdx.x / kNormBlocks;
+    const long long hi = static_cast<long long>(count) * (blockIdx.x + 1) / kNormBlocks;
+    double s = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) s += sq[i];
+    const double tot = block_tree_sum(s, part);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = tot;
+        __threadfence();
+        last = (atomicAdd(ticket, 1u) == kNormBlocks - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const double v = reinterpret_cast<volatile double*>(partials)[threadIdx.x];
+    const double all = block_tree_sum(v, part);
+    if (threadIdx.x == 0) {
+        out[0] = sqrt(all);
+        *ticket = 0;  // ready for the next launch (stream-ordered)
+    }
 }
 
 int launch_norm_from_squares(const double* sq, int count, double* out, cudaStream_t s) {
-    norm_kernel<<<1, 1024, 0, s>>>(sq, count, out);
+    // out[0] = norm; out[8..8+256) partials; the ticket lives at out[4]
+    norm_kernel<<<kNormBlocks, 256, 0, s>>>(sq, count, out + 8, reinterpret_cast<unsigned*>(out + 4),
+                                           out);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -479,6 +479,9 @@ void Engine::build_coefs(Shard& s) {
             c.cneg_c = hh.cneg_c;
             c.sigma = hh.sigma;
             c.ncw = hh.ncw;
+            c.corr_dot = std::getenv("ATM_CORR_DOT") ? 1 : 0;
+            // timing experiments only (wrong numerics): drop the boundary correction
+            if (std::getenv("ATM_DEBUG_NOCORR")) c.ncw = 0;
             c.n = n_;
             c.pitch = pitch_;
             c.nt = hh.nt;

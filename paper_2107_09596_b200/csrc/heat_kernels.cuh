@@ -43,6 +43,7 @@ struct HeatCoefDev {
     double beta_c, gamma_c, cneg_c;  // fixed-point factors: 1/d*, r/d*, -c*
     double sigma;          // Sherman-Morrison scale
     int ncw;               // warps that carry the rank-1 correction
+    int corr_dot;          // 1: g . b partial sums before the barrier (else x_c[0] broadcast)
     int n, pitch, nt, L;
     int substeps;
 };

@@ -284,6 +284,7 @@ struct Slots {                // small shared scratch
     double ta[2][kMaxWarps];  // backward warp totals, C_w-free part
     double gd[2][kMaxWarps];  // g . b partial sums of the correction warps
     double red[kMaxWarps];
+    double xc0;               // (M^{-1} b)_0 shared among the correction warps
     uint64_t bar[4];
 };
 
@@ -315,9 +316,9 @@ __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L>& ln) 
 template <int L>
 __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
                                           const Tabs& tb, Slots& sl) {
-    // 0. g . b partial: only when the correction spans several warps (with a
-    //    single correction warp, x_c[0] is thread 0's own result, see 6.)
-    const bool dot = ln.corr && co.ncw > 1;
+    // 0. g . b partial: only in the dot-product variant of the correction
+    //    (ATM_CORR_DOT); by default x_c[0] is thread 0's own result after 6.
+    const bool dot = ln.corr && co.ncw > 1 && co.corr_dot;
     double gd = 0.0;
     if (dot) {
         const double* gt = co.corr_g + ln.s;
@@ -406,8 +407,13 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
         if (dot) {
             g0 = 0.0;
             for (int w = 0; w < co.ncw; ++w) g0 += sl.gd[par][w];
-        } else {
+        } else if (co.ncw == 1) {
             g0 = __shfl_sync(0xffffffffu, x[0], 0);  // (M^{-1} b)_0 held by thread 0
+        } else {
+            // only the correction warps meet here (named barrier 1)
+            if (ln.t == 0) sl.xc0 = x[0];
+            asm volatile("bar.sync 1, %0;" ::"r"(co.ncw * 32) : "memory");
+            g0 = sl.xc0;
         }
         const double ms = -co.sigma * g0;
         const double* wt = co.corr_w + ln.s;
