@@ -60,6 +60,25 @@ CUtensorMap make_row_map(double* ptr, int rows, int pitch) {
     return m;
 }
 
+// 3D view [rows][pitch/16][16 doubles], box = one warp's slice of a row
+// (32 threads x L doubles = 2L lines of 128 B), 128B swizzle; the part of a
+// box past the row end is clipped by the TMA unit.
+CUtensorMap make_slice_map(double* ptr, int rows, int pitch, int L) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    const cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(pitch / 16), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(pitch) * 8};
+    const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(std::min(2 * L, pitch / 16)), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ptr, dims, strides, box,
+                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw Error(ATM_RUNTIME_FAULT, "cuTensorMapEncodeTiled (slice) failed (" + std::to_string(r) + ")");
+    return m;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -402,6 +421,7 @@ DArr Engine::alloc_arr(LevelDev& L, int base, int rows, bool tmap) {
     a.p = static_cast<double*>(p);
     if (tmap && heat_) {
         a.tm = make_row_map(a.p, a.rows, pitch_);
+        a.tmw = make_slice_map(a.p, a.rows, pitch_, L_heat_);
         a.has_tm = true;
     }
     return a;
@@ -603,7 +623,8 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.n_out = choose_n_out(a);
         int grid = grid_for(j1 - j0, heat_sweep_occupancy(a));
         if (const char* e = std::getenv("ATM_GRID_SWEEP")) grid = std::min(grid, std::atoi(e));
-        check_launch(launch_heat_sweep(a, Lv.u.tm, tg, to, grid, st_), "heat_sweep");
+        const CUtensorMap& tow = out_lv ? out_lv->r.tmw : Lv.u.tmw;
+        check_launch(launch_heat_sweep(a, Lv.u.tm, tg, to, Lv.u.tmw, tow, grid, st_), "heat_sweep");
     } else {
         ScalarSweepArgs a{};
         a.co = Lv.sco;
@@ -1415,7 +1436,8 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
         a.n_out = choose_n_out(a);
         const int grid = grid_for(a.j1 - a.j0, heat_sweep_occupancy(a));
         if (a.j1 > a.j0)
-            check_launch(launch_heat_sweep(a, Lv.u.tm, Lv.g_full ? Lv.g.tm : Lv.u.tm, r.tm, grid, st_),
+            check_launch(launch_heat_sweep(a, Lv.u.tm, Lv.g_full ? Lv.g.tm : Lv.u.tm, r.tm, Lv.u.tmw,
+                                           r.tmw, grid, st_),
                          "resid");
     } else {
         ScalarSweepArgs a{};

@@ -77,7 +77,8 @@ struct DArr {
     double* p = nullptr;
     int base = 0;   // global index of row 0
     int rows = 0;
-    CUtensorMap tm{};
+    CUtensorMap tm{};   // one point row per box
+    CUtensorMap tmw{};  // one warp slice of a row per box (per-warp stores)
     bool has_tm = false;
     bool valid(int i) const { return p && i >= base && i < base + rows; }
 };

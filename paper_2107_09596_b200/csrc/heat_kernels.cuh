@@ -95,7 +95,8 @@ struct WindowArgs {
 
 // Launchers (stream-ordered).  Return cudaError_t as int.
 int launch_heat_sweep(const SweepArgs& args, const CUtensorMap& tm_u, const CUtensorMap& tm_g,
-                      const CUtensorMap& tm_out, int grid, cudaStream_t s);
+                      const CUtensorMap& tm_out, const CUtensorMap& tm_uw,
+                      const CUtensorMap& tm_outw, int grid, cudaStream_t s);
 int launch_heat_window(const WindowArgs& args, const CUtensorMap& tm_x1, const CUtensorMap& tm_x2,
                        const CUtensorMap& tm_x3, const CUtensorMap& tm_out, int grid,
                        cudaStream_t s);

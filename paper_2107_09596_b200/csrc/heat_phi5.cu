@@ -527,7 +527,12 @@ template <int L, int NTMAX, int MINB>
 __global__ void __launch_bounds__(NTMAX, MINB)
     heat_sweep_kernel(const __grid_constant__ SweepArgs a, const __grid_constant__ CUtensorMap tm_u,
                       const __grid_constant__ CUtensorMap tm_g,
-                      const __grid_constant__ CUtensorMap tm_out) {
+                      const __grid_constant__ CUtensorMap tm_out,
+                      const __grid_constant__ CUtensorMap tm_uw,
+                      const __grid_constant__ CUtensorMap tm_outw) {
+    // L >= 4: every warp stores its own 1024-aligned slice of a row with its
+    // own TMA store (no CTA barrier per produced row); L = 2: whole-row store
+    constexpr bool kWarpStore = (L >= 4);
     extern __shared__ unsigned char smem_raw[];
     char* base = smem_base(smem_raw);
     const int pitch = a.co.pitch;
@@ -568,16 +573,32 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 
     // stage x into an output buffer and TMA-store it; the store that last
     // read that buffer was waited for (bulk_wait_read) before the Phi
-    auto stage_out = [&](int row, const CUtensorMap* map) {
+    auto stage_out = [&](int row, const CUtensorMap* map, const CUtensorMap* mapw) {
         char* o = ob ? bufO1 : bufO0;
         row_store<L>(o, x, ln);
         fence_proxy_async();
-        __syncthreads();
-        if (t == 0) {
-            tma_store_2d(map, 0, row * R, o);
-            bulk_commit();
+        if constexpr (kWarpStore) {
+            __syncwarp();
+            if (ln.lane == 0 && ln.warp * 32 * L < pitch) {
+                tma_store_3d(mapw, 0, ln.warp * 2 * L, row, o + ln.warp * 256 * L);
+                bulk_commit();
+            }
+        } else {
+            __syncthreads();
+            if (t == 0) {
+                tma_store_2d(map, 0, row * R, o);
+                bulk_commit();
+            }
         }
         ob = (nob == 2) ? ob ^ 1 : 0;
+    };
+    // the issuer(s) of the stores that last read the staging buffer about to
+    // be written wait for those reads; the Phi barrier orders the rest
+    auto release_staging = [&]() {
+        if (kWarpStore ? (ln.lane == 0) : (t == 0)) {
+            if (nob == 2) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+        }
     };
 
     for (int J = jb; J < je; ++J) {
@@ -633,10 +654,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 mbar_expect_tx(barA, bytes);
                 tma_load_2d(bufA, &tm_g, 0, (i - a.g_base) * R, barA);
             }
-            if (t == 0) {
-                if (nob == 2) bulk_wait_read<1>();
-                else bulk_wait_read<0>();
-            }
+            release_staging();
             phi<L>(x, a.co, ln, tb, sl, i, a.forced);
             if (a.add_g) {
                 mbar_wait(barA, phA);
@@ -644,7 +662,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 row_acc<L>(bufA, x, ln, false);
             }
             if (a.store && i >= store_from) {
-                stage_out(i - a.u_base, &tm_u);
+                stage_out(i - a.u_base, &tm_u, &tm_uw);
             } else if (a.add_g) {
                 fence_proxy_async();
                 __syncthreads();  // bufA consumed before the next load
@@ -657,10 +675,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 mbar_expect_tx(barA, bytes);
                 tma_load_2d(bufA, &tm_g, 0, (tail_i - a.g_base) * R, barA);
             }
-            if (t == 0) {
-                if (nob == 2) bulk_wait_read<1>();
-                else bulk_wait_read<0>();
-            }
+            release_staging();
             phi<L>(x, a.co, ln, tb, sl, tail_i, a.forced);
             if (a.add_g) {
                 mbar_wait(barA, phA);
@@ -672,14 +687,14 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             row_acc<L>(bufS, x, ln, true);
             if (a.kind == SW_F && J + 1 < je) seed_ready = true;  // S holds u[c_{J+1}]
             if (a.tail == TAIL_STORE) {
-                stage_out(tail_i / m - a.out_base, &tm_out);
+                stage_out(tail_i / m - a.out_base, &tm_out, &tm_outw);
             } else {
                 const double tot = cta_sum_squares<L>(x, ln, sl);
                 if (t == 0) a.sq[tail_i - a.sq_base] = tot;
             }
         }
     }
-    if (t == 0) bulk_wait<0>();
+    if (kWarpStore ? (ln.lane == 0) : (t == 0)) bulk_wait<0>();
 }
 
 // --------------------------------------------------------------------------
@@ -1055,11 +1070,12 @@ int heat_window_occupancy(const WindowArgs& a) {
 }
 
 int launch_heat_sweep(const SweepArgs& a, const CUtensorMap& u, const CUtensorMap& g,
-                      const CUtensorMap& o, int grid, cudaStream_t s) {
+                      const CUtensorMap& o, const CUtensorMap& uw, const CUtensorMap& ow, int grid,
+                      cudaStream_t s) {
     if (grid <= 0) return 0;
     SweepArgs aa = a;
-    CUtensorMap tu = u, tg = g, to = o;
-    void* args[] = {&aa, &tu, &tg, &to};
+    CUtensorMap tu = u, tg = g, to = o, tuw = uw, tow = ow;
+    void* args[] = {&aa, &tu, &tg, &to, &tuw, &tow};
     return launch(select(a.co.L).sweep, grid, a.co.nt, heat_sweep_smem(a), s, args);
 }
 
