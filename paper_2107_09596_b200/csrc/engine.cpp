@@ -487,8 +487,10 @@ void Engine::build_coefs(Shard& s) {
         if (heat_) {
             const HeatLevelHost hh = heat_level_host(n_, pitch_, L_heat_, sub_dt, h_, S);
             HeatCoefDev& c = Lv.hco;
-            c.corr_g = up(hh.corr_g);
-            c.corr_w = up(hh.corr_w);
+            if (!(hh.fit_err <= 1e-13))
+                throw Error(ATM_RUNTIME_FAULT, "heat Phi: boundary-correction carries do not "
+                                               "reproduce w (rel err " +
+                                                   std::to_string(hh.fit_err) + ")");
             c.scan = up(hh.scan);
             c.wf = up(hh.wf);
             c.wb = up(hh.wb);
@@ -499,7 +501,6 @@ void Engine::build_coefs(Shard& s) {
             c.cneg_c = hh.cneg_c;
             c.sigma = hh.sigma;
             c.ncw = hh.ncw;
-            c.corr_dot = std::getenv("ATM_CORR_DOT") ? 1 : 0;
             // timing experiments only (wrong numerics): drop the boundary correction
             if (std::getenv("ATM_DEBUG_NOCORR")) c.ncw = 0;
             c.n = n_;

@@ -18,7 +18,7 @@ namespace atm {
 constexpr int kMaxThreads = 512;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr int kMaxL = 16;
-constexpr int kScanPerThread = 16;  // Mf[5], Pf_ex, Mb[5], Pb_ex, SB, q0, pad
+constexpr int kScanPerThread = 16;  // Mf[5], Pf_ex, Mb[5], Pb_ex, SB, q0, cfw, cbw
 
 // Device view of one level's Phi coefficients.
 //
@@ -27,13 +27,14 @@ constexpr int kScanPerThread = 16;  // Mf[5], Pf_ex, Mb[5], Pb_ex, SB, q0, pad
 // (c*, d*) of the Thomas recurrence everywhere except entry (0,0):
 //     T = M + delta e0 e0^T,  delta = a c*.
 // Phi is therefore computed as x = M^{-1} b - s w with w = M^{-1} e0,
-// s = sigma (g . b), g = M^{-T} e0, sigma = delta / (1 + delta w0)
-// (Sherman-Morrison).  w and g decay geometrically from index 0, so only
-// the first `ncw` warps touch them.
+// s = sigma x0, x0 = (M^{-1} b)_0, sigma = delta / (1 + delta w0)
+// (Sherman-Morrison: g . b = (M^{-1} b)_0 for g = M^{-T} e0).  On every
+// thread's chunk w lies in span{q, p_b} -- the two vectors the blocked solve
+// already combines -- so the correction only shifts the chunk's two carry
+// coefficients by (-s) * (cfw, cbw).  w decays geometrically from index 0:
+// only the first `ncw` warps apply it.
 struct HeatCoefDev {
-    const double* corr_g;  // [nt*L] g = M^{-T} e0 (0 past the decay cut-off)
-    const double* corr_w;  // [nt*L] w = M^{-1} e0 (0 past the cut-off and beyond n)
-    const double* scan;    // [nt][16] per-thread scan multipliers
+    const double* scan;    // [nt][16] per-thread scan multipliers + (cfw, cbw)
     const double* wf;      // [kMaxWarps][kMaxWarps] cross-warp carry weights (forward)
     const double* wb;      // [kMaxWarps][kMaxWarps] (backward)
     const double* wk;      // [kMaxWarps][kMaxWarps] forward-into-backward coupling weights
@@ -43,15 +44,15 @@ struct HeatCoefDev {
     double beta_c, gamma_c, cneg_c;  // fixed-point factors: 1/d*, r/d*, -c*
     double sigma;          // Sherman-Morrison scale
     int ncw;               // warps that carry the rank-1 correction
-    int corr_dot;          // 1: g . b partial sums before the barrier (else x_c[0] broadcast)
     int n, pitch, nt, L;
     int substeps;
 };
 
 // Host-side construction of a level's coefficients (heat1d.cpp:24-45).
 struct HeatLevelHost {
-    std::vector<double> corr_g, corr_w, scan, wf, wb, wk, powc;
+    std::vector<double> scan, wf, wb, wk, powc;
     double r = 0, beta_c = 0, gamma_c = 0, cneg_c = 0, sigma = 0;
+    double fit_err = 0;  // max |w - (cfw q + cbw p_b)| / max |w| over the correction chunks
     int ncw = 0, n = 0, pitch = 0, nt = 0, L = 0, substeps = 1;
 };
 HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, int substeps);

@@ -75,36 +75,25 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
     H.beta_c = static_cast<double>(1.0L / d);
     H.gamma_c = static_cast<double>(r / d);
     H.cneg_c = static_cast<double>(-c);
-    // correction vectors: w = M^{-1} e0 (L_c: d* diag, a sub; U_c: 1 diag, c* super)
-    std::vector<LD> w(n), v(n), g(n);
+    // correction vector w = M^{-1} e0 (L_c: d* diag, a sub; U_c: 1 diag,
+    // c* super); yf keeps the forward (L_c^{-1}) values: the carries into
+    // every chunk
+    std::vector<LD> w(n), yf(n);
     {
         LD p = 0.0L;
         for (int i = 0; i < n; ++i) {
             p = ((i == 0 ? 1.0L : 0.0L) - a * p) / d;
-            w[i] = p;
+            yf[i] = w[i] = p;
         }
         for (int i = n - 2; i >= 0; --i) w[i] -= c * w[i + 1];
-        // g = M^{-T} e0: U_c^T v = e0, then L_c^T g = v
-        v[0] = 1.0L;
-        for (int i = 1; i < n; ++i) v[i] = -c * v[i - 1];
-        for (int i = n - 1; i >= 0; --i) g[i] = (v[i] - (i + 1 < n ? a * g[i + 1] : 0.0L)) / d;
     }
     const LD delta = a * c;
     H.sigma = static_cast<double>(delta / (1.0L + delta * w[0]));
-    LD wmax = 0.0L, gmax = 0.0L;
-    for (int i = 0; i < n; ++i) {
-        wmax = std::max(wmax, std::fabs(w[i]));
-        gmax = std::max(gmax, std::fabs(g[i]));
-    }
-    int K = 0;  // past K both vectors are below 1e-20 of their peak
+    LD wmax = 0.0L;
+    for (int i = 0; i < n; ++i) wmax = std::max(wmax, std::fabs(w[i]));
+    int K = 0;  // past K, w is below 1e-20 of its peak
     for (int i = 0; i < n; ++i)
-        if (std::fabs(w[i]) > 1e-20L * wmax || std::fabs(g[i]) > 1e-20L * gmax) K = i + 1;
-    H.corr_w.assign(npad, 0.0);
-    H.corr_g.assign(npad, 0.0);
-    for (int i = 0; i < K; ++i) {
-        H.corr_w[i] = static_cast<double>(w[i]);
-        H.corr_g[i] = static_cast<double>(g[i]);
-    }
+        if (std::fabs(w[i]) > 1e-20L * wmax) K = i + 1;
     H.ncw = (K + 32 * L - 1) / (32 * L);
     // effective per-element coefficients; padding elements (>= n) carry
     // gamma = 0 so no forward carry crosses them
@@ -203,6 +192,30 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
             sc[13] = q0[32 * wi + l];
         }
     }
+    // w on chunk t is cfw_t q_t + cbw_t p_b: cfw_t = the forward carry into
+    // the chunk (for t = 0 the local forward of e0 is beta gamma^e = (beta /
+    // gamma) p_f), cbw_t = w at the first element of the next chunk
+    {
+        LD err = 0.0L;
+        const int tl = (n - 1) / L;
+        for (int t = 0; t < nt && t * L < n; ++t) {
+            const LD cf = (t == 0) ? 1.0L / r : yf[t * L - 1];
+            const LD cb = ((t + 1) * L < n) ? w[(t + 1) * L] : 0.0L;
+            double* sc = &H.scan[static_cast<size_t>(t) * kScanPerThread];
+            if (t < 32 * H.ncw) {
+                sc[14] = static_cast<double>(cf);
+                sc[15] = static_cast<double>(cb);
+            }
+            const int ne = std::min(L, n - t * L);
+            for (int e = 0; e < ne; ++e) {
+                const LD qe = (t == tl) ? static_cast<LD>(H.powc[2 * kMaxL + e])
+                                        : static_cast<LD>(H.powc[e]);
+                const LD fit = cf * qe + cb * static_cast<LD>(H.powc[kMaxL + e]);
+                err = std::max(err, std::fabs(fit - w[t * L + e]));
+            }
+        }
+        H.fit_err = static_cast<double>(err / wmax);
+    }
     // cross-warp weights (zero outside the causal range)
     H.wf.assign(kMaxWarps * kMaxWarps, 0.0);
     H.wb.assign(kMaxWarps * kMaxWarps, 0.0);
@@ -241,7 +254,8 @@ struct Lane {
     int pad0;            // first padding element of the chunk, L if none
     int par;             // parity of the warp-total slots (one barrier per Phi)
     bool corr, inside;   // carries the rank-1 correction; chunk inside the row
-    double Mf[5], Pfex, Mb[5], Pbex, SB, q0, lm, rm;
+    double Mf[5], Pfex, Mb[5], Pbex, SB, q0;
+    double cfw, cbw;     // correction carries of the chunk
 };
 
 template <int L>
@@ -268,8 +282,8 @@ __device__ __forceinline__ void lane_init(Lane<L>& ln, const HeatCoefDev& co) {
     ln.Pbex = __ldg(sc + 11);
     ln.SB = __ldg(sc + 12);
     ln.q0 = __ldg(sc + 13);
-    ln.lm = ln.lane > 0 ? 1.0 : 0.0;
-    ln.rm = ln.lane < 31 ? 1.0 : 0.0;
+    ln.cfw = ln.corr ? __ldg(sc + 14) : 0.0;
+    ln.cbw = ln.corr ? __ldg(sc + 15) : 0.0;
 }
 
 struct Tabs {              // per-CTA copy of the level's small tables
@@ -277,14 +291,14 @@ struct Tabs {              // per-CTA copy of the level's small tables
     double wb[kMaxWarps * kMaxWarps];
     double wk[kMaxWarps * kMaxWarps];
     double powc[3 * kMaxL];  // q, p_b of interior threads; q of the padded last thread
+    double pbex0;            // thread 0's Pb_ex
 };
 
 struct Slots {                // small shared scratch
     double tf[2][kMaxWarps];  // forward warp totals (double-buffered by Phi parity)
     double ta[2][kMaxWarps];  // backward warp totals, C_w-free part
-    double gd[2][kMaxWarps];  // g . b partial sums of the correction warps
     double red[kMaxWarps];
-    double xc0;               // (M^{-1} b)_0 shared among the correction warps
+    double z0[2], ra0[2];     // thread 0's z_loc[0] and RA_next (ncw > 1)
     uint64_t bar[4];
 };
 
@@ -295,11 +309,11 @@ __device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev
         tb.wk[i] = co.wk[i];
     }
     for (int i = threadIdx.x; i < 3 * kMaxL; i += blockDim.x) tb.powc[i] = co.powc[i];
+    if (threadIdx.x == 0) tb.pbex0 = co.scan[11];
     // warp slots beyond the CTA are read with zero weights: keep them finite
     for (int i = threadIdx.x; i < 2 * kMaxWarps; i += blockDim.x) {
         sl.tf[i / kMaxWarps][i % kMaxWarps] = 0.0;
         sl.ta[i / kMaxWarps][i % kMaxWarps] = 0.0;
-        sl.gd[i / kMaxWarps][i % kMaxWarps] = 0.0;
     }
 }
 
@@ -316,27 +330,6 @@ __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L>& ln) 
 template <int L>
 __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
                                           const Tabs& tb, Slots& sl) {
-    // 0. g . b partial: only in the dot-product variant of the correction
-    //    (ATM_CORR_DOT); by default x_c[0] is thread 0's own result after 6.
-    const bool dot = ln.corr && co.ncw > 1 && co.corr_dot;
-    double gd = 0.0;
-    if (dot) {
-        const double* gt = co.corr_g + ln.s;
-        if constexpr (L >= 4) {
-            double g1 = 0.0, g2 = 0.0, g3 = 0.0;
-#pragma unroll
-            for (int e = 0; e < L; e += 4) {
-                gd = fma(__ldg(gt + e), x[e], gd);
-                g1 = fma(__ldg(gt + e + 1), x[e + 1], g1);
-                g2 = fma(__ldg(gt + e + 2), x[e + 2], g2);
-                g3 = fma(__ldg(gt + e + 3), x[e + 3], g3);
-            }
-            gd = (gd + g1) + (g2 + g3);
-        } else {
-#pragma unroll
-            for (int e = 0; e < L; ++e) gd = fma(__ldg(gt + e), x[e], gd);
-        }
-    }
     // 1. forward local  y_i = beta x_i + gamma y_{i-1}
     double y = 0.0;
     {
@@ -353,7 +346,8 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     double B = y;
 #pragma unroll
     for (int d = 0; d < 5; ++d) B = fma(ln.Mf[d], __shfl_up_sync(0xffffffffu, B, 1 << d), B);
-    const double E = __shfl_up_sync(0xffffffffu, B, 1) * ln.lm;
+    double E = __shfl_up_sync(0xffffffffu, B, 1);
+    if (ln.lane == 0) E = 0.0;
     // 3. backward local on the uncorrected forward values
     double z = 0.0;
     {
@@ -368,57 +362,65 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     double R = fma(E, ln.q0, z);
 #pragma unroll
     for (int d = 0; d < 5; ++d) R = fma(ln.Mb[d], __shfl_down_sync(0xffffffffu, R, 1 << d), R);
-    const double RAn = __shfl_down_sync(0xffffffffu, R, 1) * ln.rm;
-    if (dot) {
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) gd += __shfl_xor_sync(0xffffffffu, gd, off);
-    }
-    // 5. publish warp totals; one barrier; cross-warp carries
+    double RAn = __shfl_down_sync(0xffffffffu, R, 1);
+    if (ln.lane == 31) RAn = 0.0;
+    // 5. publish warp totals; one barrier; cross-warp carries.  The
+    //    correction needs x0 = (M^{-1} b)_0 = z0 + c_b(thread 0) p_b[0]
+    //    (thread 0 has no forward carry), c_b(thread 0) = Pb_ex0 D_0 + RA0:
+    //    thread 0's z0 and RA0 travel by shuffle (ncw == 1) or smem.
     const int par = ln.par;
     if (ln.lane == 31) sl.tf[par][ln.warp] = B;
     if (ln.lane == 0) sl.ta[par][ln.warp] = R;
-    if (dot && ln.lane == 1) sl.gd[par][ln.warp] = gd;
+    const bool far = ln.corr && ln.warp > 0;  // correction warp without warp 0's D
+    double z00 = 0.0, ra0 = 0.0;
+    if (co.ncw > 1) {
+        if (ln.t == 0) {
+            sl.z0[par] = x[0];
+            sl.ra0[par] = RAn;
+        }
+    } else if (ln.corr) {
+        z00 = __shfl_sync(0xffffffffu, x[0], 0);
+        ra0 = __shfl_sync(0xffffffffu, RAn, 0);
+    }
     __syncthreads();
     ln.par ^= 1;
-    double cC, cD;
+    double cC, cD, cD0 = 0.0;
     {
         const int v = ln.lane & (kMaxWarps - 1);
         const double tf = sl.tf[par][v], ta = sl.ta[par][v];
         const int row = ln.warp * kMaxWarps + v;
         cC = tb.wf[row] * tf;
         cD = fma(tb.wb[row], ta, tb.wk[row] * tf);
+        if (far) cD0 = fma(tb.wb[v], ta, tb.wk[v] * tf);
 #pragma unroll
         for (int off = kMaxWarps / 2; off >= 1; off >>= 1) {
             cC += __shfl_xor_sync(0xffffffffu, cC, off);
             cD += __shfl_xor_sync(0xffffffffu, cD, off);
         }
+        if (far) {
+#pragma unroll
+            for (int off = kMaxWarps / 2; off >= 1; off >>= 1)
+                cD0 += __shfl_xor_sync(0xffffffffu, cD0, off);
+        }
     }
-    const double cf = fma(ln.Pfex, cC, E);
-    const double cb = fma(ln.Pbex, cD, fma(ln.SB, cC, RAn));
-    // 6. x = z_loc + c_f q + c_b p_b (- s w)
+    double cf = fma(ln.Pfex, cC, E);
+    double cb = fma(ln.Pbex, cD, fma(ln.SB, cC, RAn));
+    if (ln.corr) {
+        if (co.ncw > 1) {
+            z00 = sl.z0[par];
+            ra0 = sl.ra0[par];
+        }
+        const double x0 = fma(fma(tb.pbex0, far ? cD0 : cD, ra0), tb.powc[kMaxL], z00);
+        const double ms = -co.sigma * x0;
+        cf = fma(ms, ln.cfw, cf);
+        cb = fma(ms, ln.cbw, cb);
+    }
+    // 6. x = z_loc + c_f q + c_b p_b
     {
         const double* qv = (ln.pad0 < L) ? tb.powc + 2 * kMaxL : tb.powc;
 #pragma unroll
         for (int e = 0; e < L; ++e) x[e] = fma(cb, tb.powc[kMaxL + e], fma(cf, qv[e], x[e]));
         zero_padding<L>(x, ln);
-    }
-    if (ln.corr) {
-        double g0;
-        if (dot) {
-            g0 = 0.0;
-            for (int w = 0; w < co.ncw; ++w) g0 += sl.gd[par][w];
-        } else if (co.ncw == 1) {
-            g0 = __shfl_sync(0xffffffffu, x[0], 0);  // (M^{-1} b)_0 held by thread 0
-        } else {
-            // only the correction warps meet here (named barrier 1)
-            if (ln.t == 0) sl.xc0 = x[0];
-            asm volatile("bar.sync 1, %0;" ::"r"(co.ncw * 32) : "memory");
-            g0 = sl.xc0;
-        }
-        const double ms = -co.sigma * g0;
-        const double* wt = co.corr_w + ln.s;
-#pragma unroll
-        for (int e = 0; e < L; ++e) x[e] = fma(ms, __ldg(wt + e), x[e]);
     }
 }
 
