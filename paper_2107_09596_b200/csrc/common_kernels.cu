@@ -241,7 +241,7 @@ __global__ void scalar_sweep_kernel(ScalarSweepArgs a) {
     for (int i = start + 1; i <= end; ++i) {
         x = sc_phi(a.co, i, x);
         if (a.add_g) x += a.g[i - a.g_base];
-        if (a.store && i >= store_from) a.u[i - a.u_base] = x;
+        if (i >= store_from && store_row(a.store, i, m)) a.u[i - a.u_base] = x;
     }
     if (a.tail != TAIL_NONE && end + 1 <= last && ((end + 1) % m) == 0) {
         const int ti = end + 1;

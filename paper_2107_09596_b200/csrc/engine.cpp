@@ -596,7 +596,7 @@ void Engine::phase_end() {
 
 // sweep jobs [j0, j1) on one shard/level
 void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail, int m_override,
-                        double* sq, int sq_base) {
+                        double* sq, int sq_base, int store) {
     if (j1 <= j0) return;
     LevelDev& Lv = s.lv[level];
     const int m = m_override > 0 ? m_override : H_.m[level];
@@ -614,7 +614,7 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.g_base = add_g ? Lv.g.base : 0;
         a.add_g = add_g;
         a.forced = folded_ && prob_.manufactured;
-        a.store = 1;
+        a.store = store;
         a.tail = tail;
         a.out_base = out_lv ? out_lv->r.base : 0;
         a.sq = sq;
@@ -639,7 +639,7 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.g = add_g ? Lv.g.p : nullptr;
         a.g_base = add_g ? Lv.g.base : 0;
         a.add_g = add_g;
-        a.store = 1;
+        a.store = store;
         a.tail = tail;
         a.out = out_lv ? out_lv->r.p : nullptr;
         a.out_base = out_lv ? out_lv->r.base : 0;
@@ -903,7 +903,7 @@ void Engine::point0_residual(Shard& s, int level, double* r_out, double* sq_out)
 }
 
 // F-relaxation over own intervals (kernels.cpp:7-17) with optional tail
-void Engine::f_sweep(int level, int tail, int /*out_level*/) {
+void Engine::f_sweep(int level, int tail, int store) {
     halo(level, &LevelDev::u);
     const char* tag = level != 0 ? nullptr : tail == TAIL_SQ ? "sweep_correct"
                                            : tail == TAIL_STORE ? "sweep_relax" : "sweep_f";
@@ -912,16 +912,19 @@ void Engine::f_sweep(int level, int tail, int /*out_level*/) {
         LevelDev& Lv = s.lv[level];
         if (Lv.iv_count == 0) continue;
         sweep_jobs(s, level, SW_F, Lv.iv_first, Lv.iv_first + Lv.iv_count, tail, 0,
-                   tail == TAIL_SQ ? d_sq_c_ : nullptr, 0);
+                   tail == TAIL_SQ ? d_sq_c_ : nullptr, 0, store);
     }
     if (tag) phase_end();
 }
 
 // relax_level (solver.cpp:160-172).  With F-relaxation the restriction
 // residuals are produced by the sweep's tail.
-void Engine::relax_level(int level, bool restrict_tail) {
+void Engine::relax_level(int level, bool restrict_tail, bool f_dead) {
+    // F rows a later pass still reads: none with F-relaxation (the residual
+    // comes from the sweep's tail), the last F row of every interval otherwise
+    const int fst = !f_dead ? STORE_ALL : sol_.relaxation == ATM_RELAX_F ? STORE_NONE : STORE_CF;
     if (sol_.relaxation == ATM_RELAX_F) {
-        f_sweep(level, restrict_tail ? TAIL_STORE : TAIL_NONE, level + 1);
+        f_sweep(level, restrict_tail ? TAIL_STORE : TAIL_NONE, fst);
         return;
     }
     if (sol_.nu == 1) {
@@ -932,7 +935,7 @@ void Engine::relax_level(int level, bool restrict_tail) {
             LevelDev& Lv = s.lv[level];
             if (Lv.c_count == 0) continue;
             int j1 = Lv.c_first + Lv.c_count;
-            sweep_jobs(s, level, SW_FCF, Lv.c_first, j1, TAIL_NONE, 0, nullptr, 0);
+            sweep_jobs(s, level, SW_FCF, Lv.c_first, j1, TAIL_NONE, 0, nullptr, 0, fst);
         }
         if (G_ > 1) {
             // the first interval of a shard waits for its left neighbour's new C
@@ -940,19 +943,20 @@ void Engine::relax_level(int level, bool restrict_tail) {
             for (Shard& s : sh_) {
                 LevelDev& Lv = s.lv[level];
                 if (Lv.iv_count == 0 || Lv.iv_first >= Lv.c_first) continue;
-                sweep_jobs(s, level, SW_F, Lv.iv_first, Lv.iv_first + 1, TAIL_NONE, 0, nullptr, 0);
+                sweep_jobs(s, level, SW_F, Lv.iv_first, Lv.iv_first + 1, TAIL_NONE, 0, nullptr, 0,
+                           fst);
             }
         }
         return;
     }
-    f_sweep(level, TAIL_NONE, level + 1);
+    f_sweep(level, TAIL_NONE, fst);
     for (int it = 0; it < sol_.nu; ++it) {
         for (Shard& s : sh_) {
             LevelDev& Lv = s.lv[level];
             const int j0 = std::max(1, Lv.c_first), j1 = Lv.c_first + Lv.c_count;
             sweep_jobs(s, level, SW_CRELAX, j0, j1, TAIL_NONE, 0, nullptr, 0);
         }
-        f_sweep(level, TAIL_NONE, level + 1);
+        f_sweep(level, TAIL_NONE, fst);
     }
 }
 
@@ -1076,7 +1080,7 @@ void Engine::correct_from(int level) {
         check_launch(launch_c_correct(F.u.p, F.u.base, m, C.u.p, C.v.p, C.u.base, pitch_, n_,
                                       F.c_first, F.c_first + F.c_count, st_), "c_correct");
     }
-    f_sweep(level, level == 0 ? TAIL_SQ : TAIL_NONE, level + 1);
+    f_sweep(level, level == 0 ? TAIL_SQ : TAIL_NONE);
     if (level == 0)
         for (Shard& s : sh_) point0_residual(s, 0, d_row_, d_sq_c_);
 }
@@ -1088,7 +1092,7 @@ void Engine::v_cycle(int level) {
         return;
     }
     phase_begin("relax");
-    relax_level(level, sol_.relaxation == ATM_RELAX_F);
+    relax_level(level, sol_.relaxation == ATM_RELAX_F, true);
     phase_end();
     phase_begin("restrict");
     restrict_to(level);
@@ -1102,7 +1106,7 @@ void Engine::v_cycle(int level) {
 void Engine::two_level_cycle() {
     // solver.cpp:305-320
     phase_begin("relax");
-    relax_level(0, sol_.relaxation == ATM_RELAX_F);
+    relax_level(0, sol_.relaxation == ATM_RELAX_F, true);
     phase_end();
     phase_begin("restrict");
     if (sol_.relaxation != ATM_RELAX_F) resid_c(0);
@@ -1110,7 +1114,7 @@ void Engine::two_level_cycle() {
     phase_end();
     coarsest_linear();
     phase_begin("correct");
-    f_sweep(0, TAIL_SQ, 1);
+    f_sweep(0, TAIL_SQ);
     for (Shard& s : sh_) point0_residual(s, 0, d_row_, d_sq_c_);
     phase_end();
 }
@@ -1187,7 +1191,7 @@ void Engine::nested_init() {
                                  rowb * m, C.u.p + static_cast<size_t>(F.c_first - C.u.base) * pitch_,
                                  rowb, rowb, F.c_count, cudaMemcpyDeviceToDevice, st_));
         }
-        f_sweep(l, TAIL_NONE, l + 1);
+        f_sweep(l, TAIL_NONE);
         if (l >= 1) v_cycle(l);
     }
     CK(cudaStreamSynchronize(st_));
@@ -1431,7 +1435,7 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
         a.add_g = Lv.g_full;
         a.g_base = Lv.g_full ? Lv.g.base : 0;
         a.forced = folded_ && prob_.manufactured;
-        a.store = 1;
+        a.store = STORE_ALL;
         a.tail = TAIL_STORE;
         a.out_base = first;
         a.n_out = choose_n_out(a);

@@ -140,10 +140,13 @@ private:
     void fill_initial_guess();
     void fill_level_rhs(int level);
     // cycle pieces
-    void relax_level(int level, bool restrict_tail);
-    void f_sweep(int level, int tail, int out_level);
+    // f_dead: the cycle's correction F-sweep rewrites every F row of the
+    // level before anything reads it, so only C rows and the rows a later
+    // residual / C-relaxation reads are stored (STORE_CF / STORE_NONE)
+    void relax_level(int level, bool restrict_tail, bool f_dead);
+    void f_sweep(int level, int tail, int store = STORE_ALL);
     void sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail, int m_override,
-                    double* sq, int sq_base);
+                    double* sq, int sq_base, int store = STORE_ALL);
     void resid_c(int level);  // r at own C (j>=1) of level into level+1 r, plus r_0
     void restrict_to(int level);
     void coarsest_linear();

@@ -60,6 +60,10 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
 // Job kinds of the sweep kernel (one job per C-point index J of a level).
 enum SweepKind { SW_F = 0, SW_FCF = 1, SW_CRELAX = 2, SW_RESID = 3 };
 enum TailKind { TAIL_NONE = 0, TAIL_STORE = 1, TAIL_SQ = 2 };
+enum StoreKind { STORE_NONE = 0, STORE_ALL = 1, STORE_CF = 2 };
+__host__ __device__ inline bool store_row(int mode, int i, int m) {
+    return mode == STORE_ALL || (mode == STORE_CF && (i % m == 0 || (i + 1) % m == 0));
+}
 
 struct SweepArgs {
     HeatCoefDev co;
@@ -70,7 +74,9 @@ struct SweepArgs {
     int g_base;        // global index of row 0 of the g array
     int add_g;         // u_i = Phi(u_{i-1}) + g_i with g stored per point
     int forced;        // Phi includes forcing (folded manufactured)
-    int store;         // store produced points (full storage)
+    int store;         // STORE_ALL, or STORE_CF: only C rows and the last F row of
+                       // each interval (the rest are rewritten by the cycle's
+                       // correction F-sweep before anything reads them)
     int tail;          // TailKind: residual at the next C-point
     int out_base;      // global (coarse) index of row 0 of the tail target
     double* sq;        // per-point squares (TAIL_SQ), indexed by tail point - sq_base

@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 phA ^= 1;
                 row_acc<L>(bufA, x, ln, false);
             }
-            if (a.store && i >= store_from) {
+            if (i >= store_from && store_row(a.store, i, m)) {
                 stage_out(i - a.u_base, &tm_u, &tm_uw);
             } else if (a.add_g) {
                 fence_proxy_async();
