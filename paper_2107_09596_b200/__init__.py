@@ -5,7 +5,7 @@ host runtime behind the C ABI in include/atmgrit.h).  This package is the
 reference-shaped Python binding used by tests and the benchmark.
 """
 from .api import (  # noqa: F401
-    Application, ConfigError, ConvergenceReport, CycleDriver, CycleMode, Dahlquist,
+    AllenCahn, Application, ConfigError, ConvergenceReport, CycleDriver, CycleMode, Dahlquist,
     DivergenceError, Heat1D, Hierarchy, InitialGuess, NonlinearSolveError, NormKind,
     Relaxation, RuntimeFault, ScalarLinear, SolveResult, SolverConfig, StopReason, TimeGrid,
     build_comm_groups, build_hierarchy, build_layout, make_cf_split, random_state,

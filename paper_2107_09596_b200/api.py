@@ -327,6 +327,41 @@ class ScalarLinear(Application):
         return p
 
 
+class AllenCahn(Application):
+    """1D Allen-Cahn u_t = eps^2 u_xx + u - u^3, periodic on [0, length)
+    (BASELINE config 3; no reference Phi, see oracle/atm_oracle.c ac_step).
+    Backward Euler per sub-step, Newton with the stopping rule of
+    gray_scott.cpp:113 (stop = max(tol, tol |F_0|)) and its iteration cap
+    (NonlinearSolveError, gray_scott.cpp:165-169).  Forcing is folded (zero)."""
+    kind = 4
+
+    def __init__(self, n=4096, eps=0.02, length=1.0, newton_tol=1e-12, newton_max=30,
+                 initial_condition=None):
+        if n < 16 or n % 8 or n > 4096:
+            raise ConfigError("allen-cahn: n must be a multiple of 8 in [16, 4096]")
+        if not (eps > 0.0 and length > 0.0):
+            raise ConfigError("allen-cahn: bad eps/length")
+        self.n, self.eps, self.length = n, eps, length
+        self.newton_tol, self.newton_max = newton_tol, newton_max
+        self.ic = None if initial_condition is None else np.ascontiguousarray(initial_condition, np.float64)
+
+    def vector_size(self):
+        return self.n
+
+    def forcing_folded(self):
+        return True
+
+    def c_problem(self, keep):
+        p = _capi.atm_problem()
+        p.kind, p.n, p.folded = self.kind, self.n, 1
+        p.eps, p.length = self.eps, self.length
+        p.newton_tol, p.newton_max = self.newton_tol, self.newton_max
+        if self.ic is not None:
+            keep.append(self.ic)
+            p.ic = ptr(self.ic)
+        return p
+
+
 # ---------------------------------------------------------------------------
 # the driver
 

@@ -280,6 +280,17 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
                 config_error("scalar: one multiplier per level");
             break;
         case ATM_PHI_ALLEN_CAHN:
+            // BASELINE config 3 (no reference Phi; oracle/atm_oracle.c ac_step)
+            n_ = p.n;
+            if (n_ < 16 || n_ % 8 != 0 || n_ > 4096)
+                config_error("allen-cahn: n must be a multiple of 8 in [16, 4096]");
+            if (!(p.eps > 0.0) || !(p.length > 0.0)) config_error("allen-cahn: bad eps/length");
+            if (!(p.newton_tol > 0.0) || p.newton_max < 1)
+                config_error("allen-cahn: newton_tol > 0 and newton_max >= 1 required");
+            heat_ = true;  // row kernels
+            ac_ = true;
+            folded_ = true;
+            break;
         case ATM_PHI_HEAT2D:
             config_error("Phi family not available in this build");
         default:
@@ -303,12 +314,12 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     pitch_ = heat_ ? ((n_ + 15) / 16) * 16 : 1;
     // host copies of caller-owned inputs
     ic_.assign(n_, 0.0);
-    if (heat_) {
+    if (heat_ && !ac_) {
         h_ = (p.x1 - p.x0) / static_cast<double>(n_ + 1);  // heat1d.cpp:16
         sinp_.resize(n_);
         for (int i = 0; i < n_; ++i) sinp_[i] = std::sin(kPi * (p.x0 + h_ * (i + 1)));
         ic_ = sinp_;  // heat1d.cpp:85-91
-    } else {
+    } else if (!ac_) {
         ic_[0] = p.u0;
     }
     if (p.ic) ic_.assign(p.ic, p.ic + n_);
@@ -333,7 +344,8 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     G_ = world_ > 1 ? world_ : local;
     lay_ = build_layout(H_, G_);
     trace_ = rt.trace != 0;
-    if (const char* e = std::getenv("ATM_HEAT_L")) L_heat_ = std::atoi(e);
+    if (ac_) L_heat_ = 8;
+    else if (const char* e = std::getenv("ATM_HEAT_L")) L_heat_ = std::atoi(e);
     else {
         L_heat_ = 2;
         while (L_heat_ < 16 && pitch_ / L_heat_ > 256) L_heat_ *= 2;
@@ -380,6 +392,7 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     d_prevf_ = dalloc(sizeof(double) * np0);
     d_ic_ = dalloc(sizeof(double) * pitch_);
     d_row_ = dalloc(sizeof(double) * pitch_);
+    d_fail_ = reinterpret_cast<int*>(dalloc(sizeof(int) * 4));
     CK(cudaMemcpy(d_ic_, ic_.data(), sizeof(double) * n_, cudaMemcpyHostToDevice));
     if (!fw_.empty()) {
         d_fw_ = dalloc(sizeof(double) * n_);
@@ -450,7 +463,7 @@ void Engine::alloc_shard(Shard& s) {
         // g: full per-point array where forcing is stored, else point 0 only
         bool g_full = false;
         if (l == 0 && !folded_) {
-            const bool heat_forced = heat_ && prob_.manufactured;
+            const bool heat_forced = heat_ && !ac_ && prob_.manufactured;
             const bool scalar_forced = (kind_ == ATM_PHI_SCALAR) && !ff_.empty();
             g_full = heat_forced || scalar_forced;
         }
@@ -485,8 +498,35 @@ void Engine::build_coefs(Shard& s) {
             return static_cast<const double*>(p);
         };
         if (heat_) {
-            const HeatLevelHost hh = heat_level_host(n_, pitch_, L_heat_, sub_dt, h_, S);
+            // Allen-Cahn: the Newton inner solve uses the shifted linear part
+            // A_s = tridiag(-dt c, 1 + 2 dt c - dt + s, -dt c), cyclic
+            const double ac_c = ac_ ? prob_.eps * prob_.eps /
+                                          ((prob_.length / n_) * (prob_.length / n_))
+                                    : 0.0;
+            const double ac_s = 1.5 * sub_dt;
+            const HeatLevelHost hh =
+                ac_ ? heat_level_host(n_, pitch_, L_heat_, sub_dt * ac_c, ac_s - sub_dt, S, true)
+                    : heat_level_host(n_, pitch_, L_heat_, sub_dt / (h_ * h_), 0.0, S, false);
             HeatCoefDev& c = Lv.hco;
+            c.xw = up(hh.xw);
+            c.cyclic = hh.cyclic;
+            c.ncw_r0 = hh.ncw_r0;
+            c.tl = hh.tl;
+            c.pl = hh.pl;
+            for (int q = 0; q < 4; ++q) c.S[q] = hh.S[q];
+            c.ql = hh.ql;
+            c.pbl = hh.pbl;
+            c.prob = ac_ ? 1 : 0;
+            if (ac_) {
+                c.ac_dt = sub_dt;
+                c.ac_c = ac_c;
+                c.ac_shift = ac_s;
+                c.newton_tol = prob_.newton_tol;
+                c.newton_max = prob_.newton_max;
+                c.ac_umax2 = 1.0;
+                c.inner_eta = 1e-15;
+                c.fail = d_fail_;
+            }
             if (!(hh.fit_err <= 1e-13))
                 throw Error(ATM_RUNTIME_FAULT, "heat Phi: boundary-correction carries do not "
                                                "reproduce w (rel err " +
@@ -508,7 +548,7 @@ void Engine::build_coefs(Shard& s) {
             c.nt = hh.nt;
             c.L = hh.L;
             c.substeps = S;
-            if (prob_.manufactured) {
+            if (prob_.manufactured && !ac_) {
                 // theta per (index, substep): heat1d.cpp:72-75 evaluated on the host
                 const int np = H_.np[l];
                 std::vector<double> th(static_cast<size_t>(np) * S, 0.0);
@@ -1125,6 +1165,21 @@ void Engine::cycle() {
     if (sol_.mode == ATM_TWO_LEVEL) two_level_cycle();
     else v_cycle(0);
     last_launches_ = launches_;
+    check_newton();
+}
+
+// NonlinearSolveError (gray_scott.cpp:165-169 analogue): a Newton solve hit
+// newton_max somewhere in the last batch of Allen-Cahn Phi applications
+void Engine::check_newton() {
+    if (!ac_) return;
+    int f = 0;
+    CK(cudaMemcpyAsync(&f, d_fail_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    if (f) {
+        CK(cudaMemsetAsync(d_fail_, 0, sizeof(int), st_));
+        throw Error(ATM_NONLINEAR_FAIL, "allen-cahn: Newton did not converge in " +
+                                            std::to_string(prob_.newton_max) + " iterations");
+    }
 }
 
 void Engine::nested_init() {
@@ -1195,6 +1250,7 @@ void Engine::nested_init() {
         if (l >= 1) v_cycle(l);
     }
     CK(cudaStreamSynchronize(st_));
+    check_newton();
 }
 
 double Engine::residual_norm() {
@@ -1399,6 +1455,7 @@ void Engine::apply_phi(int level, int first, int count, const double* in, double
     CK(cudaStreamSynchronize(st_));
     (void)save;
     for (void* p : tmp.allocs) cudaFree(p);
+    check_newton();
 }
 
 void Engine::kernel_f_relax(int level, int first_iv, int count) {
@@ -1406,6 +1463,7 @@ void Engine::kernel_f_relax(int level, int first_iv, int count) {
     setup();
     sweep_jobs(sh_[0], level, SW_F, first_iv, first_iv + count, TAIL_NONE, 0, nullptr, 0);
     CK(cudaStreamSynchronize(st_));
+    check_newton();
 }
 
 void Engine::kernel_c_relax(int level, int first_c, int count) {
@@ -1414,6 +1472,7 @@ void Engine::kernel_c_relax(int level, int first_c, int count) {
     sweep_jobs(sh_[0], level, SW_CRELAX, std::max(1, first_c), first_c + count, TAIL_NONE, 0,
                nullptr, 0);
     CK(cudaStreamSynchronize(st_));
+    check_newton();
 }
 
 void Engine::kernel_residual(int level, int first, int count, double* out) {

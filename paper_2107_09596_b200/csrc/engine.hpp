@@ -180,7 +180,7 @@ private:
     Hier H_;
     Layout lay_;
     int n_ = 1, pitch_ = 1, kind_ = 0;
-    bool folded_ = false, heat_ = false;
+    bool folded_ = false, heat_ = false, ac_ = false;
     int L_heat_ = 16;
     int sms_ = 148;
     int world_ = 1, rank_ = 0, G_ = 1;
@@ -201,6 +201,8 @@ private:
     double* d_row_ = nullptr;
     double* d_ff_ = nullptr;
     double* d_prof_ = nullptr;
+    int* d_fail_ = nullptr;   // Allen-Cahn Newton failure flag
+    void check_newton();
     std::vector<void*> gallocs_;
     // NCCL (world > 1)
     std::unique_ptr<NcclApi> nccl_;

@@ -18,7 +18,7 @@ namespace atm {
 constexpr int kMaxThreads = 512;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr int kMaxL = 16;
-constexpr int kScanPerThread = 16;  // Mf[5], Pf_ex, Mb[5], Pb_ex, SB, q0, cfw, cbw
+constexpr int kScanPerThread = 18;  // Mf[5], Pf_ex, Mb[5], Pb_ex, SB, q0, cfw, cbw, pad, cbwr
 
 // Device view of one level's Phi coefficients.
 //
@@ -43,19 +43,34 @@ struct HeatCoefDev {
     const double* prof;    // [nt*L] forcing profile sin(pi x_i) or null
     double beta_c, gamma_c, cneg_c;  // fixed-point factors: 1/d*, r/d*, -c*
     double sigma;          // Sherman-Morrison scale
-    int ncw;               // warps that carry the rank-1 correction
+    int ncw;               // warps [0, ncw) carry the left correction vector
+    int ncw_r0;            // cyclic: warps [ncw_r0, nw) carry the right one
+    // cyclic (periodic) matrices: Woodbury capacitance S (2x2) and the
+    // x_{n-1} pick-up of thread tl (element pl-1)
+    int cyclic, tl, pl;
+    double S[4], ql, pbl;
+    const double* xw;      // [4][kMaxWarps] x0 / xn weights of the warp totals
+    // Allen-Cahn Newton (prob == 1): F(u) = u - dt (c D2 u + u - u^3) - u_prev
+    int prob;              // 0 heat, 1 Allen-Cahn
+    int newton_max;
+    double ac_dt, ac_c, ac_shift, newton_tol, ac_umax2, inner_eta;
+    int* fail;             // set to 1 when Newton hits newton_max
     int n, pitch, nt, L;
     int substeps;
 };
 
 // Host-side construction of a level's coefficients (heat1d.cpp:24-45).
 struct HeatLevelHost {
-    std::vector<double> scan, wf, wb, wk, powc;
+    std::vector<double> scan, wf, wb, wk, powc, xw;
     double r = 0, beta_c = 0, gamma_c = 0, cneg_c = 0, sigma = 0;
+    double S[4] = {0, 0, 0, 0}, ql = 0, pbl = 0;
+    int cyclic = 0, ncw_r0 = 0, tl = 0, pl = 0;
     double fit_err = 0;  // max |w - (cfw q + cbw p_b)| / max |w| over the correction chunks
     int ncw = 0, n = 0, pitch = 0, nt = 0, L = 0, substeps = 1;
 };
-HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, int substeps);
+// r = sub_dt/h^2 (a = -r, diagonal 1 + 2r + shift); cyclic: periodic corners
+HeatLevelHost heat_level_host(int n, int pitch, int L, double r, double shift, int substeps,
+                              bool cyclic);
 
 // Job kinds of the sweep kernel (one job per C-point index J of a level).
 enum SweepKind { SW_F = 0, SW_FCF = 1, SW_CRELAX = 2, SW_RESID = 3 };

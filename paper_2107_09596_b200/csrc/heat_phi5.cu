@@ -55,30 +55,34 @@ namespace atm {
 // --------------------------------------------------------------------------
 // host: fixed-point factors, correction vectors and every scan multiplier
 
-HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, int substeps) {
+HeatLevelHost heat_level_host(int n, int pitch, int L, double r_in, double shift, int substeps,
+                              bool cyclic) {
     using LD = long double;
     HeatLevelHost H;
     H.n = n;
     H.pitch = pitch;
     H.L = L;
     H.substeps = substeps;
+    H.cyclic = cyclic ? 1 : 0;
     const int nt = ((pitch + L - 1) / L + 127) / 128 * 128;
     H.nt = nt;
     const int npad = nt * L;
-    // heat1d.cpp:28-31: r = sub_dt/h^2, a = -r, b = 1 + 2r
-    H.r = sub_dt / (h * h);
+    // heat1d.cpp:28-31: r = sub_dt/h^2, a = -r, b = 1 + 2r (+ shift: the
+    // Allen-Cahn linear part 1 + 2r - dt + s)
+    H.r = r_in;
     const LD r = static_cast<LD>(H.r);
-    const LD a = -r, b = 1.0L + 2.0L * r;
+    const LD a = -r, b = 1.0L + 2.0L * r + static_cast<LD>(shift);
     // fixed point of c = a / (b - a c): the root of a c^2 - b c + a with |c| < 1
-    const LD c = 2.0L * a / (b + std::sqrt(1.0L + 4.0L * r));
+    const LD disc = (shift == 0.0) ? 1.0L + 4.0L * r : b * b - 4.0L * r * r;
+    const LD c = 2.0L * a / (b + std::sqrt(disc));
     const LD d = b - a * c;
     H.beta_c = static_cast<double>(1.0L / d);
     H.gamma_c = static_cast<double>(r / d);
     H.cneg_c = static_cast<double>(-c);
-    // correction vector w = M^{-1} e0 (L_c: d* diag, a sub; U_c: 1 diag,
-    // c* super); yf keeps the forward (L_c^{-1}) values: the carries into
-    // every chunk
-    std::vector<LD> w(n), yf(n);
+    // correction vectors: wl = M^{-1} e0 (L_c: d* diag, a sub; U_c: 1 diag,
+    // c* super), yf its forward (L_c^{-1}) values = the carries into every
+    // chunk; cyclic: wr = M^{-1} e_{n-1} = (-c)^{n-1-i} / d
+    std::vector<LD> w(n), yf(n), wr(n, 0.0L);
     {
         LD p = 0.0L;
         for (int i = 0; i < n; ++i) {
@@ -86,15 +90,43 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
             yf[i] = w[i] = p;
         }
         for (int i = n - 2; i >= 0; --i) w[i] -= c * w[i + 1];
+        if (cyclic) {
+            LD q = 1.0L / d;
+            for (int i = n - 1; i >= 0; --i) {
+                wr[i] = q;
+                q *= -c;
+            }
+        }
     }
+    // Woodbury: T = M + U C U^T, U = [e0, e_{n-1}], C = [[delta, a], [a, 0]]
+    // (cyclic) or U = e0, C = delta; T^{-1} b = M^{-1} b - W S U^T M^{-1} b,
+    // S = (C^{-1} + U^T W)^{-1}
     const LD delta = a * c;
     H.sigma = static_cast<double>(delta / (1.0L + delta * w[0]));
-    LD wmax = 0.0L;
-    for (int i = 0; i < n; ++i) wmax = std::max(wmax, std::fabs(w[i]));
-    int K = 0;  // past K, w is below 1e-20 of its peak
+    H.S[0] = H.sigma;
+    H.S[1] = H.S[2] = H.S[3] = 0.0;
+    if (cyclic) {
+        const LD m00 = w[0], m01 = 1.0L / a + wr[0];
+        const LD m10 = 1.0L / a + w[n - 1], m11 = -delta / (a * a) + wr[n - 1];
+        const LD det = m00 * m11 - m01 * m10;
+        H.S[0] = static_cast<double>(m11 / det);
+        H.S[1] = static_cast<double>(-m01 / det);
+        H.S[2] = static_cast<double>(-m10 / det);
+        H.S[3] = static_cast<double>(m00 / det);
+    }
+    LD wmax = 0.0L, wrmax = 0.0L;
+    for (int i = 0; i < n; ++i) {
+        wmax = std::max(wmax, std::fabs(w[i]));
+        wrmax = std::max(wrmax, std::fabs(wr[i]));
+    }
+    int K = 0, KR = n;  // below 1e-20 of the peak past K (wl) and before KR (wr)
     for (int i = 0; i < n; ++i)
         if (std::fabs(w[i]) > 1e-20L * wmax) K = i + 1;
+    if (cyclic)
+        for (int i = n - 1; i >= 0; --i)
+            if (std::fabs(wr[i]) > 1e-20L * wrmax) KR = i;
     H.ncw = (K + 32 * L - 1) / (32 * L);
+    H.ncw_r0 = cyclic ? KR / (32 * L) : kMaxWarps;
     // effective per-element coefficients; padding elements (>= n) carry
     // gamma = 0 so no forward carry crosses them
     std::vector<double> eg(npad), ec(npad);
@@ -192,29 +224,37 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
             sc[13] = q0[32 * wi + l];
         }
     }
-    // w on chunk t is cfw_t q_t + cbw_t p_b: cfw_t = the forward carry into
+    // wl on chunk t is cfw_t q_t + cbw_t p_b: cfw_t = the forward carry into
     // the chunk (for t = 0 the local forward of e0 is beta gamma^e = (beta /
-    // gamma) p_f), cbw_t = w at the first element of the next chunk
+    // gamma) p_f = -p_f / a), cbw_t = wl at the first element of the next
+    // chunk; wr on chunk t is cbwr_t p_b
     {
         LD err = 0.0L;
         const int tl = (n - 1) / L;
+        const int pl = n - tl * L;
         for (int t = 0; t < nt && t * L < n; ++t) {
-            const LD cf = (t == 0) ? 1.0L / r : yf[t * L - 1];
+            const LD cf = (t == 0) ? -1.0L / a : yf[t * L - 1];
             const LD cb = ((t + 1) * L < n) ? w[(t + 1) * L] : 0.0L;
+            const LD cbr = !cyclic ? 0.0L
+                           : (t < tl) ? wr[(t + 1) * L]
+                                      : wr[n - 1] / static_cast<LD>(H.powc[kMaxL + pl - 1]);
             double* sc = &H.scan[static_cast<size_t>(t) * kScanPerThread];
-            if (t < 32 * H.ncw) {
+            const int wt = t / 32;
+            if (wt < H.ncw || wt >= H.ncw_r0) {
                 sc[14] = static_cast<double>(cf);
                 sc[15] = static_cast<double>(cb);
+                sc[17] = static_cast<double>(cbr);
             }
             const int ne = std::min(L, n - t * L);
             for (int e = 0; e < ne; ++e) {
                 const LD qe = (t == tl) ? static_cast<LD>(H.powc[2 * kMaxL + e])
                                         : static_cast<LD>(H.powc[e]);
-                const LD fit = cf * qe + cb * static_cast<LD>(H.powc[kMaxL + e]);
-                err = std::max(err, std::fabs(fit - w[t * L + e]));
+                const LD pe = static_cast<LD>(H.powc[kMaxL + e]);
+                err = std::max(err, std::fabs(cf * qe + cb * pe - w[t * L + e]) / wmax);
+                if (cyclic) err = std::max(err, std::fabs(cbr * pe - wr[t * L + e]) / wrmax);
             }
         }
-        H.fit_err = static_cast<double>(err / wmax);
+        H.fit_err = static_cast<double>(err);
     }
     // cross-warp weights (zero outside the causal range)
     H.wf.assign(kMaxWarps * kMaxWarps, 0.0);
@@ -241,6 +281,30 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double sub_dt, double h, 
                 k += H.wb[wi * kMaxWarps + vv] * TB[vv] * H.wf[vv * kMaxWarps + u];
             H.wk[wi * kMaxWarps + u] = k;
         }
+    // cyclic: x0 = (M^{-1} b)_0 and xn = (M^{-1} b)_{n-1} as fixed combinations
+    // of the published warp totals and of thread 0's / thread tl's scalars:
+    //   x0 = z0 + pb0 (Pb_ex0 D_0 + RA0),  D_w = sum_v wb[w][v] TA_v + wk[w][v] Tf_v
+    //   xn = zl + ql (Pf_ex,tl C_wl + E_tl) + pbl (Pb_ex,tl D_wl + SB_tl C_wl + RA_tl)
+    H.xw.assign(4 * kMaxWarps, 0.0);
+    if (cyclic) {
+        const int tl = (n - 1) / L, wl = tl / 32, pl = n - tl * L;
+        const size_t KS = kScanPerThread;
+        const double pb0 = H.powc[kMaxL], pbex0 = H.scan[11];
+        const double ql = (pl < L) ? H.powc[2 * kMaxL + pl - 1] : H.powc[pl - 1];
+        const double pbl = H.powc[kMaxL + pl - 1];
+        const double pfe = H.scan[tl * KS + 5], pbe = H.scan[tl * KS + 11], sbl = H.scan[tl * KS + 12];
+        for (int v = 0; v < nw; ++v) {
+            H.xw[v] = pb0 * pbex0 * H.wk[v];
+            H.xw[kMaxWarps + v] = pb0 * pbex0 * H.wb[v];
+            H.xw[2 * kMaxWarps + v] = (ql * pfe + pbl * sbl) * H.wf[wl * kMaxWarps + v] +
+                                      pbl * pbe * H.wk[wl * kMaxWarps + v];
+            H.xw[3 * kMaxWarps + v] = pbl * pbe * H.wb[wl * kMaxWarps + v];
+        }
+        H.tl = tl;
+        H.pl = pl;
+        H.ql = ql;
+        H.pbl = pbl;
+    }
     return H;
 }
 
@@ -253,9 +317,10 @@ struct Lane {
     int q7, qx, ch0;     // swizzled row-staging geometry of this chunk
     int pad0;            // first padding element of the chunk, L if none
     int par;             // parity of the warp-total slots (one barrier per Phi)
-    bool corr, inside;   // carries the rank-1 correction; chunk inside the row
+    bool corr, inside;   // carries the boundary correction; chunk inside the row
     double Mf[5], Pfex, Mb[5], Pbex, SB, q0;
-    double cfw, cbw;     // correction carries of the chunk
+    double cfw, cbw;     // correction carries of the chunk (left vector)
+    double cbwr;         // cyclic: right correction vector's p_b coefficient
 };
 
 template <int L>
@@ -265,7 +330,7 @@ __device__ __forceinline__ void lane_init(Lane<L>& ln, const HeatCoefDev& co) {
     ln.warp = ln.t >> 5;
     ln.nw = blockDim.x >> 5;
     ln.s = ln.t * L;
-    ln.corr = ln.warp < co.ncw;
+    ln.corr = ln.warp < co.ncw || ln.warp >= co.ncw_r0;
     ln.inside = ln.s < co.pitch;  // chunks never straddle pitch (pitch % 16 == 0)
     ln.q7 = (ln.s >> 4) << 7;
     ln.qx = (ln.s >> 4) & 7;
@@ -284,6 +349,7 @@ __device__ __forceinline__ void lane_init(Lane<L>& ln, const HeatCoefDev& co) {
     ln.q0 = __ldg(sc + 13);
     ln.cfw = ln.corr ? __ldg(sc + 14) : 0.0;
     ln.cbw = ln.corr ? __ldg(sc + 15) : 0.0;
+    ln.cbwr = ln.corr ? __ldg(sc + 17) : 0.0;
 }
 
 struct Tabs {              // per-CTA copy of the level's small tables
@@ -292,6 +358,7 @@ struct Tabs {              // per-CTA copy of the level's small tables
     double wk[kMaxWarps * kMaxWarps];
     double powc[3 * kMaxL];  // q, p_b of interior threads; q of the padded last thread
     double pbex0;            // thread 0's Pb_ex
+    double xw[4 * kMaxWarps];  // cyclic: x0 / xn weights of (Tf, TA)
 };
 
 struct Slots {                // small shared scratch
@@ -299,6 +366,8 @@ struct Slots {                // small shared scratch
     double ta[2][kMaxWarps];  // backward warp totals, C_w-free part
     double red[kMaxWarps];
     double z0[2], ra0[2];     // thread 0's z_loc[0] and RA_next (ncw > 1)
+    double zl[2], el[2], ral[2];  // cyclic: thread tl's z_loc[pl-1], E, RA_next
+    double nrm[2][kMaxWarps][2];  // Newton: per-warp residual square sums, max u^2
     uint64_t bar[4];
 };
 
@@ -310,6 +379,7 @@ __device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev
     }
     for (int i = threadIdx.x; i < 3 * kMaxL; i += blockDim.x) tb.powc[i] = co.powc[i];
     if (threadIdx.x == 0) tb.pbex0 = co.scan[11];
+    for (int i = threadIdx.x; i < 4 * kMaxWarps; i += blockDim.x) tb.xw[i] = co.xw[i];
     // warp slots beyond the CTA are read with zero weights: keep them finite
     for (int i = threadIdx.x; i < 2 * kMaxWarps; i += blockDim.x) {
         sl.tf[i / kMaxWarps][i % kMaxWarps] = 0.0;
@@ -326,8 +396,9 @@ __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L>& ln) 
     }
 }
 
-// (I + sub_dt L) x = x, in place, over the CTA (heat1d.cpp:47-60).
-template <int L>
+// (I + sub_dt L) x = x, in place, over the CTA (heat1d.cpp:47-60); CYC:
+// the periodic matrix with corner entries a (Allen-Cahn linear part).
+template <int L, bool CYC = false>
 __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
                                           const Tabs& tb, Slots& sl) {
     // 1. forward local  y_i = beta x_i + gamma y_{i-1}
@@ -371,9 +442,23 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     const int par = ln.par;
     if (ln.lane == 31) sl.tf[par][ln.warp] = B;
     if (ln.lane == 0) sl.ta[par][ln.warp] = R;
-    const bool far = ln.corr && ln.warp > 0;  // correction warp without warp 0's D
+    const bool far = !CYC && ln.corr && ln.warp > 0;  // correction warp without warp 0's D
     double z00 = 0.0, ra0 = 0.0;
-    if (co.ncw > 1) {
+    if (CYC) {
+        if (ln.t == 0) {
+            sl.z0[par] = x[0];
+            sl.ra0[par] = RAn;
+        }
+        if (ln.t == co.tl) {
+            double zl = x[0];
+#pragma unroll
+            for (int e = 1; e < L; ++e)
+                if (e == co.pl - 1) zl = x[e];
+            sl.zl[par] = zl;
+            sl.el[par] = E;
+            sl.ral[par] = RAn;
+        }
+    } else if (co.ncw > 1) {
         if (ln.t == 0) {
             sl.z0[par] = x[0];
             sl.ra0[par] = RAn;
@@ -385,6 +470,7 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     __syncthreads();
     ln.par ^= 1;
     double cC, cD, cD0 = 0.0;
+    double p0 = 0.0, pN = 0.0;
     {
         const int v = ln.lane & (kMaxWarps - 1);
         const double tf = sl.tf[par][v], ta = sl.ta[par][v];
@@ -392,6 +478,10 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
         cC = tb.wf[row] * tf;
         cD = fma(tb.wb[row], ta, tb.wk[row] * tf);
         if (far) cD0 = fma(tb.wb[v], ta, tb.wk[v] * tf);
+        if (CYC && ln.corr) {
+            p0 = fma(tb.xw[v], tf, tb.xw[kMaxWarps + v] * ta);
+            pN = fma(tb.xw[2 * kMaxWarps + v], tf, tb.xw[3 * kMaxWarps + v] * ta);
+        }
 #pragma unroll
         for (int off = kMaxWarps / 2; off >= 1; off >>= 1) {
             cC += __shfl_xor_sync(0xffffffffu, cC, off);
@@ -402,10 +492,27 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
             for (int off = kMaxWarps / 2; off >= 1; off >>= 1)
                 cD0 += __shfl_xor_sync(0xffffffffu, cD0, off);
         }
+        if (CYC && ln.corr) {
+#pragma unroll
+            for (int off = kMaxWarps / 2; off >= 1; off >>= 1) {
+                p0 += __shfl_xor_sync(0xffffffffu, p0, off);
+                pN += __shfl_xor_sync(0xffffffffu, pN, off);
+            }
+        }
     }
     double cf = fma(ln.Pfex, cC, E);
     double cb = fma(ln.Pbex, cD, fma(ln.SB, cC, RAn));
-    if (ln.corr) {
+    if (CYC) {
+        if (ln.corr) {
+            // Woodbury: s = S [x0, xn], x -= s0 wl + s1 wr
+            const double x0 = fma(tb.powc[kMaxL], sl.ra0[par], sl.z0[par]) + p0;
+            const double xn = fma(co.pbl, sl.ral[par], fma(co.ql, sl.el[par], sl.zl[par])) + pN;
+            const double s0 = fma(co.S[0], x0, co.S[1] * xn);
+            const double s1 = fma(co.S[2], x0, co.S[3] * xn);
+            cf = fma(-s0, ln.cfw, cf);
+            cb = fma(-s0, ln.cbw, fma(-s1, ln.cbwr, cb));
+        }
+    } else if (ln.corr) {
         if (co.ncw > 1) {
             z00 = sl.z0[par];
             ra0 = sl.ra0[par];
@@ -437,6 +544,122 @@ __device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, Lane<
         }
         tri_solve<L>(x, co, ln, tb, sl);
     }
+}
+
+// Allen-Cahn Phi: S backward-Euler sub-steps, each solved by Newton on
+//   F(u) = u - dt (c (u_l - 2u + u_r) + u - u^3) - u_prev   (periodic),
+//   J = A + D,  A = tridiag(-dt c, 1 + 2 dt c - dt, -dt c) cyclic, D = 3 dt u^2,
+// with the Newton stopping rule of gray_scott.cpp:113 (stop = max(tol, tol
+// |F_0|), cap -> NonlinearSolveError, :165-169).  J delta = -F is solved by
+// Richardson on the shifted constant part A_s = A + s I (the fast cyclic
+// solve): delta <- A_s^{-1}(-F - (D - s) delta), rate
+// rho <= max(s, 3 dt umax^2 - s) / (1 - dt + s), iterated to rho^K <= eta.
+// Chunk ends travel through smem (one barrier per residual); the residual
+// norm and max u^2 ride on a second barrier.
+template <int L>
+__device__ __forceinline__ void ac_residual(const double (&u)[L], const double (&up)[L],
+                                            double (&F)[L], const HeatCoefDev& co,
+                                            const Lane<L>& ln, double* ends, double& sq,
+                                            double& u2) {
+    const int nt = blockDim.x;
+    ends[ln.t] = u[0];
+    ends[nt + ln.t] = u[L - 1];
+    __syncthreads();
+    const bool real = ln.t <= co.tl;
+    const double ul = ends[nt + (ln.t == 0 ? co.tl : ln.t - 1)];
+    const double ur = ends[ln.t == co.tl ? 0 : ln.t + 1];
+    const double dt = co.ac_dt, c = co.ac_c;
+    sq = 0.0;
+    u2 = 0.0;
+#pragma unroll
+    for (int e = 0; e < L; ++e) {
+        const double a = e == 0 ? ul : u[e - 1];
+        const double b = e == L - 1 ? ur : u[e + 1];
+        const double ui = u[e];
+        const double lap = c * (a - 2.0 * ui + b);
+        const double f = real ? ui - dt * (lap + ui - ui * ui * ui) - up[e] : 0.0;
+        F[e] = f;
+        sq = fma(f, f, sq);
+        u2 = fmax(u2, ui * ui);
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void ac_reduce(double sq, double u2, const Lane<L>& ln, Slots& sl,
+                                          int par, double& res, double& umax2) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, off);
+        u2 = fmax(u2, __shfl_xor_sync(0xffffffffu, u2, off));
+    }
+    if (ln.lane == 0) {
+        sl.nrm[par][ln.warp][0] = sq;
+        sl.nrm[par][ln.warp][1] = u2;
+    }
+    __syncthreads();
+    res = 0.0;
+    umax2 = 0.0;
+    for (int w = 0; w < ln.nw; ++w) {
+        res += sl.nrm[par][w][0];
+        umax2 = fmax(umax2, sl.nrm[par][w][1]);
+    }
+    res = sqrt(res);
+}
+
+template <int L>
+__device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, Lane<L>& ln,
+                                       const Tabs& tb, Slots& sl, double* ends) {
+    int rpar = 0;
+    for (int s = 0; s < co.substeps; ++s) {
+        double up[L], F[L];
+#pragma unroll
+        for (int e = 0; e < L; ++e) up[e] = u[e];
+        double sq, u2, res, umax2;
+        ac_residual<L>(u, up, F, co, ln, ends + rpar * 2 * blockDim.x, sq, u2);
+        ac_reduce<L>(sq, u2, ln, sl, rpar, res, umax2);
+        rpar ^= 1;
+        const double stop = fmax(co.newton_tol, co.newton_tol * res);
+        int it = 0;
+        while (res > stop) {
+            if (it >= co.newton_max) {
+                if (ln.t == 0) atomicExch(co.fail, 1);
+                break;
+            }
+            // inner iterations for this Newton step (uniform over the CTA)
+            const double dt = co.ac_dt, sh = co.ac_shift;
+            const double rho =
+                fmax(sh, 3.0 * dt * fmax(umax2, co.ac_umax2) - sh) / (1.0 - dt + sh);
+            int K = 1;
+            for (double e = rho; e > co.inner_eta && K < 64; e *= rho) ++K;
+            double d[L];
+#pragma unroll
+            for (int e = 0; e < L; ++e) d[e] = -F[e];
+            tri_solve<L, true>(d, co, ln, tb, sl);
+            for (int k = 1; k < K; ++k) {
+#pragma unroll
+                for (int e = 0; e < L; ++e) {
+                    const double De = fma(3.0 * dt * u[e], u[e], -sh);
+                    d[e] = fma(-De, d[e], -F[e]);
+                }
+                tri_solve<L, true>(d, co, ln, tb, sl);
+            }
+#pragma unroll
+            for (int e = 0; e < L; ++e) u[e] += d[e];
+            ac_residual<L>(u, up, F, co, ln, ends + rpar * 2 * blockDim.x, sq, u2);
+            ac_reduce<L>(sq, u2, ln, sl, rpar, res, umax2);
+            rpar ^= 1;
+            ++it;
+        }
+    }
+}
+
+// problem dispatch: P = 0 heat (forcing optional), P = 1 Allen-Cahn
+template <int P, int L>
+__device__ __forceinline__ void phi_p(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
+                                      const Tabs& tb, Slots& sl, double* ends, int index,
+                                      int forced) {
+    if constexpr (P == 1) ac_phi<L>(x, co, ln, tb, sl, ends);
+    else phi<L>(x, co, ln, tb, sl, index, forced);
 }
 
 // --------------------------------------------------------------------------
@@ -525,7 +748,7 @@ __host__ __device__ inline int row_bytes_al(int pitch) { return ((pitch * 8) + 1
 // sweep kernel: F / fused FCF / C-relax / residual jobs over C-point indices
 // smem: [S seed/tail][O0][O1 if n_out=2][A if add_g][Tabs][Slots]
 
-template <int L, int NTMAX, int MINB>
+template <int L, int NTMAX, int MINB, int P>
 __global__ void __launch_bounds__(NTMAX, MINB)
     heat_sweep_kernel(const __grid_constant__ SweepArgs a, const __grid_constant__ CUtensorMap tm_u,
                       const __grid_constant__ CUtensorMap tm_g,
@@ -547,6 +770,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     char* tl = base + (1 + nob + (a.add_g ? 1 : 0)) * rb;
     Tabs& tb = *reinterpret_cast<Tabs*>(tl);
     Slots& sl = *reinterpret_cast<Slots*>(tl + sizeof(Tabs));
+    double* ends = reinterpret_cast<double*>(tl + sizeof(Tabs) + sizeof(Slots));
     uint64_t* barS = &sl.bar[0];
     uint64_t* barA = &sl.bar[1];
     const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
@@ -657,7 +881,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 tma_load_2d(bufA, &tm_g, 0, (i - a.g_base) * R, barA);
             }
             release_staging();
-            phi<L>(x, a.co, ln, tb, sl, i, a.forced);
+            phi_p<P, L>(x, a.co, ln, tb, sl, ends, i, a.forced);
             if (a.add_g) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
@@ -678,7 +902,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 tma_load_2d(bufA, &tm_g, 0, (tail_i - a.g_base) * R, barA);
             }
             release_staging();
-            phi<L>(x, a.co, ln, tb, sl, tail_i, a.forced);
+            phi_p<P, L>(x, a.co, ln, tb, sl, ends, tail_i, a.forced);
             if (a.add_g) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
@@ -707,7 +931,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 // fetched into S ahead of its emit, updated in place and stored back.
 // smem: [A0][A1][S][Tabs][Slots]
 
-template <int L, int NTMAX, int MINB>
+template <int L, int NTMAX, int MINB, int P>
 __global__ void __launch_bounds__(NTMAX, MINB)
     heat_window_linear_kernel(const __grid_constant__ WindowArgs a,
                               const __grid_constant__ CUtensorMap tm_r,
@@ -721,6 +945,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     char* bufS = base + 2 * rb;
     Tabs& tb = *reinterpret_cast<Tabs*>(base + 3 * rb);
     Slots& sl = *reinterpret_cast<Slots*>(base + 3 * rb + sizeof(Tabs));
+    double* ends = reinterpret_cast<double*>(base + 3 * rb + sizeof(Tabs) + sizeof(Slots));
     uint64_t* barA0 = &sl.bar[0];
     uint64_t* barA1 = &sl.bar[1];
     uint64_t* barS = &sl.bar[2];
@@ -808,7 +1033,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         }
         for (int s = lo; s <= e1; ++s) {
             if (s > lo) {
-                phi<L>(x, a.co, ln, tb, sl, s, a.forced);
+                phi_p<P, L>(x, a.co, ln, tb, sl, ends, s, a.forced);
                 consume(true);  // e = Psi(e) + r_s
             }
             if (s >= e0) {
@@ -844,7 +1069,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 // given rows, forcing, Psi(v_{j-1})) and the FAS coarse right-hand side
 // (solver.cpp:214-218).  smem: [O0][O1][A1][A2][A3][Tabs][Slots]
 
-template <int L, int NTMAX, int MINB>
+template <int L, int NTMAX, int MINB, int P>
 __global__ void __launch_bounds__(NTMAX, MINB)
     heat_window_kernel(const __grid_constant__ WindowArgs a,
                        const __grid_constant__ CUtensorMap tm_x1,
@@ -864,6 +1089,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     char* tl = base + (three ? 5 : 3) * rb;
     Tabs& tb = *reinterpret_cast<Tabs*>(tl);
     Slots& sl = *reinterpret_cast<Slots*>(tl + sizeof(Tabs));
+    double* ends = reinterpret_cast<double*>(tl + sizeof(Tabs) + sizeof(Slots));
     uint64_t* barA = &sl.bar[1];
     const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
     const int R = pitch >> 4;
@@ -922,7 +1148,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 row_load<L>(bufA1, x, ln);
             }
             if (t == 0) bulk_wait_read<1>();
-            phi<L>(x, a.co, ln, tb, sl, a.idx0 + p, a.forced);
+            phi_p<P, L>(x, a.co, ln, tb, sl, ends, a.idx0 + p, a.forced);
             if (a.kind == WK_FAS_RHS) {
                 // g_j = (v_j - Psi_j(v_{j-1})) + r_j  (solver.cpp:214-218)
                 double y[L];
@@ -973,7 +1199,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 tma_load_2d(bufA3, &tm_x3, 0, (s - a.x3_base) * R, barA);
             }
             if (t == 0) bulk_wait_read<1>();
-            phi<L>(x, a.co, ln, tb, sl, s, a.forced);
+            phi_p<P, L>(x, a.co, ln, tb, sl, ends, s, a.forced);
             if (fas) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
@@ -993,16 +1219,23 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 // --------------------------------------------------------------------------
 // host launchers
 
+// Allen-Cahn kernels also keep the chunk ends of the Newton residual
+static size_t ends_bytes(const HeatCoefDev& co) {
+    return co.prob == 1 ? sizeof(double) * 4 * static_cast<size_t>(co.nt) : 0;
+}
+
 size_t heat_sweep_smem(const SweepArgs& a) {
     const int rows = 1 + a.n_out + (a.add_g ? 1 : 0);
-    return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) + sizeof(Slots);
+    return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) +
+           sizeof(Slots) + ends_bytes(a.co);
 }
 
 size_t heat_window_smem(const WindowArgs& a) {
     int rows;
     if (a.kind == WK_LINEAR) rows = 3;
     else rows = (a.kind == WK_FAS || a.kind == WK_FAS_RHS) ? 5 : 3;
-    return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) + sizeof(Slots);
+    return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) +
+           sizeof(Slots) + ends_bytes(a.co);
 }
 
 namespace {
@@ -1015,14 +1248,18 @@ struct KernelPtrs {
 
 template <int L, int NT, int MB>
 KernelPtrs kptrs() {
-    return {reinterpret_cast<const void*>(heat_sweep_kernel<L, NT, MB>),
-            reinterpret_cast<const void*>(heat_window_linear_kernel<L, NT, MB>),
-            reinterpret_cast<const void*>(heat_window_kernel<L, NT, MB>)};
+    return {reinterpret_cast<const void*>(heat_sweep_kernel<L, NT, MB, 0>),
+            reinterpret_cast<const void*>(heat_window_linear_kernel<L, NT, MB, 0>),
+            reinterpret_cast<const void*>(heat_window_kernel<L, NT, MB, 0>)};
 }
 
-// L=16 serves 2048 < n <= 4096 with 256 threads; smaller L use up to 512
-KernelPtrs select(int L) {
-    switch (L) {
+// heat: L=16 serves 2048 < n <= 4096 with 256 threads; smaller L use up to
+// 512.  Allen-Cahn (Newton Phi, FAS only): L = 8, up to 512 threads.
+KernelPtrs select(const HeatCoefDev& co) {
+    if (co.prob == 1)
+        return {reinterpret_cast<const void*>(heat_sweep_kernel<8, 512, 1, 1>), nullptr,
+                reinterpret_cast<const void*>(heat_window_kernel<8, 512, 1, 1>)};
+    switch (co.L) {
         case 2: return kptrs<2, 512, 1>();
         case 4: return kptrs<4, 512, 1>();
         case 8: return kptrs<8, 512, 1>();
@@ -1063,11 +1300,11 @@ int launch(const void* fn, int grid, int nt, size_t smem, cudaStream_t s, void**
 }  // namespace
 
 int heat_sweep_occupancy(const SweepArgs& a) {
-    return occupancy(select(a.co.L).sweep, a.co.nt, heat_sweep_smem(a));
+    return occupancy(select(a.co).sweep, a.co.nt, heat_sweep_smem(a));
 }
 
 int heat_window_occupancy(const WindowArgs& a) {
-    const KernelPtrs k = select(a.co.L);
+    const KernelPtrs k = select(a.co);
     return occupancy(a.kind == WK_LINEAR ? k.wlin : k.win, a.co.nt, heat_window_smem(a));
 }
 
@@ -1078,7 +1315,7 @@ int launch_heat_sweep(const SweepArgs& a, const CUtensorMap& u, const CUtensorMa
     SweepArgs aa = a;
     CUtensorMap tu = u, tg = g, to = o, tuw = uw, tow = ow;
     void* args[] = {&aa, &tu, &tg, &to, &tuw, &tow};
-    return launch(select(a.co.L).sweep, grid, a.co.nt, heat_sweep_smem(a), s, args);
+    return launch(select(a.co).sweep, grid, a.co.nt, heat_sweep_smem(a), s, args);
 }
 
 int launch_heat_window(const WindowArgs& a, const CUtensorMap& x1, const CUtensorMap& x2,
@@ -1086,7 +1323,8 @@ int launch_heat_window(const WindowArgs& a, const CUtensorMap& x1, const CUtenso
     if (grid <= 0) return 0;
     WindowArgs aa = a;
     CUtensorMap t1 = x1, t2 = x2, t3 = x3, to = o;
-    const KernelPtrs k = select(a.co.L);
+    const KernelPtrs k = select(a.co);
+    if (a.kind == WK_LINEAR && !k.wlin) return static_cast<int>(cudaErrorInvalidValue);
     if (a.kind == WK_LINEAR) {
         void* args[] = {&aa, &t1, &to};
         return launch(k.wlin, grid, a.co.nt, heat_window_smem(a), s, args);
