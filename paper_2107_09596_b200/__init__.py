@@ -6,9 +6,10 @@ reference-shaped Python binding used by tests and the benchmark.
 """
 from .api import (  # noqa: F401
     AllenCahn, Application, ConfigError, ConvergenceReport, CycleDriver, CycleMode, Dahlquist,
-    DivergenceError, Heat1D, Hierarchy, InitialGuess, NonlinearSolveError, NormKind,
+    DivergenceError, Heat1D, Heat2D, Hierarchy, InitialGuess, NonlinearSolveError, NormKind,
     Relaxation, RuntimeFault, ScalarLinear, SolveResult, SolverConfig, StopReason, TimeGrid,
-    build_comm_groups, build_hierarchy, build_layout, make_cf_split, random_state,
+    allen_cahn_ic, build_comm_groups, build_hierarchy, build_layout, fourier_ic, gaussian_source,
+    make_cf_split, random_state,
     rank_ranges, run_parallel, solve, window_recvs,
 )
 from ._capi import LIB_PATH, lib  # noqa: F401

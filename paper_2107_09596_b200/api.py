@@ -362,6 +362,41 @@ class AllenCahn(Application):
         return p
 
 
+class Heat2D(Application):
+    """2D heat u_t = Lap(u) + f on the unit square, nx x nx interior points,
+    5-point stencil, zero Dirichlet (BASELINE configs 2 and 4; no reference
+    Phi, see oracle/atm_oracle.c h2_solve).  Backward Euler per sub-step
+    solved by matrix-free CG to |r| <= cg_rtol |b| from x0 = u_prev; the
+    source enters as forcing(level, i) = A^{-1}(dt f) (explicit) or inside
+    Phi (folded), like heat1d.cpp:66-100."""
+    kind = 5
+
+    def __init__(self, nx=127, folded=False, source=None, cg_rtol=1e-12, cg_max=10000,
+                 initial_condition=None):
+        if nx < 1:
+            raise ConfigError("heat2d: need at least one interior point per side")
+        self.nx, self.folded = nx, folded
+        self.cg_rtol, self.cg_max = cg_rtol, cg_max
+        self.source = None if source is None else np.ascontiguousarray(source, np.float64).ravel()
+        self.ic = None if initial_condition is None else np.ascontiguousarray(initial_condition, np.float64).ravel()
+
+    def vector_size(self):
+        return self.nx * self.nx
+
+    def forcing_folded(self):
+        return self.folded
+
+    def c_problem(self, keep):
+        p = _capi.atm_problem()
+        p.kind, p.n, p.folded = self.kind, self.nx * self.nx, int(self.folded)
+        p.nx, p.cg_rtol, p.cg_max = self.nx, self.cg_rtol, self.cg_max
+        for arr, field in ((self.source, "source"), (self.ic, "ic")):
+            if arr is not None:
+                keep.append(arr)
+                setattr(p, field, ptr(arr))
+        return p
+
+
 # ---------------------------------------------------------------------------
 # the driver
 
@@ -581,6 +616,47 @@ def random_state(seed: int, n: int) -> np.ndarray:
     out = np.empty(n, np.float64)
     lib().atm_random_state(C.c_uint64(seed), n, ptr(out))
     return out
+
+
+# ---------------------------------------------------------------------------
+# seeded synthetic inputs of the BASELINE configs 2-4 (pinned in DESIGN.md;
+# SURVEY 8(d) leaves the mappings to the builder).  Host-side numpy, shared
+# by the tests, the oracle runs and bench.py.
+
+
+def gaussian_source(nx: int, seed: int = 11) -> np.ndarray:
+    """Config 2: f(x, y) = sum_{j<8} a_j exp(-((x-x_j)^2 + (y-y_j)^2) / (2 s_j^2))
+    on the nx x nx interior grid (x_i = (i+1) h, h = 1/(nx+1)), with
+    (a, x, y, s)_j from random_state(seed, 32) mapped to a in [-1, 1),
+    centres in [0.2, 0.8)^2, s in [0.03, 0.1)."""
+    d = random_state(seed, 32).reshape(8, 4)
+    h = 1.0 / (nx + 1)
+    x = (np.arange(nx) + 1) * h
+    X, Y = np.meshgrid(x, x, indexing="xy")  # row j = y index, column i = x index
+    f = np.zeros((nx, nx))
+    for a, cx, cy, s in d:
+        cx, cy = 0.5 + 0.3 * cx, 0.5 + 0.3 * cy
+        sig = 0.065 + 0.035 * s
+        f += a * np.exp(-((X - cx) ** 2 + (Y - cy) ** 2) / (2.0 * sig * sig))
+    return f.ravel()
+
+
+def fourier_ic(nx: int, seed: int = 13) -> np.ndarray:
+    """Config 4: u0 = sum_{p,q=1..8} c_pq sin(p pi x) sin(q pi y) / (p^2 + q^2),
+    c_pq from random_state(seed, 64)."""
+    c = random_state(seed, 64).reshape(8, 8)
+    h = 1.0 / (nx + 1)
+    x = (np.arange(nx) + 1) * h
+    k = np.arange(1, 9)
+    S = np.sin(np.pi * np.outer(k, x))          # [8, nx]
+    w = c / (k[:, None] ** 2 + k[None, :] ** 2)  # w[p-1, q-1]
+    u = S.T @ w.T @ S                           # u[j, i] = sum_pq w_pq sin(q pi y_j) sin(p pi x_i)
+    return np.ascontiguousarray(u).ravel()
+
+
+def allen_cahn_ic(n: int, seed: int = 3) -> np.ndarray:
+    """Config 3: u0 = 0.05 random_state(seed, n), uniform in [-0.05, 0.05)."""
+    return 0.05 * random_state(seed, n)
 
 
 @dataclasses.dataclass

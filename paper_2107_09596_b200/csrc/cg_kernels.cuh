@@ -1,0 +1,65 @@
+// cg_kernels.cuh -- 2D heat Phi (BASELINE configs 2 and 4): backward Euler
+// with the 5-point Laplacian (zero Dirichlet), each sub-step solved by
+// matrix-free CG to |r| <= rtol |b| from x0 = u_prev.  No reference Phi
+// exists; the restatement is oracle/atm_oracle.c h2_solve.
+//
+// One system is owned by a thread-block cluster of `cs` CTAs; CTA q holds
+// rows [q R, q R + R) of the nx x nx grid.  The search direction p lives in
+// shared memory with one halo row above and below (read from the
+// neighbouring CTAs through DSMEM); x and r live in shared memory when they
+// fit (clusters of up to 4 CTAs), else in two global scratch rows per
+// cluster (L2-resident).  Dot products are fixed-order CTA sums followed by a
+// rank-ordered cluster sum, so every CTA holds bitwise the same alpha/beta.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace atm {
+
+struct CgCoefDev {
+    int nx, n, pitch;
+    int cs, R;            // CTAs per system (cluster size), grid rows per CTA
+    double c, diag;       // c = sub_dt / h^2, diag = 1 + 4c
+    double sdt;           // sub-step
+    const double* src;    // source f (n values) or null
+    int substeps;
+    double rtol;
+    int cg_max;
+    int* fail;            // set to 1 when CG hits cg_max
+    int x_smem;           // x and r in shared memory (else xg)
+    double* xg;           // global scratch: x, r rows per cluster slot
+    int E;                // unused (1)
+    int nt;               // threads per CTA
+};
+
+// same job semantics as ScalarSweepArgs / the heat sweep kernel
+struct CgSweepArgs {
+    CgCoefDev co;
+    int kind, m, np, j0, j1;
+    double* u; int u_base;
+    const double* g; int g_base; int add_g;
+    int forced, store, tail;
+    double* out; int out_base;
+    double* sq; int sq_base;
+};
+
+struct CgWindowArgs {
+    CgCoefDev co;
+    int kind, k;
+    int pre_lo, pre_e0, pre_e1, p0, p1;
+    const double* x1; int x1_base;
+    const double* x2; int x2_base;
+    const double* x3; int x3_base;
+    double* out; int out_base; int out_stride;
+    int forced, seed_zero, idx0, seed_off;
+};
+
+// host: cluster geometry for an nx x nx system (cs, R, E, nt, x placement)
+void cg_geometry(int nx, CgCoefDev& co);
+size_t cg_smem_bytes(const CgCoefDev& co);
+// clusters that can be resident at once (the number of x scratch rows needed)
+int cg_max_clusters(const CgCoefDev& co);
+int launch_cg_sweep(const CgSweepArgs& a, cudaStream_t s);
+int launch_cg_window(const CgWindowArgs& a, cudaStream_t s);
+
+}  // namespace atm

@@ -292,7 +292,15 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
             folded_ = true;
             break;
         case ATM_PHI_HEAT2D:
-            config_error("Phi family not available in this build");
+            // BASELINE configs 2, 4 (no reference Phi; oracle/atm_oracle.c h2_solve)
+            if (p.nx < 1) config_error("heat2d: need at least one interior point per side");
+            if (p.nx > 1024) config_error("heat2d: nx > 1024 exceeds the cluster CG kernel");
+            if (!(p.cg_rtol > 0.0) || p.cg_max < 1)
+                config_error("heat2d: cg_rtol > 0 and cg_max >= 1 required");
+            n_ = p.nx * p.nx;
+            h2d_ = true;
+            folded_ = p.folded != 0;
+            break;
         default:
             config_error("unknown problem kind " + std::to_string(kind_));
     }
@@ -311,7 +319,7 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     if (s.initial_guess == ATM_GUESS_PROVIDED && !s.provided)
         config_error("provided initial guess has the wrong number of points");
 
-    pitch_ = heat_ ? ((n_ + 15) / 16) * 16 : 1;
+    pitch_ = (heat_ || h2d_) ? ((n_ + 15) / 16) * 16 : 1;
     // host copies of caller-owned inputs
     ic_.assign(n_, 0.0);
     if (heat_ && !ac_) {
@@ -319,9 +327,10 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
         sinp_.resize(n_);
         for (int i = 0; i < n_; ++i) sinp_[i] = std::sin(kPi * (p.x0 + h_ * (i + 1)));
         ic_ = sinp_;  // heat1d.cpp:85-91
-    } else if (!ac_) {
+    } else if (!ac_ && !h2d_) {
         ic_[0] = p.u0;
     }
+    if (h2d_ && p.source) src_.assign(p.source, p.source + n_);
     if (p.ic) ic_.assign(p.ic, p.ic + n_);
     if (kind_ == ATM_PHI_SCALAR && p.fine_forcing && p.n_ff > 0)
         ff_.assign(p.fine_forcing, p.fine_forcing + p.n_ff);
@@ -393,6 +402,10 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     d_ic_ = dalloc(sizeof(double) * pitch_);
     d_row_ = dalloc(sizeof(double) * pitch_);
     d_fail_ = reinterpret_cast<int*>(dalloc(sizeof(int) * 4));
+    if (!src_.empty()) {
+        d_src_ = dalloc(sizeof(double) * n_);
+        CK(cudaMemcpy(d_src_, src_.data(), sizeof(double) * n_, cudaMemcpyHostToDevice));
+    }
     CK(cudaMemcpy(d_ic_, ic_.data(), sizeof(double) * n_, cudaMemcpyHostToDevice));
     if (!fw_.empty()) {
         d_fw_ = dalloc(sizeof(double) * n_);
@@ -402,6 +415,8 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
         d_ff_ = dalloc(sizeof(double) * ff_.size());
         CK(cudaMemcpy(d_ff_, ff_.data(), sizeof(double) * ff_.size(), cudaMemcpyHostToDevice));
     }
+    // Phi adds its forcing itself (folded integrators with a source term)
+    phi_forced_ = folded_ && ((heat_ && !ac_ && prob_.manufactured) || (h2d_ && d_src_));
     for (Shard& s : sh_) alloc_shard(s);
     for (Shard& s : sh_) build_coefs(s);
 }
@@ -463,7 +478,7 @@ void Engine::alloc_shard(Shard& s) {
         // g: full per-point array where forcing is stored, else point 0 only
         bool g_full = false;
         if (l == 0 && !folded_) {
-            const bool heat_forced = heat_ && !ac_ && prob_.manufactured;
+            const bool heat_forced = (heat_ && !ac_ && prob_.manufactured) || (h2d_ && d_src_);
             const bool scalar_forced = (kind_ == ATM_PHI_SCALAR) && !ff_.empty();
             g_full = heat_forced || scalar_forced;
         }
@@ -563,6 +578,31 @@ void Engine::build_coefs(Shard& s) {
                 for (int i = 0; i < n_; ++i) prof[i] = sinp_[i];
                 c.prof = up(prof);
             }
+        } else if (h2d_) {
+            CgCoefDev& c = Lv.gco;
+            c.pitch = pitch_;
+            cg_geometry(prob_.nx, c);
+            if (c.cs < 1) config_error("heat2d: nx too large for the cluster CG kernel");
+            const double hh = 1.0 / static_cast<double>(prob_.nx + 1);
+            c.c = sub_dt / (hh * hh);
+            c.diag = 1.0 + 4.0 * c.c;
+            c.sdt = sub_dt;
+            c.src = d_src_;
+            c.substeps = S;
+            c.rtol = prob_.cg_rtol;
+            c.cg_max = prob_.cg_max;
+            c.fail = d_fail_;
+            if (!c.x_smem) {
+                // x and r rows per cluster that can be resident at once
+                const int ncl = cg_max_clusters(c);
+                if (!d_xg_) {
+                    void* p = nullptr;
+                    CK(cudaMalloc(&p, sizeof(double) * 2 * static_cast<size_t>(ncl) * pitch_));
+                    gallocs_.push_back(p);
+                    d_xg_ = static_cast<double*>(p);
+                }
+            }
+            c.xg = d_xg_;
         } else {
             ScalarCoefDev& c = Lv.sco;
             if (kind_ == ATM_PHI_DAHLQUIST) {
@@ -653,7 +693,7 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.u_base = Lv.u.base;
         a.g_base = add_g ? Lv.g.base : 0;
         a.add_g = add_g;
-        a.forced = folded_ && prob_.manufactured;
+        a.forced = phi_forced_;
         a.store = store;
         a.tail = tail;
         a.out_base = out_lv ? out_lv->r.base : 0;
@@ -666,6 +706,27 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         if (const char* e = std::getenv("ATM_GRID_SWEEP")) grid = std::min(grid, std::atoi(e));
         const CUtensorMap& tow = out_lv ? out_lv->r.tmw : Lv.u.tmw;
         check_launch(launch_heat_sweep(a, Lv.u.tm, tg, to, Lv.u.tmw, tow, grid, st_), "heat_sweep");
+    } else if (h2d_) {
+        CgSweepArgs a{};
+        a.co = Lv.gco;
+        a.kind = kind;
+        a.m = m;
+        a.np = H_.np[level];
+        a.j0 = j0;
+        a.j1 = j1;
+        a.u = Lv.u.p;
+        a.u_base = Lv.u.base;
+        a.g = add_g ? Lv.g.p : nullptr;
+        a.g_base = add_g ? Lv.g.base : 0;
+        a.add_g = add_g;
+        a.forced = phi_forced_;
+        a.store = store;
+        a.tail = tail;
+        a.out = out_lv ? out_lv->r.p : nullptr;
+        a.out_base = out_lv ? out_lv->r.base : 0;
+        a.sq = sq;
+        a.sq_base = sq_base;
+        check_launch(launch_cg_sweep(a, st_), "cg_sweep");
     } else {
         ScalarSweepArgs a{};
         a.co = Lv.sco;
@@ -712,7 +773,7 @@ void Engine::window_launch(Shard& s, int level, int kind, int pre_lo, int pre_e0
         a.x3_base = x3.base;
         a.out_base = out.base;
         a.out_stride = out_stride;
-        a.forced = forced;
+        a.forced = forced && Lv.hco.theta != nullptr;  // heat1d: manufactured forcing only
         a.seed_zero = seed_zero;
         a.idx0 = idx0;
         a.seed_off = seed_off;
@@ -722,6 +783,30 @@ void Engine::window_launch(Shard& s, int level, int kind, int pre_lo, int pre_e0
         int grid = grid_for(jobs, heat_window_occupancy(a));
         if (const char* e = std::getenv("ATM_GRID_WINDOW")) grid = std::min(grid, std::atoi(e));
         check_launch(launch_heat_window(a, t1, t2, t3, out.tm, grid, st_), "heat_window");
+    } else if (h2d_) {
+        CgWindowArgs a{};
+        a.co = Lv.gco;
+        a.kind = kind;
+        a.k = H_.k;
+        a.pre_lo = pre_lo;
+        a.pre_e0 = pre_e0;
+        a.pre_e1 = pre_e1;
+        a.p0 = p0;
+        a.p1 = p1;
+        a.x1 = x1.p;
+        a.x1_base = x1.base;
+        a.x2 = x2.p;
+        a.x2_base = x2.base;
+        a.x3 = x3.p;
+        a.x3_base = x3.base;
+        a.out = out.p;
+        a.out_base = out.base;
+        a.out_stride = out_stride;
+        a.forced = forced && d_src_ != nullptr;
+        a.seed_zero = seed_zero;
+        a.idx0 = idx0;
+        a.seed_off = seed_off;
+        check_launch(launch_cg_window(a, st_), "cg_window");
     } else {
         ScalarWindowArgs a{};
         a.co = Lv.sco;
@@ -899,6 +984,16 @@ void Engine::fill_level_rhs(int level) {
         } else if (heat_) {
             // forcing(level, i) = propagate(zero, with forcing) (heat1d.cpp:97-100)
             window_launch(s, level, WK_APPLY, 0, 0, -1, i0, i1, Lv.g, Lv.g, Lv.g, Lv.g, 1, 1, 1, 0, 0);
+        } else if (h2d_) {
+            // heat2d forcing is the same for every i (time-independent source):
+            // one CG solve, then copies
+            if (i1 >= i0) {
+                window_launch(s, level, WK_APPLY, 0, 0, -1, i0, i0, Lv.g, Lv.g, Lv.g, Lv.g, 1, 1, 1, 0, 0);
+                if (i1 > i0)
+                    check_launch(launch_fill_rows(Lv.g.p, Lv.g.base, pitch_, n_, i0 + 1, i1 + 1,
+                                                  Lv.g.p + static_cast<size_t>(i0 - Lv.g.base) * pitch_,
+                                                  st_), "g rows");
+            }
         } else {
             // scalar fixture: forcing(0, i) = ff[i] (tests/support.hpp:43-49)
             std::vector<double> rows(static_cast<size_t>(i1 - i0 + 1), 0.0);
@@ -1037,7 +1132,7 @@ void Engine::restrict_to(int level) {
             // g_j = (v_j - Psi_j(v_{j-1})) + r_j, j >= 1; g_0 = v_0 + r_0
             const int p0 = std::max(1, j0), p1 = j0 + cnt - 1;
             window_launch(s, level + 1, WK_FAS_RHS, 0, 0, -1, p0, p1, C.v, C.v, C.r, C.g, 1,
-                          folded_ && prob_.manufactured, 0, 0, 0);
+                          phi_forced_, 0, 0, 0);
             if (j0 == 0)
                 check_launch(launch_row_sum(C.g.p, C.v.p, C.r.p, n_, st_), "g0 fas");
         }
@@ -1056,7 +1151,7 @@ void Engine::windows(int kind) {
         // windows with lo = 0 (p <= k-1) share one prefix chain
         const int pre_e0 = plo, pre_e1 = std::min(k - 1, phi);
         const int p0 = std::max(plo, k), p1 = phi;
-        const int forced = folded_ && prob_.manufactured;
+        const int forced = phi_forced_;
         if (kind == WK_LINEAR) {
             LevelDev& F = s.lv[0];
             const char* dump = std::getenv("ATM_DEBUG_DUMP");
@@ -1171,12 +1266,15 @@ void Engine::cycle() {
 // NonlinearSolveError (gray_scott.cpp:165-169 analogue): a Newton solve hit
 // newton_max somewhere in the last batch of Allen-Cahn Phi applications
 void Engine::check_newton() {
-    if (!ac_) return;
+    if (!ac_ && !h2d_) return;
     int f = 0;
     CK(cudaMemcpyAsync(&f, d_fail_, sizeof(int), cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
     if (f) {
         CK(cudaMemsetAsync(d_fail_, 0, sizeof(int), st_));
+        if (h2d_)
+            throw Error(ATM_NONLINEAR_FAIL, "heat2d: CG did not converge in " +
+                                                std::to_string(prob_.cg_max) + " iterations");
         throw Error(ATM_NONLINEAR_FAIL, "allen-cahn: Newton did not converge in " +
                                             std::to_string(prob_.newton_max) + " iterations");
     }
@@ -1199,7 +1297,7 @@ void Engine::nested_init() {
         }
         fill_level_rhs(l + 1);
     }
-    const int forced = folded_ && prob_.manufactured;
+    const int forced = phi_forced_;
     if (H_.k >= H_.np[lc]) {
         // chain_forward: sequential across shards (parallel.cpp:257-277)
         for (size_t si = 0; si < sh_.size(); ++si) {
@@ -1433,12 +1531,9 @@ void Engine::apply_phi(int level, int first, int count, const double* in, double
     if (!forcing)
         CK(cudaMemcpy2DAsync(x.p, sizeof(double) * pitch_, in, sizeof(double) * n_,
                              sizeof(double) * n_, count, cudaMemcpyHostToDevice, st_));
-    const int forced = forcing ? 1 : (folded_ && prob_.manufactured);
+    const int forced = forcing ? 1 : (phi_forced_);
     LevelDev save = s.lv[level];
-    if (!heat_ && !forcing) {
-        // scalar: folded fine forcing indexes ff by step index
-    }
-    if (!heat_ && forcing) {
+    if (!heat_ && !h2d_ && forcing) {
         // scalar forcing(level, i): ff[i] on level 0 explicit, else zero
         std::vector<double> h(count, 0.0);
         for (int j = 0; j < count; ++j) {
@@ -1493,7 +1588,7 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
         a.u_base = Lv.u.base;
         a.add_g = Lv.g_full;
         a.g_base = Lv.g_full ? Lv.g.base : 0;
-        a.forced = folded_ && prob_.manufactured;
+        a.forced = phi_forced_;
         a.store = STORE_ALL;
         a.tail = TAIL_STORE;
         a.out_base = first;
@@ -1503,6 +1598,25 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
             check_launch(launch_heat_sweep(a, Lv.u.tm, Lv.g_full ? Lv.g.tm : Lv.u.tm, r.tm, Lv.u.tmw,
                                            r.tmw, grid, st_),
                          "resid");
+    } else if (h2d_) {
+        CgSweepArgs a{};
+        a.co = Lv.gco;
+        a.kind = SW_RESID;
+        a.m = 1;
+        a.np = H_.np[level];
+        a.j0 = std::max(1, first);
+        a.j1 = first + count;
+        a.u = Lv.u.p;
+        a.u_base = Lv.u.base;
+        a.g = Lv.g_full ? Lv.g.p : nullptr;
+        a.g_base = Lv.g_full ? Lv.g.base : 0;
+        a.add_g = Lv.g_full;
+        a.forced = phi_forced_;
+        a.store = STORE_ALL;
+        a.tail = TAIL_STORE;
+        a.out = r.p;
+        a.out_base = first;
+        if (a.j1 > a.j0) check_launch(launch_cg_sweep(a, st_), "resid");
     } else {
         ScalarSweepArgs a{};
         a.co = Lv.sco;

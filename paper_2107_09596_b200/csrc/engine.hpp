@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "atmgrit.h"
+#include "cg_kernels.cuh"
 #include "common_kernels.cuh"
 #include "heat_kernels.cuh"
 
@@ -93,6 +94,7 @@ struct LevelDev {
     // Phi coefficients
     HeatCoefDev hco{};
     ScalarCoefDev sco{};
+    CgCoefDev gco{};
     std::vector<void*> allocs;
 };
 
@@ -180,7 +182,8 @@ private:
     Hier H_;
     Layout lay_;
     int n_ = 1, pitch_ = 1, kind_ = 0;
-    bool folded_ = false, heat_ = false, ac_ = false;
+    bool folded_ = false, heat_ = false, ac_ = false, h2d_ = false;
+    bool phi_forced_ = false;
     int L_heat_ = 16;
     int sms_ = 148;
     int world_ = 1, rank_ = 0, G_ = 1;
@@ -201,7 +204,9 @@ private:
     double* d_row_ = nullptr;
     double* d_ff_ = nullptr;
     double* d_prof_ = nullptr;
-    int* d_fail_ = nullptr;   // Allen-Cahn Newton failure flag
+    int* d_fail_ = nullptr;   // Allen-Cahn Newton / heat2d CG failure flag
+    double* d_src_ = nullptr; // heat2d source f
+    double* d_xg_ = nullptr;  // heat2d CG x scratch (one row per resident cluster)
     void check_newton();
     std::vector<void*> gallocs_;
     // NCCL (world > 1)

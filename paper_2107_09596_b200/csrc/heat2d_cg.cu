@@ -1,0 +1,525 @@
+// heat2d_cg.cu -- 2D heat Phi chains for sm_100a (BASELINE configs 2, 4).
+//
+// Phi_i(u) = sub-steps of (I - dt Lap_h) x = u (+ dt f when folded), each
+// solved by CG exactly as oracle/atm_oracle.c h2_solve restates it:
+//   r = b - A x0 (x0 = u_prev), stop = rtol |b|, p = r;
+//   while |r| > stop: ap = A p; alpha = rr / p.ap; x += alpha p;
+//                     r -= alpha ap; beta = rr' / rr; p = r + beta p.
+// A x = (1 + 4c) x - c (((x_w + x_e) + x_s) + x_n), c = dt / h^2.
+//
+// Layout: one system per thread-block cluster (cg_kernels.cuh).  p is kept
+// in shared memory as (R + 2) x (nx + 2) doubles -- zero columns left and
+// right, halo rows above/below copied from the neighbouring CTAs' shared
+// memory through DSMEM after each cluster barrier -- so the stencil needs no
+// bounds checks.  A p is recomputed in the update pass instead of stored.
+//
+// Job semantics (sweep: F / FCF / C-relax / residual with STORE or SQ
+// tails; windows: linear / FAS / forward / apply / FAS right-hand side)
+// are those of the scalar backend (common_kernels.cu) and the heat kernels,
+// restating kernels.cpp:7-95 of the reference.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "cg_kernels.cuh"
+#include "heat_kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace atm {
+
+namespace {
+
+constexpr int kMaxCgThreads = 1024;
+constexpr size_t kCgSmemCap = 220 * 1024;
+
+struct CgShared {
+    double wred[32][2];   // per-warp partial sums
+    double cslot[2][2];   // this CTA's partial sums (parity double-buffered)
+};
+
+// per-CTA context
+struct Ctx {
+    int q, cs, rows, own, W, t, nt;
+    int row0, col0, dq, dr;  // element k of thread t: idx = t + k nt -> (row, col)
+    double* ps;              // (R + 2) x W, own rows 1..rows
+    double* xs;              // own x (shared) or null
+    double* rs;              // own r (shared) or null
+    CgShared* sh;
+    int par;
+};
+
+__device__ __forceinline__ void csync(const Ctx& cx) {
+    if (cx.cs > 1) cg::this_cluster().sync();
+    else __syncthreads();
+}
+
+// fixed-order sum over the CTA, then over the cluster in rank order
+template <int NV>
+__device__ __forceinline__ void cluster_sum(double (&v)[NV], Ctx& cx) {
+    const int lane = cx.t & 31, warp = cx.t >> 5, nw = (cx.nt + 31) >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) cx.sh->wred[warp][i] = v[i];
+    __syncthreads();
+    const int par = cx.par;
+    cx.par ^= 1;
+    if (cx.t == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += cx.sh->wred[w][i];
+            cx.sh->cslot[par][i] = s;
+        }
+    }
+    if (cx.cs == 1) {
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = cx.sh->cslot[par][i];
+        return;
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double s = 0.0;
+        for (int r = 0; r < cx.cs; ++r) s += *cl.map_shared_rank(&cx.sh->cslot[par][i], r);
+        v[i] = s;
+    }
+}
+
+// halo rows from the neighbouring CTAs (after a cluster barrier)
+__device__ __forceinline__ void halos(const Ctx& cx, int nx, int R) {
+    if (cx.cs == 1) return;
+    cg::cluster_group cl = cg::this_cluster();
+    const int W = cx.W;
+    if (cx.q > 0) {
+        const double* src = cl.map_shared_rank(cx.ps, cx.q - 1) + static_cast<size_t>(R) * W;
+        for (int c = cx.t; c < nx; c += cx.nt) cx.ps[1 + c] = src[1 + c];
+    }
+    if (cx.q < cx.cs - 1) {
+        const double* src = cl.map_shared_rank(cx.ps, cx.q + 1) + W;
+        double* dst = cx.ps + static_cast<size_t>(cx.rows + 1) * W;
+        for (int c = cx.t; c < nx; c += cx.nt) dst[1 + c] = src[1 + c];
+    }
+    __syncthreads();
+}
+
+// own-element iteration: f(idx, off), idx = t + j nt (coalesced, conflict-free)
+template <class F>
+__device__ __forceinline__ void for_own(const Ctx& cx, F&& f) {
+    int row = cx.row0, col = cx.col0;
+    const int nx = cx.W - 2;
+#pragma unroll 2
+    for (int idx = cx.t; idx < cx.own; idx += cx.nt) {
+        f(idx, (row + 1) * cx.W + col + 1);
+        col += cx.dr;
+        row += cx.dq;
+        if (col >= nx) {
+            col -= nx;
+            ++row;
+        }
+    }
+}
+
+__device__ __forceinline__ double stencil(const double* ps, int off, int W, double diag, double c) {
+    return diag * ps[off] - c * (((ps[off - 1] + ps[off + 1]) + ps[off - W]) + ps[off + W]);
+}
+
+// Phi in place on the cluster's x (xb: this CTA's band of x; rb: its band
+// of the residual r)
+__device__ void cg_phi(const CgCoefDev& co, Ctx& cx, double* xb, double* rb, int band,
+                       bool forced) {
+    const int W = cx.W;
+    const double c = co.c, diag = co.diag;
+    for (int s = 0; s < co.substeps; ++s) {
+        // prologue: p <- x0, r = b - A x0, |b|, |r|
+        for_own(cx, [&](int idx, int off) { cx.ps[off] = xb[idx]; });
+        csync(cx);
+        halos(cx, co.nx, co.R);
+        double v2[2] = {0.0, 0.0};
+        for_own(cx, [&](int idx, int off) {
+            double b = cx.ps[off];
+            if (forced) b += co.sdt * __ldg(co.src + band + idx);
+            const double rk = b - stencil(cx.ps, off, W, diag, c);
+            rb[idx] = rk;
+            v2[0] = fma(b, b, v2[0]);
+            v2[1] = fma(rk, rk, v2[1]);
+        });
+        cluster_sum<2>(v2, cx);
+        const double stop = co.rtol * sqrt(v2[0]);
+        double rr = v2[1];
+        for_own(cx, [&](int idx, int off) { cx.ps[off] = rb[idx]; });
+        int it = 0;
+        while (sqrt(rr) > stop) {
+            if (it >= co.cg_max) {
+                if (cx.t == 0 && cx.q == 0) atomicExch(co.fail, 1);
+                break;
+            }
+            csync(cx);
+            halos(cx, co.nx, co.R);
+            double pap[1] = {0.0};
+            for_own(cx, [&](int, int off) {
+                pap[0] = fma(cx.ps[off], stencil(cx.ps, off, W, diag, c), pap[0]);
+            });
+            cluster_sum<1>(pap, cx);
+            const double alpha = rr / pap[0];
+            double rn[1] = {0.0};
+            for_own(cx, [&](int idx, int off) {
+                const double pk = cx.ps[off];
+                const double ap = stencil(cx.ps, off, W, diag, c);
+                xb[idx] += alpha * pk;
+                const double rk = rb[idx] - alpha * ap;
+                rb[idx] = rk;
+                rn[0] = fma(rk, rk, rn[0]);
+            });
+            cluster_sum<1>(rn, cx);
+            const double beta = rn[0] / rr;
+            rr = rn[0];
+            for_own(cx, [&](int idx, int off) { cx.ps[off] = rb[idx] + beta * cx.ps[off]; });
+            ++it;
+        }
+    }
+}
+
+__device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned char* smem) {
+    cx.cs = co.cs;
+    cx.q = (co.cs > 1) ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+    cx.rows = max(0, min(co.R, co.nx - cx.q * co.R));
+    cx.own = cx.rows * co.nx;
+    cx.W = co.nx + 2;
+    cx.t = threadIdx.x;
+    cx.nt = blockDim.x;
+    cx.row0 = cx.t / co.nx;
+    cx.col0 = cx.t - cx.row0 * co.nx;
+    cx.dq = cx.nt / co.nx;
+    cx.dr = cx.nt - cx.dq * co.nx;
+    cx.sh = reinterpret_cast<CgShared*>(smem);
+    cx.ps = reinterpret_cast<double*>(smem + sizeof(CgShared));
+    const size_t psn = static_cast<size_t>(co.R + 2) * cx.W;
+    cx.xs = co.x_smem ? cx.ps + psn : nullptr;
+    cx.rs = co.x_smem ? cx.ps + psn + static_cast<size_t>(co.R) * co.nx : nullptr;
+    cx.par = 0;
+    // zero p (padding columns and the domain-boundary halo rows stay zero)
+    for (size_t i = cx.t; i < psn; i += cx.nt) cx.ps[i] = 0.0;
+    __syncthreads();
+}
+
+// this CTA's band of the cluster's x and r (shared, or two global scratch
+// rows per cluster slot)
+__device__ __forceinline__ double* x_band(const CgCoefDev& co, const Ctx& cx, int slot) {
+    return co.x_smem ? cx.xs
+                     : co.xg + static_cast<size_t>(2 * slot) * co.pitch + static_cast<size_t>(cx.q) * co.R * co.nx;
+}
+__device__ __forceinline__ double* r_band(const CgCoefDev& co, const Ctx& cx, int slot) {
+    return co.x_smem ? cx.rs
+                     : co.xg + static_cast<size_t>(2 * slot + 1) * co.pitch + static_cast<size_t>(cx.q) * co.R * co.nx;
+}
+
+__global__ void __launch_bounds__(kMaxCgThreads, 1) cg_sweep_kernel(const __grid_constant__ CgSweepArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Ctx cx;
+    ctx_init(cx, a.co, smem);
+    const int cid = blockIdx.x / a.co.cs, ncl = gridDim.x / a.co.cs;
+    const int band = cx.q * a.co.R * a.co.nx;
+    double* xb = x_band(a.co, cx, cid);
+    double* rb = r_band(a.co, cx, cid);
+    const size_t P = a.co.pitch;
+    auto row = [&](double* base, int i, int b0) { return base + static_cast<size_t>(i - b0) * P + band; };
+    auto crow = [&](const double* base, int i, int b0) {
+        return base + static_cast<size_t>(i - b0) * P + band;
+    };
+    const int m = a.m, last = a.np - 1;
+    for (int J = a.j0 + cid; J < a.j1; J += ncl) {
+        const int c = J * m;
+        int start, end, store_from;
+        switch (a.kind) {
+            case SW_FCF:
+                start = (J == 0) ? 0 : c - m;
+                store_from = (J == 0) ? 1 : c;
+                end = min(c + m - 1, last);
+                break;
+            case SW_CRELAX: start = c - 1; end = c; store_from = c; break;
+            case SW_RESID: start = c - 1; end = c - 1; store_from = INT_MAX; break;
+            default: start = c; end = min(c + m - 1, last); store_from = c + 1; break;
+        }
+        if (end < start) end = start;
+        {
+            const double* src = crow(a.u, start, a.u_base);
+            for_own(cx, [&](int idx, int) { xb[idx] = src[idx]; });
+        }
+        for (int i = start + 1; i <= end; ++i) {
+            cg_phi(a.co, cx, xb, rb, band, a.forced);
+            if (a.add_g) {
+                const double* g = crow(a.g, i, a.g_base);
+                for_own(cx, [&](int idx, int) { xb[idx] += g[idx]; });
+            }
+            if (i >= store_from && store_row(a.store, i, m)) {
+                double* dst = row(a.u, i, a.u_base);
+                for_own(cx, [&](int idx, int) { dst[idx] = xb[idx]; });
+            }
+        }
+        if (a.tail != TAIL_NONE && end + 1 <= last && ((end + 1) % m) == 0) {
+            const int ti = end + 1;
+            cg_phi(a.co, cx, xb, rb, band, a.forced);
+            const double* g = a.add_g ? crow(a.g, ti, a.g_base) : nullptr;
+            const double* uc = crow(a.u, ti, a.u_base);
+            if (a.tail == TAIL_STORE) {
+                double* dst = row(a.out, ti / m, a.out_base);
+                for_own(cx, [&](int idx, int) {
+                    double v = xb[idx];
+                    if (g) v += g[idx];
+                    dst[idx] = v - uc[idx];
+                });
+            } else {
+                double s2[1] = {0.0};
+                for_own(cx, [&](int idx, int) {
+                    double v = xb[idx];
+                    if (g) v += g[idx];
+                    v -= uc[idx];
+                    s2[0] = fma(v, v, s2[0]);
+                });
+                cluster_sum<1>(s2, cx);
+                if (cx.q == 0 && cx.t == 0) a.sq[ti - a.sq_base] = s2[0];
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kMaxCgThreads, 1) cg_window_kernel(const __grid_constant__ CgWindowArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Ctx cx;
+    ctx_init(cx, a.co, smem);
+    const int cid = blockIdx.x / a.co.cs, ncl = gridDim.x / a.co.cs;
+    const int band = cx.q * a.co.R * a.co.nx;
+    double* xb = x_band(a.co, cx, cid);
+    double* rb = r_band(a.co, cx, cid);
+    const size_t P = a.co.pitch;
+    auto crow = [&](const double* base, int i, int b0) {
+        return base + static_cast<size_t>(i - b0) * P + band;
+    };
+    auto orow = [&](int i) { return a.out + static_cast<size_t>(i - a.out_base) * P + band; };
+    if (a.kind == WK_APPLY || a.kind == WK_FAS_RHS) {
+        for (int p = a.p0 + cid; p <= a.p1; p += ncl) {
+            if (a.kind == WK_APPLY) {
+                if (a.seed_zero) {
+                    for_own(cx, [&](int idx, int) { xb[idx] = 0.0; });
+                } else {
+                    const double* s = crow(a.x1, p + a.seed_off, a.x1_base);
+                    for_own(cx, [&](int idx, int) { xb[idx] = s[idx]; });
+                }
+                cg_phi(a.co, cx, xb, rb, band, a.forced);
+                double* d = orow(p);
+                for_own(cx, [&](int idx, int) { d[idx] = xb[idx]; });
+            } else {
+                // g_p = v_p - Psi(v_{p-1}) + r_p (solver.cpp:206-216)
+                const double* s = crow(a.x1, p - 1, a.x1_base);
+                for_own(cx, [&](int idx, int) { xb[idx] = s[idx]; });
+                cg_phi(a.co, cx, xb, rb, band, a.forced);
+                const double* v = crow(a.x2, p, a.x2_base);
+                const double* rr = crow(a.x3, p, a.x3_base);
+                double* d = orow(p);
+                for_own(cx, [&](int idx, int) {
+                    double y = v[idx];
+                    y -= xb[idx];
+                    y += rr[idx];
+                    d[idx] = y;
+                });
+            }
+        }
+        return;
+    }
+    const bool has_pre = a.pre_e1 >= a.pre_e0;
+    const int nj = (has_pre ? 1 : 0) + max(0, a.p1 - a.p0 + 1);
+    for (int qj = cid; qj < nj; qj += ncl) {
+        int lo, e0, e1;
+        if (has_pre && qj == 0) {
+            lo = a.pre_lo;
+            e0 = a.pre_e0;
+            e1 = a.pre_e1;
+        } else {
+            const int p = a.p0 + qj - (has_pre ? 1 : 0);
+            lo = max(0, p - a.k + 1);
+            e0 = e1 = p;
+        }
+        {
+            const double* s1 = crow(a.x1, lo, a.x1_base);
+            if (a.kind == WK_FAS) {
+                const double* s2 = crow(a.x2, lo, a.x2_base);
+                for_own(cx, [&](int idx, int) { xb[idx] = s2[idx] + s1[idx]; });
+            } else {
+                for_own(cx, [&](int idx, int) { xb[idx] = s1[idx]; });
+            }
+        }
+        auto emit = [&](int p) {
+            if (a.kind == WK_LINEAR) {
+                double* d = a.out + static_cast<size_t>(p * a.out_stride - a.out_base) * P + band;
+                for_own(cx, [&](int idx, int) { d[idx] += xb[idx]; });
+            } else {
+                double* d = orow(p);
+                for_own(cx, [&](int idx, int) { d[idx] = xb[idx]; });
+            }
+        };
+        if (lo >= e0) emit(lo);
+        for (int s = lo + 1; s <= e1; ++s) {
+            cg_phi(a.co, cx, xb, rb, band, a.forced);
+            if (a.kind == WK_LINEAR) {
+                const double* r1 = crow(a.x1, s, a.x1_base);
+                for_own(cx, [&](int idx, int) { xb[idx] += r1[idx]; });
+            } else if (a.kind == WK_FAS) {
+                const double* v = crow(a.x2, s, a.x2_base);
+                const double* w = crow(a.x3, s, a.x3_base);
+                const double* r1 = crow(a.x1, s, a.x1_base);
+                for_own(cx, [&](int idx, int) {
+                    double y = xb[idx];
+                    y += v[idx];
+                    y -= w[idx];
+                    y += r1[idx];
+                    xb[idx] = y;
+                });
+            }
+            if (s >= e0) emit(s);
+        }
+    }
+}
+
+struct CgKernels {
+    const void* sweep;
+    const void* window;
+};
+
+CgKernels cg_kernels(int) {
+    return {reinterpret_cast<const void*>(cg_sweep_kernel),
+            reinterpret_cast<const void*>(cg_window_kernel)};
+}
+
+void cg_prepare(const void* fn) {
+    static std::mutex mu;
+    static std::map<const void*, bool> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[fn]) return;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    done[fn] = true;
+}
+
+int cg_launch(const void* fn, const CgCoefDev& co, int jobs, void** args, cudaStream_t s) {
+    if (jobs <= 0) return 0;
+    cg_prepare(fn);
+    const int ncl = std::min(jobs, cg_max_clusters(co));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ncl * co.cs);
+    cfg.blockDim = dim3(co.nt);
+    cfg.dynamicSmemBytes = cg_smem_bytes(co);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = co.cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return static_cast<int>(cudaLaunchKernelExC(&cfg, fn, args));
+}
+
+}  // namespace
+
+void cg_geometry(int nx, CgCoefDev& co) {
+    co.nx = nx;
+    co.n = nx * nx;
+    const size_t red = sizeof(CgShared) + 64;
+    // smallest cluster holding p, x and r on chip (up to 4 CTAs); else the
+    // smallest cluster holding p, with x and r in global scratch rows
+    int pick_cs = -1, pick_sm = 0;
+    for (int pass = 0; pass < 2 && pick_cs < 0; ++pass) {
+        for (int cs = 1; cs <= 16; ++cs) {
+            const int R = (nx + cs - 1) / cs;
+            if ((cs - 1) * R >= nx) continue;
+            const size_t ps = static_cast<size_t>(R + 2) * (nx + 2) * 8;
+            const size_t xr = 2 * static_cast<size_t>(R) * nx * 8;
+            if (pass == 0 && cs <= 4 && ps + xr + red <= kCgSmemCap) {
+                pick_cs = cs;
+                pick_sm = 1;
+                break;
+            }
+            if (pass == 1 && ps + red <= kCgSmemCap) {
+                pick_cs = cs;
+                pick_sm = 0;
+                break;
+            }
+        }
+    }
+    if (pick_cs < 0) {
+        co.cs = 0;
+        return;
+    }
+    co.cs = pick_cs;
+    co.R = (nx + pick_cs - 1) / pick_cs;
+    co.x_smem = pick_sm;
+    co.E = 1;
+    const int own = co.R * nx;
+    co.nt = std::min(kMaxCgThreads, std::max(64, (own + 31) / 32 * 32));
+}
+
+size_t cg_smem_bytes(const CgCoefDev& co) {
+    size_t b = sizeof(CgShared) + static_cast<size_t>(co.R + 2) * (co.nx + 2) * 8;
+    if (co.x_smem) b += 2 * static_cast<size_t>(co.R) * co.nx * 8;
+    return b;
+}
+
+int cg_max_clusters(const CgCoefDev& co) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, size_t>, int> cache;
+    const size_t smem = cg_smem_bytes(co);
+    const auto key = std::make_tuple(co.E, co.cs, co.nt, smem);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    const void* fn = cg_kernels(co.E).sweep;
+    cg_prepare(fn);
+    cg_prepare(cg_kernels(co.E).window);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(co.cs * 148);
+    cfg.blockDim = dim3(co.nt);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = co.cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n < 1) n = 1;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = n;
+    return n;
+}
+
+int launch_cg_sweep(const CgSweepArgs& a, cudaStream_t s) {
+    CgSweepArgs aa = a;
+    void* args[] = {&aa};
+    return cg_launch(cg_kernels(a.co.E).sweep, a.co, a.j1 - a.j0, args, s);
+}
+
+int launch_cg_window(const CgWindowArgs& a, cudaStream_t s) {
+    int nj;
+    if (a.kind == WK_APPLY || a.kind == WK_FAS_RHS) nj = a.p1 - a.p0 + 1;
+    else nj = ((a.pre_e1 >= a.pre_e0) ? 1 : 0) + std::max(0, a.p1 - a.p0 + 1);
+    CgWindowArgs aa = a;
+    void* args[] = {&aa};
+    return cg_launch(cg_kernels(a.co.E).window, a.co, nj, args, s);
+}
+
+}  // namespace atm

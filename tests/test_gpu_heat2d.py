@@ -1,0 +1,124 @@
+"""2D heat (BASELINE configs 2 and 4) on the device vs the C oracle.
+
+No reference Phi exists for this family: oracle/atm_oracle.c
+h2_solve restates backward Euler with the 5-point Laplacian and plain CG
+(|r| <= rtol |b| from x0 = u_prev).  The device runs the same CG per
+thread-block cluster (heat2d_cg.cu) with fixed-order, rank-ordered
+reductions, so only the summation order of the dot products differs; the
+bar is the solver's: same MGRIT iteration count, final u within 1e-10
+relative l2.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2107_09596_b200 as T
+from helpers import rel_l2
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(nx, n_points, tf, ms, k, mode="two-level", folded=False, source=True, ic="zero",
+          tol=1e-9, max_iters=60, cg_max=10000, substeps=1, relax="F"):
+    n = nx * nx
+    f = T.gaussian_source(nx) if source else None
+    u0 = T.fourier_ic(nx) if ic == "fourier" else None
+    app = T.Heat2D(nx, folded=folded, source=f, cg_rtol=1e-12, cg_max=cg_max, initial_condition=u0)
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, tf, n_points), ms, k)
+    cm = {"two-level": T.CycleMode.TwoLevel, "v-cycle": T.CycleMode.VCycle,
+          "nested-v": T.CycleMode.NestedV}[mode]
+    cfg = T.SolverConfig(mode=cm, relaxation=T.Relaxation.FCF if relax == "FCF" else T.Relaxation.F,
+                         max_iters=max_iters, tol=tol, initial_guess=T.InitialGuess.Random, seed=20,
+                         coarse_substeps=substeps)
+    om = {"two-level": O.TWO_LEVEL, "v-cycle": O.VCYCLE, "nested-v": O.NESTED_V}[mode]
+    orc = O.Driver(dict(kind=O.HEAT2D, n=n, nx=nx, folded=int(folded), source=f, ic=u0,
+                        cg_rtol=1e-12, cg_max=cg_max),
+                   dict(tf=tf, n_points=n_points, m=list(ms), k=k),
+                   dict(mode=om, relaxation=O.RELAX_FCF if relax == "FCF" else O.RELAX_F,
+                        max_iters=max_iters, tol=tol, initial_guess=O.GUESS_RANDOM, seed=20,
+                        coarse_substeps=substeps))
+    return app, hier, cfg, orc
+
+
+# nx = 1, 7, 63: one CTA; 127: cluster of 2 with x, r on chip; 200: cluster
+# of 2 with x, r in global scratch; 511: cluster of 11 (config 4's grid)
+@pytest.mark.parametrize("nx", [1, 7, 63, 127, 200, 511])
+def test_heat2d_phi_matches_oracle(nx):
+    app, hier, cfg, orc = _pair(nx, 65, 1.0, [16], 4, substeps=2)
+    drv = T.CycleDriver(app, hier, cfg)
+    xs = np.stack([O.random_state(70 + j, nx * nx) for j in range(2)])
+    for level in (0, 1):
+        got = drv.apply_phi(level, 1, xs)
+        for j in range(xs.shape[0]):
+            want = orc.step(level, 1 + j, xs[j])
+            assert rel_l2(got[j], want) <= 1e-10, (level, j, rel_l2(got[j], want))
+
+
+@pytest.mark.parametrize("nx", [15, 127])
+def test_heat2d_forcing_matches_oracle(nx):
+    app, hier, cfg, orc = _pair(nx, 65, 1.0, [16], 4)
+    drv = T.CycleDriver(app, hier, cfg)
+    got = drv.forcing(0, 1, 3)
+    for j in range(3):
+        assert rel_l2(got[j], orc.forcing(0, 1 + j)) <= 1e-10
+
+
+def test_heat2d_symmetry():
+    # the stencil commutes with the grid transpose
+    nx = 63
+    app, hier, cfg, _ = _pair(nx, 65, 1.0, [16], 4, source=False)
+    drv = T.CycleDriver(app, hier, cfg)
+    x = O.random_state(5, nx * nx)
+    xt = x.reshape(nx, nx).T.ravel().copy()
+    got = drv.apply_phi(0, 1, np.stack([x, xt]))
+    assert rel_l2(got[0].reshape(nx, nx).T.ravel(), got[1]) <= 1e-12
+
+
+def test_heat2d_config2_shape_two_level():
+    # config 2 (two-level, m = 16, k = 4, explicit Gaussian source, u0 = 0)
+    # at nx = 31, N_t = 256
+    app, hier, cfg, orc = _pair(31, 257, 1.0 / 16, [16], 4, tol=1e-10)
+    res = T.solve(app, hier, cfg)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"], (res.report.iterations, ref["iterations"])
+    hist = np.array(res.report.residual_norms)
+    assert np.all(np.abs(hist - ref["history"]) <= 1e-8 * np.abs(ref["history"]) + 1e-13)
+    assert rel_l2(res.state, orc.array(0)) <= 1e-10
+
+
+def test_heat2d_config2_grid_short_horizon():
+    # config 2's grid (nx = 127, cluster of 2) over N_t = 64
+    app, hier, cfg, orc = _pair(127, 65, 1.0 / 64, [16], 4, tol=1e-10)
+    res = T.solve(app, hier, cfg)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"]
+    assert rel_l2(res.state, orc.array(0)) <= 1e-10
+
+
+def test_heat2d_config4_shape_fas():
+    # config 4 (four-level FAS V-cycle, m = (8, 8, 8), k = 2, folded, smooth
+    # Fourier u0) at nx = 31, N_t = 512 over [0, 1/32]
+    app, hier, cfg, orc = _pair(31, 513, 1.0 / 32, [8, 8, 8], 2, mode="v-cycle", folded=True,
+                                source=False, ic="fourier", tol=1e-10)
+    res = T.solve(app, hier, cfg)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"], (res.report.iterations, ref["iterations"])
+    assert rel_l2(res.state, orc.array(0)) <= 1e-10
+
+
+def test_heat2d_folded_source_nested_fcf():
+    app, hier, cfg, orc = _pair(15, 129, 0.25, [4, 4], 3, mode="nested-v", folded=True,
+                                relax="FCF", substeps=2, tol=1e-10)
+    res = T.solve(app, hier, cfg)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"]
+    assert rel_l2(res.state, orc.array(0)) <= 1e-10
+
+
+def test_heat2d_cg_cap_raises():
+    app, hier, cfg, _ = _pair(31, 65, 1.0, [16], 4, cg_max=2)
+    drv = T.CycleDriver(app, hier, cfg)
+    with pytest.raises(T.NonlinearSolveError):
+        drv.apply_phi(1, 1, O.random_state(1, 31 * 31)[None, :])
