@@ -293,6 +293,8 @@ __global__ void __launch_bounds__(kMaxCgThreads, 1) cg_sweep_kernel(const __grid
             }
         }
     }
+    // no CTA may leave while a peer can still read its shared memory (DSMEM)
+    if (a.co.cs > 1) cg::this_cluster().sync();
 }
 
 __global__ void __launch_bounds__(kMaxCgThreads, 1) cg_window_kernel(const __grid_constant__ CgWindowArgs a) {
@@ -336,6 +338,7 @@ __global__ void __launch_bounds__(kMaxCgThreads, 1) cg_window_kernel(const __gri
                 });
             }
         }
+        if (a.co.cs > 1) cg::this_cluster().sync();
         return;
     }
     const bool has_pre = a.pre_e1 >= a.pre_e0;
@@ -390,6 +393,7 @@ __global__ void __launch_bounds__(kMaxCgThreads, 1) cg_window_kernel(const __gri
             if (s >= e0) emit(s);
         }
     }
+    if (a.co.cs > 1) cg::this_cluster().sync();
 }
 
 struct CgKernels {

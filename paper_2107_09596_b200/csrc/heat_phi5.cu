@@ -887,12 +887,13 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 phA ^= 1;
                 row_acc<L>(bufA, x, ln, false);
             }
-            if (i >= store_from && store_row(a.store, i, m)) {
-                stage_out(i - a.u_base, &tm_u, &tm_uw);
-            } else if (a.add_g) {
+            if (a.add_g) {
+                // bufA consumed by every warp before the next step refills it
+                // (the per-warp stores below carry no CTA barrier)
                 fence_proxy_async();
-                __syncthreads();  // bufA consumed before the next load
+                __syncthreads();
             }
+            if (i >= store_from && store_row(a.store, i, m)) stage_out(i - a.u_base, &tm_u, &tm_uw);
         }
 
         // ---- tail: residual at the next C-point, r = Phi(u_last) + g_c - u_c
@@ -1113,6 +1114,9 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 
     auto emit_store = [&](int row) {
         char* o = ob ? bufO1 : bufO0;
+        // the store issued two emits ago read this buffer: wait for it
+        if (t == 0) bulk_wait_read<1>();
+        __syncthreads();
         row_store<L>(o, x, ln);
         fence_proxy_async();
         __syncthreads();

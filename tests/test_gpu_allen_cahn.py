@@ -101,3 +101,30 @@ def test_ac_newton_cap_raises():
     drv = T.CycleDriver(app, hier, cfg)
     with pytest.raises(T.NonlinearSolveError):
         drv.apply_phi(0, 1, O.random_state(1, 64)[None, :])
+
+
+def test_ac_and_heat_fas_cycles_are_deterministic():
+    # repeated runs are bitwise identical (guards the staging-buffer hazards
+    # of the FAS sweeps with stored right-hand sides)
+    app, hier, cfg, _ = _pair(4096, 2049, 1.0, [8, 8], 4)
+    runs = []
+    for _ in range(3):
+        d = T.CycleDriver(app, hier, cfg)
+        d.setup()
+        norms = d.iterate(2)
+        runs.append((norms, d.get_level(0)))
+    for norms, u in runs[1:]:
+        assert np.array_equal(norms, runs[0][0])
+        assert np.array_equal(u, runs[0][1])
+    heat = T.Heat1D(4095, folded=True, manufactured_forcing=True)
+    hh = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, 4097), [8, 8], 4)
+    hc = T.SolverConfig(mode=T.CycleMode.VCycle, max_iters=10, tol=1e-12,
+                        initial_guess=T.InitialGuess.Random, seed=20)
+    hr = []
+    for _ in range(3):
+        d = T.CycleDriver(heat, hh, hc)
+        d.setup()
+        hr.append((d.iterate(2), d.get_level(0)))
+    for norms, u in hr[1:]:
+        assert np.array_equal(norms, hr[0][0])
+        assert np.array_equal(u, hr[0][1])

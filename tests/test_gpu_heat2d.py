@@ -122,3 +122,21 @@ def test_heat2d_cg_cap_raises():
     drv = T.CycleDriver(app, hier, cfg)
     with pytest.raises(T.NonlinearSolveError):
         drv.apply_phi(1, 1, O.random_state(1, 31 * 31)[None, :])
+
+
+def test_heat2d_config4_grid_cluster11_cycles():
+    # config 4's grid (nx = 511: an 11-CTA cluster with x, r in global
+    # scratch): two cycles incl. the fused C-point norm (cluster-summed
+    # squares) against the oracle's cycles and full residual norm
+    app, hier, cfg, orc = _pair(511, 9, 0.01, [4], 2, source=False, ic="fourier", max_iters=2)
+    drv = T.CycleDriver(app, hier, cfg)
+    drv.setup()
+    orc.setup()
+    r0 = orc.residual_norm()
+    for _ in range(2):
+        got = drv.iterate(1)[0]
+        orc.cycle()
+        want = orc.residual_norm()
+        # the second cycle is at rounding level (k = 2 is exact after 2 cycles)
+        assert abs(got - want) <= 1e-9 * abs(want) + 1e-12 * r0
+    assert rel_l2(drv.get_level(0), orc.array(0)) <= 1e-10

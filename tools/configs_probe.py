@@ -1,0 +1,105 @@
+"""Device throughput of the BASELINE configs 1-4 (the parity configs; config 5
+is bench.py's workload).  Per config: build, setup (+ nested init), one
+warm-up iteration, then K timed iterations with CUDA events
+(CycleDriver.iterate_timed).  DOF*steps counts n x relaxation Phi
+applications (2 F-sweeps per level visit, + the C-relaxation for FCF), the
+same count atm_solve reports.  Writes one JSON object per config.
+
+  python tools/configs_probe.py [--out profiles/configs_r01.json] [--only 2,3]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2107_09596_b200 as T  # noqa: E402
+
+
+def configs():
+    c = {}
+    # 1: 1D heat nx=63, Nt=1024, two-level m=16 k=2 FCF
+    c[1] = dict(
+        name="config1_heat1d_n63_Nt1024_m16_k2_FCF",
+        app=lambda: T.Heat1D(63, 0.0, 1.0, folded=False, manufactured_forcing=False,
+                             initial_condition=np.sin(np.pi * np.arange(1, 64) / 64) + 0.1 * T.random_state(1, 63)),
+        grid=(0.0, 1.0, 1025, [16], 2), mode=T.CycleMode.TwoLevel, relax=T.Relaxation.FCF, iters=10)
+    # 2: 2D heat 127^2, Nt=4096 over [0,1], Gaussian source, two-level m=16 k=4
+    c[2] = dict(
+        name="config2_heat2d_127x127_Nt4096_m16_k4",
+        app=lambda: T.Heat2D(127, folded=False, source=T.gaussian_source(127), cg_rtol=1e-12),
+        grid=(0.0, 1.0, 4097, [16], 4), mode=T.CycleMode.TwoLevel, relax=T.Relaxation.F, iters=2)
+    # 3: Allen-Cahn n=4096, Nt=16384 over [0,8], three-level m=8 k=4 (FAS)
+    c[3] = dict(
+        name="config3_allencahn_n4096_Nt16384_m8x8_k4",
+        app=lambda: T.AllenCahn(4096, 0.02, 1.0, 1e-12, 30, initial_condition=T.allen_cahn_ic(4096)),
+        grid=(0.0, 8.0, 16385, [8, 8], 4), mode=T.CycleMode.VCycle, relax=T.Relaxation.F, iters=2)
+    # 4: 2D heat 511^2, four-level m=8 k=2 (FAS), Fourier u0.  Full N_t = 65536
+    # needs ~205 GB of level arrays (more than one B200): N_t = 4096 here
+    c[4] = dict(
+        name="config4_heat2d_511x511_Nt4096(of 65536)_m8x8x8_k2",
+        app=lambda: T.Heat2D(511, folded=True, source=None, cg_rtol=1e-12,
+                             initial_condition=T.fourier_ic(511)),
+        grid=(0.0, 4.0 * 4096 / 65536, 4097, [8, 8, 8], 2), mode=T.CycleMode.VCycle, relax=T.Relaxation.F,
+        iters=1)
+    return c
+
+
+def dof_steps(hier, n, relax, nu=1):
+    tot = 0.0
+    for l in range(hier.n_levels() - 1):
+        np_l = hier.level(l).n_points
+        nc = (np_l - 1) // hier.m[l] + 1
+        F = np_l - nc
+        per = 2.0 * F
+        if relax == T.Relaxation.FCF:
+            per += nu * (F + nc - 1)
+        tot += per * n
+    return tot
+
+
+def run(cfg):
+    app = cfg["app"]()
+    t0, tf, npts, ms, k = cfg["grid"]
+    hier = T.build_hierarchy(T.TimeGrid.make(t0, tf, npts), ms, k)
+    sc = T.SolverConfig(mode=cfg["mode"], relaxation=cfg["relax"], max_iters=100, tol=1e-10,
+                        initial_guess=T.InitialGuess.Random, seed=20)
+    drv = T.CycleDriver(app, hier, sc)
+    w0 = time.perf_counter()
+    drv.setup()
+    if cfg["mode"] == T.CycleMode.NestedV:
+        drv.nested_init()
+    drv.iterate(1)
+    setup_s = time.perf_counter() - w0
+    norms, ms_dev = drv.iterate_timed(cfg["iters"])
+    ds = dof_steps(hier, app.vector_size(), cfg["relax"]) * cfg["iters"]
+    return dict(config=cfg["name"], n=app.vector_size(), iterations_timed=cfg["iters"],
+                ms_per_iteration=ms_dev / cfg["iters"], dof_steps_per_s=ds / (ms_dev * 1e-3),
+                setup_plus_first_iteration_s=setup_s, norms=[float(v) for v in norms])
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default="1,2,3,4")
+    a = ap.parse_args()
+    res = []
+    cs = configs()
+    for i in [int(x) for x in a.only.split(",")]:
+        r = run(cs[i])
+        print(json.dumps(r), flush=True)
+        res.append(r)
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
