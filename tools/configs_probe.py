@@ -85,15 +85,56 @@ def run(cfg):
                 setup_plus_first_iteration_s=setup_s, norms=[float(v) for v in norms])
 
 
+# bounded CPU samples (C oracle restatement, one thread) of the same n and
+# per-level dt at reduced N_t: one cycle each
+# (config 4: two levels, m = 8, at 17 points -- its four-level hierarchy
+# needs >= 513 points, hours of single-thread CG)
+CPU_SAMPLES = {1: (1025, None), 2: (257, None), 3: (1025, None), 4: (17, [8])}
+
+
+def run_cpu(i, cfg):
+    from oracle import oracle as O
+    app = cfg["app"]()
+    t0, tf, npts, ms, k = cfg["grid"]
+    sp, ms_over = CPU_SAMPLES[i]
+    if ms_over:
+        ms = ms_over
+    tf_s = t0 + (tf - t0) * (sp - 1) / (npts - 1)
+    hier = T.build_hierarchy(T.TimeGrid.make(t0, tf_s, sp), ms, k)
+    keep = []
+    p = app.c_problem(keep)
+    kind = {T.Heat1D: O.HEAT1D, T.Heat2D: O.HEAT2D, T.AllenCahn: O.ALLEN_CAHN}[type(app)]
+    prob = dict(kind=kind, n=app.vector_size(), folded=int(p.folded), manufactured=int(p.manufactured),
+                eps=p.eps, length=p.length, newton_tol=p.newton_tol, newton_max=p.newton_max,
+                nx=p.nx, cg_rtol=p.cg_rtol, cg_max=p.cg_max,
+                source=getattr(app, "source", None), ic=getattr(app, "ic", None))
+    mode = {T.CycleMode.TwoLevel: O.TWO_LEVEL, T.CycleMode.VCycle: O.VCYCLE}[cfg["mode"]]
+    if len(ms) == 1 and mode == O.VCYCLE:
+        mode = O.VCYCLE  # FAS two-grid (folded)
+    orc = O.Driver(prob, dict(t0=t0, tf=tf_s, n_points=sp, m=list(ms), k=k),
+                   dict(mode=mode, relaxation=O.RELAX_FCF if cfg["relax"] == T.Relaxation.FCF else O.RELAX_F,
+                        max_iters=100, tol=1e-10, initial_guess=O.GUESS_RANDOM, seed=20))
+    orc.setup()
+    w0 = time.perf_counter()
+    orc.cycle()
+    dt = time.perf_counter() - w0
+    ds = dof_steps(hier, app.vector_size(), cfg["relax"])
+    return dict(cpu_kind="port (oracle/atm_oracle.c, 1 thread)", cpu_sample_points=sp, cpu_sample_m=list(ms),
+                cpu_s_per_iteration=dt, cpu_dof_steps_per_s=ds / dt)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--only", default="1,2,3,4")
+    ap.add_argument("--cpu", action="store_true")
     a = ap.parse_args()
     res = []
     cs = configs()
     for i in [int(x) for x in a.only.split(",")]:
         r = run(cs[i])
+        if a.cpu:
+            r.update(run_cpu(i, cs[i]))
         print(json.dumps(r), flush=True)
         res.append(r)
     if a.out:
