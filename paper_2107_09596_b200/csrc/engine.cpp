@@ -353,11 +353,17 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     G_ = world_ > 1 ? world_ : local;
     lay_ = build_layout(H_, G_);
     trace_ = rt.trace != 0;
-    if (ac_) L_heat_ = 8;
-    else if (const char* e = std::getenv("ATM_HEAT_L")) L_heat_ = std::atoi(e);
-    else {
-        L_heat_ = 2;
-        while (L_heat_ < 16 && pitch_ / L_heat_ > 256) L_heat_ *= 2;
+    // chunk length per level: n > 2048 sweeps run 128-thread CTAs (L = 32,
+    // three per SM); the coarsest level (windows only) keeps 256 threads
+    // (L = 16), whose window kernel holds twice the warps per SM
+    Lvl_.assign(H_.L, 16);
+    for (int l = 0; l < H_.L; ++l) {
+        int L = 2;
+        while (L < 16 && pitch_ / L > 256) L *= 2;
+        if (pitch_ > 2048 && l < H_.coarsest()) L = 32;
+        if (const char* e = std::getenv("ATM_HEAT_L")) L = std::atoi(e);
+        if (ac_) L = 8;
+        Lvl_[l] = L;
     }
 
     CK(cudaSetDevice(rt.device));
@@ -436,7 +442,7 @@ Engine::~Engine() {
     if (st_) cudaStreamDestroy(st_);
 }
 
-DArr Engine::alloc_arr(LevelDev& L, int base, int rows, bool tmap) {
+DArr Engine::alloc_arr(LevelDev& L, int base, int rows, bool tmap, int slice_L) {
     DArr a;
     a.base = base;
     a.rows = std::max(rows, 0);
@@ -449,7 +455,7 @@ DArr Engine::alloc_arr(LevelDev& L, int base, int rows, bool tmap) {
     a.p = static_cast<double*>(p);
     if (tmap && heat_) {
         a.tm = make_row_map(a.p, a.rows, pitch_);
-        a.tmw = make_slice_map(a.p, a.rows, pitch_, L_heat_);
+        a.tmw = make_slice_map(a.p, a.rows, pitch_, slice_L > 0 ? slice_L : 16);
         a.has_tm = true;
     }
     return a;
@@ -474,7 +480,7 @@ void Engine::alloc_shard(Shard& s) {
         if (l == lc && l >= 1) base = std::min(base, std::max(0, Lv.lo - H_.k + 1));
         Lv.base = base;
         const int rows = Lv.hi - base + 1;
-        Lv.u = alloc_arr(Lv, base, rows, true);
+        Lv.u = alloc_arr(Lv, base, rows, true, Lvl_.empty() ? 0 : Lvl_[l]);
         // g: full per-point array where forcing is stored, else point 0 only
         bool g_full = false;
         if (l == 0 && !folded_) {
@@ -488,7 +494,7 @@ void Engine::alloc_shard(Shard& s) {
         else if (base == 0) Lv.g = alloc_arr(Lv, 0, 1, true);
         if (l >= 1) {
             Lv.v = alloc_arr(Lv, base, rows, true);
-            Lv.r = alloc_arr(Lv, base, rows, true);
+            Lv.r = alloc_arr(Lv, base, rows, true, Lvl_.empty() ? 0 : Lvl_[l - 1]);
             if (l == lc && sol_.mode != ATM_TWO_LEVEL) {
                 Lv.w = alloc_arr(Lv, base, rows, true);
                 Lv.x = alloc_arr(Lv, base, rows, true);
@@ -520,8 +526,8 @@ void Engine::build_coefs(Shard& s) {
                                     : 0.0;
             const double ac_s = 1.5 * sub_dt;
             const HeatLevelHost hh =
-                ac_ ? heat_level_host(n_, pitch_, L_heat_, sub_dt * ac_c, ac_s - sub_dt, S, true)
-                    : heat_level_host(n_, pitch_, L_heat_, sub_dt / (h_ * h_), 0.0, S, false);
+                ac_ ? heat_level_host(n_, pitch_, Lvl_[l], sub_dt * ac_c, ac_s - sub_dt, S, true)
+                    : heat_level_host(n_, pitch_, Lvl_[l], sub_dt / (h_ * h_), 0.0, S, false);
             HeatCoefDev& c = Lv.hco;
             c.xw = up(hh.xw);
             c.cyclic = hh.cyclic;
@@ -1575,7 +1581,7 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
     setup();
     Shard& s = sh_[0];
     LevelDev tmp;
-    DArr r = alloc_arr(tmp, first, count, true);
+    DArr r = alloc_arr(tmp, first, count, true, Lvl_.empty() ? 0 : Lvl_[level]);
     LevelDev& Lv = s.lv[level];
     if (heat_) {
         SweepArgs a{};

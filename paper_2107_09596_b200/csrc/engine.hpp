@@ -138,7 +138,9 @@ private:
     // setup helpers
     void alloc_shard(Shard& s);
     void build_coefs(Shard& s);
-    DArr alloc_arr(LevelDev& L, int base, int rows, bool tmap);
+    // slice_L: chunk length of the sweep kernel that stores into this array
+    // by per-warp slices (its slice-map box is 2 slice_L rows)
+    DArr alloc_arr(LevelDev& L, int base, int rows, bool tmap, int slice_L = 0);
     void fill_initial_guess();
     void fill_level_rhs(int level);
     // cycle pieces
@@ -184,7 +186,7 @@ private:
     int n_ = 1, pitch_ = 1, kind_ = 0;
     bool folded_ = false, heat_ = false, ac_ = false, h2d_ = false;
     bool phi_forced_ = false;
-    int L_heat_ = 16;
+    std::vector<int> Lvl_;   // row-kernel chunk length per level
     int sms_ = 148;
     int world_ = 1, rank_ = 0, G_ = 1;
     std::vector<double> ic_, ff_, fw_, cval_, prov_, src_;

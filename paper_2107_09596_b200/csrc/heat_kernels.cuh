@@ -17,7 +17,7 @@ namespace atm {
 
 constexpr int kMaxThreads = 512;
 constexpr int kMaxWarps = kMaxThreads / 32;
-constexpr int kMaxL = 16;
+constexpr int kMaxL = 32;
 constexpr int kScanPerThread = 18;  // Mf[5], Pf_ex, Mb[5], Pb_ex, SB, q0, cfw, cbw, pad, cbwr
 
 // Device view of one level's Phi coefficients.

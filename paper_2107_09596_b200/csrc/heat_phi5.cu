@@ -314,7 +314,7 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double r_in, double shift
 template <int L>
 struct Lane {
     int t, lane, warp, nw, s;
-    int q7, qx, ch0;     // swizzled row-staging geometry of this chunk
+    int q7, qx, qx1, ch0;  // swizzled row-staging geometry (L = 32: two 128-B rows)
     int pad0;            // first padding element of the chunk, L if none
     int par;             // parity of the warp-total slots (one barrier per Phi)
     bool corr, inside;   // carries the boundary correction; chunk inside the row
@@ -335,6 +335,7 @@ __device__ __forceinline__ void lane_init(Lane<L>& ln, const HeatCoefDev& co) {
     ln.q7 = (ln.s >> 4) << 7;
     ln.qx = (ln.s >> 4) & 7;
     ln.ch0 = (ln.s & 15) >> 1;
+    ln.qx1 = (ln.qx + 1) & 7;
     ln.pad0 = (ln.s + L > co.n) ? max(0, co.n - ln.s) : L;
     ln.par = 0;
     const double* sc = co.scan + ln.t * kScanPerThread;
@@ -398,6 +399,10 @@ __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L>& ln) 
 
 // (I + sub_dt L) x = x, in place, over the CTA (heat1d.cpp:47-60); CYC:
 // the periodic matrix with corner entries a (Allen-Cahn linear part).
+// warps per CTA of the instantiation for chunk length L (a power of two):
+// L = 32 -> 128 threads, L = 16 -> 256, L <= 8 -> 512
+__host__ __device__ constexpr int warps_for(int L) { return L >= 32 ? 4 : (L == 16 ? 8 : 16); }
+
 template <int L, bool CYC = false>
 __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
                                           const Tabs& tb, Slots& sl) {
@@ -472,7 +477,7 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     double cC, cD, cD0 = 0.0;
     double p0 = 0.0, pN = 0.0;
     {
-        const int v = ln.lane & (kMaxWarps - 1);
+        const int v = ln.lane & (warps_for(L) - 1);
         const double tf = sl.tf[par][v], ta = sl.ta[par][v];
         const int row = ln.warp * kMaxWarps + v;
         cC = tb.wf[row] * tf;
@@ -483,18 +488,18 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
             pN = fma(tb.xw[2 * kMaxWarps + v], tf, tb.xw[3 * kMaxWarps + v] * ta);
         }
 #pragma unroll
-        for (int off = kMaxWarps / 2; off >= 1; off >>= 1) {
+        for (int off = warps_for(L) / 2; off >= 1; off >>= 1) {
             cC += __shfl_xor_sync(0xffffffffu, cC, off);
             cD += __shfl_xor_sync(0xffffffffu, cD, off);
         }
         if (far) {
 #pragma unroll
-            for (int off = kMaxWarps / 2; off >= 1; off >>= 1)
+            for (int off = warps_for(L) / 2; off >= 1; off >>= 1)
                 cD0 += __shfl_xor_sync(0xffffffffu, cD0, off);
         }
         if (CYC && ln.corr) {
 #pragma unroll
-            for (int off = kMaxWarps / 2; off >= 1; off >>= 1) {
+            for (int off = warps_for(L) / 2; off >= 1; off >>= 1) {
                 p0 += __shfl_xor_sync(0xffffffffu, p0, off);
                 pN += __shfl_xor_sync(0xffffffffu, pN, off);
             }
@@ -667,13 +672,23 @@ __device__ __forceinline__ void phi_p(double (&x)[L], const HeatCoefDev& co, Lan
 // lies in one 128-byte row q of the staging box; 16-byte unit c sits at
 // position c ^ (q & 7).
 
+// byte offset of element pair c (elements 2c, 2c+1) of this thread's chunk
+template <int L>
+__device__ __forceinline__ int pair_off(const Lane<L>& ln, int c) {
+    if constexpr (L == 32) {
+        const int half = c >> 3, cc = c & 7;
+        return ln.q7 + (half << 7) + ((cc ^ (half ? ln.qx1 : ln.qx)) << 4);
+    } else {
+        return ln.q7 + (((ln.ch0 + c) ^ ln.qx) << 4);
+    }
+}
+
 template <int L>
 __device__ __forceinline__ void row_load(const char* buf, double (&x)[L], const Lane<L>& ln) {
     if (ln.inside) {
-        const char* rp = buf + ln.q7;
 #pragma unroll
         for (int c = 0; c < L / 2; ++c) {
-            const double2 v = *reinterpret_cast<const double2*>(rp + (((ln.ch0 + c) ^ ln.qx) << 4));
+            const double2 v = *reinterpret_cast<const double2*>(buf + pair_off<L>(ln, c));
             x[2 * c] = v.x;
             x[2 * c + 1] = v.y;
         }
@@ -686,11 +701,9 @@ __device__ __forceinline__ void row_load(const char* buf, double (&x)[L], const 
 template <int L>
 __device__ __forceinline__ void row_store(char* buf, const double (&x)[L], const Lane<L>& ln) {
     if (ln.inside) {
-        char* rp = buf + ln.q7;
 #pragma unroll
         for (int c = 0; c < L / 2; ++c)
-            *reinterpret_cast<double2*>(rp + (((ln.ch0 + c) ^ ln.qx) << 4)) =
-                make_double2(x[2 * c], x[2 * c + 1]);
+            *reinterpret_cast<double2*>(buf + pair_off<L>(ln, c)) = make_double2(x[2 * c], x[2 * c + 1]);
     }
 }
 
@@ -699,10 +712,9 @@ template <int L>
 __device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], const Lane<L>& ln,
                                         bool sub) {
     if (ln.inside) {
-        const char* rp = buf + ln.q7;
 #pragma unroll
         for (int c = 0; c < L / 2; ++c) {
-            const double2 v = *reinterpret_cast<const double2*>(rp + (((ln.ch0 + c) ^ ln.qx) << 4));
+            const double2 v = *reinterpret_cast<const double2*>(buf + pair_off<L>(ln, c));
             if (sub) {
                 x[2 * c] -= v.x;
                 x[2 * c + 1] -= v.y;
@@ -1267,6 +1279,7 @@ KernelPtrs select(const HeatCoefDev& co) {
         case 2: return kptrs<2, 512, 1>();
         case 4: return kptrs<4, 512, 1>();
         case 8: return kptrs<8, 512, 1>();
+        case 32: return kptrs<32, 128, 3>();
         default: return kptrs<16, 256, 2>();
     }
 }
