@@ -3,6 +3,8 @@
 // Reference citations are relative to /root/reference/proj.
 #include "engine.hpp"
 
+#include <cstdio>
+
 #include <cudaTypedefs.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -710,6 +712,9 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.n_out = choose_n_out(a);
         int grid = grid_for(j1 - j0, heat_sweep_occupancy(a));
         if (const char* e = std::getenv("ATM_GRID_SWEEP")) grid = std::min(grid, std::atoi(e));
+        if (std::getenv("ATM_DEBUG_OCC"))
+            std::fprintf(stderr, "sweep level %d L %d nt %d n_out %d smem %zu occ %d grid %d\n", level,
+                         a.co.L, a.co.nt, a.n_out, heat_sweep_smem(a), heat_sweep_occupancy(a), grid);
         const CUtensorMap& tow = out_lv ? out_lv->r.tmw : Lv.u.tmw;
         check_launch(launch_heat_sweep(a, Lv.u.tm, tg, to, Lv.u.tmw, tow, grid, st_), "heat_sweep");
     } else if (h2d_) {
@@ -787,6 +792,9 @@ void Engine::window_launch(Shard& s, int level, int kind, int pre_lo, int pre_e0
         const CUtensorMap& t2 = x2.has_tm ? x2.tm : t1;
         const CUtensorMap& t3 = x3.has_tm ? x3.tm : t1;
         int grid = grid_for(jobs, heat_window_occupancy(a));
+        if (std::getenv("ATM_DEBUG_OCC"))
+            std::fprintf(stderr, "window kind %d level %d L %d nt %d smem %zu occ %d grid %d\n", kind,
+                         level, a.co.L, a.co.nt, heat_window_smem(a), heat_window_occupancy(a), grid);
         if (const char* e = std::getenv("ATM_GRID_WINDOW")) grid = std::min(grid, std::atoi(e));
         check_launch(launch_heat_window(a, t1, t2, t3, out.tm, grid, st_), "heat_window");
     } else if (h2d_) {

@@ -388,12 +388,47 @@ __device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev
     }
 }
 
+// x[pad0 .. L) = 0 for the thread holding element n-1 (and fully padded
+// threads).  A fall-through switch: one jump and L - pad0 moves for that
+// thread instead of L predicated selects in its whole warp.
 template <int L>
 __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L>& ln) {
     if (ln.pad0 < L) {
-#pragma unroll
-        for (int e = 0; e < L; ++e)
-            if (e >= ln.pad0) x[e] = 0.0;
+        switch (ln.pad0) {
+        case 0: if constexpr (L > 0) x[0] = 0.0; [[fallthrough]];
+        case 1: if constexpr (L > 1) x[1] = 0.0; [[fallthrough]];
+        case 2: if constexpr (L > 2) x[2] = 0.0; [[fallthrough]];
+        case 3: if constexpr (L > 3) x[3] = 0.0; [[fallthrough]];
+        case 4: if constexpr (L > 4) x[4] = 0.0; [[fallthrough]];
+        case 5: if constexpr (L > 5) x[5] = 0.0; [[fallthrough]];
+        case 6: if constexpr (L > 6) x[6] = 0.0; [[fallthrough]];
+        case 7: if constexpr (L > 7) x[7] = 0.0; [[fallthrough]];
+        case 8: if constexpr (L > 8) x[8] = 0.0; [[fallthrough]];
+        case 9: if constexpr (L > 9) x[9] = 0.0; [[fallthrough]];
+        case 10: if constexpr (L > 10) x[10] = 0.0; [[fallthrough]];
+        case 11: if constexpr (L > 11) x[11] = 0.0; [[fallthrough]];
+        case 12: if constexpr (L > 12) x[12] = 0.0; [[fallthrough]];
+        case 13: if constexpr (L > 13) x[13] = 0.0; [[fallthrough]];
+        case 14: if constexpr (L > 14) x[14] = 0.0; [[fallthrough]];
+        case 15: if constexpr (L > 15) x[15] = 0.0; [[fallthrough]];
+        case 16: if constexpr (L > 16) x[16] = 0.0; [[fallthrough]];
+        case 17: if constexpr (L > 17) x[17] = 0.0; [[fallthrough]];
+        case 18: if constexpr (L > 18) x[18] = 0.0; [[fallthrough]];
+        case 19: if constexpr (L > 19) x[19] = 0.0; [[fallthrough]];
+        case 20: if constexpr (L > 20) x[20] = 0.0; [[fallthrough]];
+        case 21: if constexpr (L > 21) x[21] = 0.0; [[fallthrough]];
+        case 22: if constexpr (L > 22) x[22] = 0.0; [[fallthrough]];
+        case 23: if constexpr (L > 23) x[23] = 0.0; [[fallthrough]];
+        case 24: if constexpr (L > 24) x[24] = 0.0; [[fallthrough]];
+        case 25: if constexpr (L > 25) x[25] = 0.0; [[fallthrough]];
+        case 26: if constexpr (L > 26) x[26] = 0.0; [[fallthrough]];
+        case 27: if constexpr (L > 27) x[27] = 0.0; [[fallthrough]];
+        case 28: if constexpr (L > 28) x[28] = 0.0; [[fallthrough]];
+        case 29: if constexpr (L > 29) x[29] = 0.0; [[fallthrough]];
+        case 30: if constexpr (L > 30) x[30] = 0.0; [[fallthrough]];
+        case 31: if constexpr (L > 31) x[31] = 0.0; [[fallthrough]];
+        default: break;
+        }
     }
 }
 
