@@ -270,7 +270,7 @@ def main():
             "config": config,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "heat_sweep_kernel<16> (correction F-sweep + C-point norm tail)",
+                         "kernel": "heat_sweep_kernel<32,128,3> (level-0 correction F-sweep + C-point norm tail)",
                          "algorithmic_bytes_per_launch": sweep_bytes, "avg_launch_ms": sweep_ms,
                          "peak_source": peak_src},
             "gpu_launches": launches * args.steps,
