@@ -28,7 +28,7 @@ struct CgCoefDev {
     int* fail;            // set to 1 when CG hits cg_max
     int x_smem;           // x and r in shared memory (else xg)
     double* xg;           // global scratch: x, r rows per cluster slot
-    int E;                // unused (1)
+    int E;                // 0: generic kernel; > 0: register variant, E elements per thread
     int nt;               // threads per CTA
 };
 

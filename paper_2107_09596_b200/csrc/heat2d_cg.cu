@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <map>
 #include <mutex>
@@ -39,8 +41,8 @@ constexpr int kMaxCgThreads = 1024;
 constexpr size_t kCgSmemCap = 220 * 1024;
 
 struct CgShared {
-    double wred[32][2];   // per-warp partial sums
-    double cslot[2][2];   // this CTA's partial sums (parity double-buffered)
+    double wred[32][2];      // per-warp partial sums
+    double cslot[2][16][2];  // CTA partials of every cluster rank (parity double-buffered)
 };
 
 // per-CTA context
@@ -59,7 +61,10 @@ __device__ __forceinline__ void csync(const Ctx& cx) {
     else __syncthreads();
 }
 
-// fixed-order sum over the CTA, then over the cluster in rank order
+// fixed-order sum over the CTA, then over the cluster in rank order.  Thread
+// 0 of every CTA writes its CTA partial into slot [rank] of every peer's
+// shared memory (DSMEM stores) before the cluster barrier, so afterwards each
+// thread sums cs local values (no per-thread DSMEM reads).
 template <int NV>
 __device__ __forceinline__ void cluster_sum(double (&v)[NV], Ctx& cx) {
     const int lane = cx.t & 31, warp = cx.t >> 5, nw = (cx.nt + 31) >> 5;
@@ -73,26 +78,39 @@ __device__ __forceinline__ void cluster_sum(double (&v)[NV], Ctx& cx) {
     __syncthreads();
     const int par = cx.par;
     cx.par ^= 1;
-    if (cx.t == 0) {
+    if (cx.cs == 1) {
+        if (cx.t == 0) {
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                double s = 0.0;
+                for (int w = 0; w < nw; ++w) s += cx.sh->wred[w][i];
+                cx.sh->cslot[par][0][i] = s;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = cx.sh->cslot[par][0][i];
+        return;
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    if (cx.t < cx.cs) {
+        // thread r delivers this CTA's partials to peer r
+        double part[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             double s = 0.0;
             for (int w = 0; w < nw; ++w) s += cx.sh->wred[w][i];
-            cx.sh->cslot[par][i] = s;
+            part[i] = s;
         }
-    }
-    if (cx.cs == 1) {
-        __syncthreads();
+        double* dst = cl.map_shared_rank(&cx.sh->cslot[par][cx.q][0], cx.t);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) v[i] = cx.sh->cslot[par][i];
-        return;
+        for (int i = 0; i < NV; ++i) dst[i] = part[i];
     }
-    cg::cluster_group cl = cg::this_cluster();
     cl.sync();
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         double s = 0.0;
-        for (int r = 0; r < cx.cs; ++r) s += *cl.map_shared_rank(&cx.sh->cslot[par][i], r);
+        for (int r = 0; r < cx.cs; ++r) s += cx.sh->cslot[par][r][i];
         v[i] = s;
     }
 }
@@ -191,6 +209,102 @@ __device__ void cg_phi(const CgCoefDev& co, Ctx& cx, double* xb, double* rb, int
     }
 }
 
+// Register variant (systems whose CTA band fits E elements per thread with
+// x on chip): r and A p stay in registers, the smem offsets of the owned
+// elements are computed once per call; one stencil pass per iteration.
+template <int E>
+__device__ void cg_phi_reg(const CgCoefDev& co, Ctx& cx, double* xb, int band, bool forced) {
+    const int W = cx.W;
+    const double c = co.c, diag = co.diag;
+    int off[E];
+    bool ok[E];
+    {
+        int row = cx.row0, col = cx.col0;
+        const int nx = W - 2;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            ok[k] = cx.t + k * cx.nt < cx.own;
+            off[k] = (row + 1) * W + col + 1;
+            col += cx.dr;
+            row += cx.dq;
+            if (col >= nx) {
+                col -= nx;
+                ++row;
+            }
+        }
+    }
+    for (int s = 0; s < co.substeps; ++s) {
+        double r[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+            if (ok[k]) cx.ps[off[k]] = xb[cx.t + k * cx.nt];
+        csync(cx);
+        halos(cx, co.nx, co.R);
+        double v2[2] = {0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            r[k] = 0.0;
+            if (ok[k]) {
+                double b = cx.ps[off[k]];
+                if (forced) b += co.sdt * __ldg(co.src + band + cx.t + k * cx.nt);
+                r[k] = b - stencil(cx.ps, off[k], W, diag, c);
+                v2[0] = fma(b, b, v2[0]);
+                v2[1] = fma(r[k], r[k], v2[1]);
+            }
+        }
+        cluster_sum<2>(v2, cx);
+        const double stop = co.rtol * sqrt(v2[0]);
+        double rr = v2[1];
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+            if (ok[k]) cx.ps[off[k]] = r[k];
+        int it = 0;
+        while (sqrt(rr) > stop) {
+            if (it >= co.cg_max) {
+                if (cx.t == 0 && cx.q == 0) atomicExch(co.fail, 1);
+                break;
+            }
+            csync(cx);
+            halos(cx, co.nx, co.R);
+            double ap[E];
+            double pap[1] = {0.0};
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                ap[k] = 0.0;
+                if (ok[k]) {
+                    ap[k] = stencil(cx.ps, off[k], W, diag, c);
+                    pap[0] = fma(cx.ps[off[k]], ap[k], pap[0]);
+                }
+            }
+            cluster_sum<1>(pap, cx);
+            const double alpha = rr / pap[0];
+            double rn[1] = {0.0};
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                if (ok[k]) {
+                    xb[cx.t + k * cx.nt] += alpha * cx.ps[off[k]];
+                    r[k] -= alpha * ap[k];
+                    rn[0] = fma(r[k], r[k], rn[0]);
+                }
+            }
+            cluster_sum<1>(rn, cx);
+            const double beta = rn[0] / rr;
+            rr = rn[0];
+#pragma unroll
+            for (int k = 0; k < E; ++k)
+                if (ok[k]) cx.ps[off[k]] = r[k] + beta * cx.ps[off[k]];
+            ++it;
+        }
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void cg_phi_any(const CgCoefDev& co, Ctx& cx, double* xb, double* rb,
+                                           int band, bool forced) {
+    if constexpr (E > 0) cg_phi_reg<E>(co, cx, xb, band, forced);
+    else cg_phi(co, cx, xb, rb, band, forced);
+}
+
 __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned char* smem) {
     cx.cs = co.cs;
     cx.q = (co.cs > 1) ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
@@ -225,7 +339,8 @@ __device__ __forceinline__ double* r_band(const CgCoefDev& co, const Ctx& cx, in
                      : co.xg + static_cast<size_t>(2 * slot + 1) * co.pitch + static_cast<size_t>(cx.q) * co.R * co.nx;
 }
 
-__global__ void __launch_bounds__(kMaxCgThreads, 1) cg_sweep_kernel(const __grid_constant__ CgSweepArgs a) {
+template <int E>
+__global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kernel(const __grid_constant__ CgSweepArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx cx;
     ctx_init(cx, a.co, smem);
@@ -258,7 +373,7 @@ __global__ void __launch_bounds__(kMaxCgThreads, 1) cg_sweep_kernel(const __grid
             for_own(cx, [&](int idx, int) { xb[idx] = src[idx]; });
         }
         for (int i = start + 1; i <= end; ++i) {
-            cg_phi(a.co, cx, xb, rb, band, a.forced);
+            cg_phi_any<E>(a.co, cx, xb, rb, band, a.forced);
             if (a.add_g) {
                 const double* g = crow(a.g, i, a.g_base);
                 for_own(cx, [&](int idx, int) { xb[idx] += g[idx]; });
@@ -270,7 +385,7 @@ __global__ void __launch_bounds__(kMaxCgThreads, 1) cg_sweep_kernel(const __grid
         }
         if (a.tail != TAIL_NONE && end + 1 <= last && ((end + 1) % m) == 0) {
             const int ti = end + 1;
-            cg_phi(a.co, cx, xb, rb, band, a.forced);
+            cg_phi_any<E>(a.co, cx, xb, rb, band, a.forced);
             const double* g = a.add_g ? crow(a.g, ti, a.g_base) : nullptr;
             const double* uc = crow(a.u, ti, a.u_base);
             if (a.tail == TAIL_STORE) {
@@ -297,7 +412,8 @@ __global__ void __launch_bounds__(kMaxCgThreads, 1) cg_sweep_kernel(const __grid
     if (a.co.cs > 1) cg::this_cluster().sync();
 }
 
-__global__ void __launch_bounds__(kMaxCgThreads, 1) cg_window_kernel(const __grid_constant__ CgWindowArgs a) {
+template <int E>
+__global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_window_kernel(const __grid_constant__ CgWindowArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx cx;
     ctx_init(cx, a.co, smem);
@@ -319,14 +435,14 @@ __global__ void __launch_bounds__(kMaxCgThreads, 1) cg_window_kernel(const __gri
                     const double* s = crow(a.x1, p + a.seed_off, a.x1_base);
                     for_own(cx, [&](int idx, int) { xb[idx] = s[idx]; });
                 }
-                cg_phi(a.co, cx, xb, rb, band, a.forced);
+                cg_phi_any<E>(a.co, cx, xb, rb, band, a.forced);
                 double* d = orow(p);
                 for_own(cx, [&](int idx, int) { d[idx] = xb[idx]; });
             } else {
                 // g_p = v_p - Psi(v_{p-1}) + r_p (solver.cpp:206-216)
                 const double* s = crow(a.x1, p - 1, a.x1_base);
                 for_own(cx, [&](int idx, int) { xb[idx] = s[idx]; });
-                cg_phi(a.co, cx, xb, rb, band, a.forced);
+                cg_phi_any<E>(a.co, cx, xb, rb, band, a.forced);
                 const double* v = crow(a.x2, p, a.x2_base);
                 const double* rr = crow(a.x3, p, a.x3_base);
                 double* d = orow(p);
@@ -374,7 +490,7 @@ __global__ void __launch_bounds__(kMaxCgThreads, 1) cg_window_kernel(const __gri
         };
         if (lo >= e0) emit(lo);
         for (int s = lo + 1; s <= e1; ++s) {
-            cg_phi(a.co, cx, xb, rb, band, a.forced);
+            cg_phi_any<E>(a.co, cx, xb, rb, band, a.forced);
             if (a.kind == WK_LINEAR) {
                 const double* r1 = crow(a.x1, s, a.x1_base);
                 for_own(cx, [&](int idx, int) { xb[idx] += r1[idx]; });
@@ -401,9 +517,22 @@ struct CgKernels {
     const void* window;
 };
 
-CgKernels cg_kernels(int) {
-    return {reinterpret_cast<const void*>(cg_sweep_kernel),
-            reinterpret_cast<const void*>(cg_window_kernel)};
+template <int E>
+CgKernels cg_k() {
+    return {reinterpret_cast<const void*>(cg_sweep_kernel<E>),
+            reinterpret_cast<const void*>(cg_window_kernel<E>)};
+}
+
+// E = 0: generic (x, r via pointers, A p recomputed); E > 0: register variant
+CgKernels cg_kernels(int E) {
+    switch (E) {
+        case 1: return cg_k<1>();
+        case 2: return cg_k<2>();
+        case 4: return cg_k<4>();
+        case 8: return cg_k<8>();
+        case 16: return cg_k<16>();
+        default: return cg_k<0>();
+    }
 }
 
 void cg_prepare(const void* fn) {
@@ -444,8 +573,9 @@ void cg_geometry(int nx, CgCoefDev& co) {
     // smallest cluster holding p, x and r on chip (up to 4 CTAs); else the
     // smallest cluster holding p, with x and r in global scratch rows
     int pick_cs = -1, pick_sm = 0;
+    const char* force = std::getenv("ATM_CG_CS");  // tuning experiments
     for (int pass = 0; pass < 2 && pick_cs < 0; ++pass) {
-        for (int cs = 1; cs <= 16; ++cs) {
+        for (int cs = force ? std::atoi(force) : 1; cs <= 16; ++cs) {
             const int R = (nx + cs - 1) / cs;
             if ((cs - 1) * R >= nx) continue;
             const size_t ps = static_cast<size_t>(R + 2) * (nx + 2) * 8;
@@ -469,9 +599,16 @@ void cg_geometry(int nx, CgCoefDev& co) {
     co.cs = pick_cs;
     co.R = (nx + pick_cs - 1) / pick_cs;
     co.x_smem = pick_sm;
-    co.E = 1;
     const int own = co.R * nx;
+    co.E = 0;
     co.nt = std::min(kMaxCgThreads, std::max(64, (own + 31) / 32 * 32));
+    if (pick_sm && own <= 512 * 16) {
+        // register variant: up to 512 threads x E elements (E a power of two)
+        int E = 1;
+        while (E < 16 && 512 * E < own) E *= 2;
+        co.E = E;
+        co.nt = std::max(64, ((own + E - 1) / E + 31) / 32 * 32);
+    }
 }
 
 size_t cg_smem_bytes(const CgCoefDev& co) {
@@ -505,7 +642,14 @@ int cg_max_clusters(const CgCoefDev& co) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n < 1) n = 1;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, fn, &cfg);
+    if (std::getenv("ATM_DEBUG_OCC"))
+        std::fprintf(stderr, "cg clusters: cs %d nt %d smem %zu -> %d (%s)\n", co.cs, co.nt, smem, n,
+                     cudaGetErrorString(e));
+    if (e != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = 1;
+    }
     std::lock_guard<std::mutex> lk(mu);
     cache[key] = n;
     return n;
