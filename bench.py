@@ -282,17 +282,21 @@ def main():
     # ---- e2e through the public API with host buffers (pinned)
     if not args.no_e2e:
         npts = W["n_points"]
-        if pg:
-            my_rows = None
+        # this rank's level-0 rows (its block plus the left halo row): only
+        # these are filled, pinned, sent and read back
+        r0 = max(0, rr["lo"][0] - 1)
+        r1 = rr["hi"][0] + 1
         guess = np.empty((npts, n), np.float64)
-        rng = np.random.default_rng(1234)
-        for i0 in range(0, npts, 16384):
-            i1 = min(npts, i0 + 16384)
+        rng = np.random.default_rng(1234 + r0)
+        for i0 in range(r0, r1, 16384):
+            i1 = min(r1, i0 + 16384)
             guess[i0:i1] = rng.uniform(-1.0, 1.0, size=(i1 - i0, n))
-        guess[0] = ic
+        if r0 == 0:
+            guess[0] = ic
         out = np.empty_like(guess)
-        reg = T.lib().atm_host_register(guess.ctypes.data, guess.nbytes) == 0
-        reg &= T.lib().atm_host_register(out.ctypes.data, out.nbytes) == 0
+        gsl, osl = guess[r0:r1], out[r0:r1]
+        reg = T.lib().atm_host_register(gsl.ctypes.data, gsl.nbytes) == 0
+        reg &= T.lib().atm_host_register(osl.ctypes.data, osl.nbytes) == 0
         cfg2 = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=1e-300,
                               max_iters=args.steps, initial_guess=T.InitialGuess.Provided,
                               provided=guess)
@@ -303,23 +307,25 @@ def main():
         t0 = time.perf_counter()
         drv2.setup()                      # H2D of the provided level-0 guess
         rep = drv2.drive()                # K iterations, norms read back each iteration
-        drv2.get_level(0, out=out)        # D2H of the level-0 solution
+        # D2H of the level-0 solution (this rank's own points)
+        o0, o1 = rr["lo"][0], rr["hi"][0] + 1
+        drv2.get_level(0, first=o0, count=o1 - o0, out=out[o0:o1])
         wall = time.perf_counter() - t0
         if pg:
             import torch
             t = torch.tensor([wall], dtype=torch.float64)
             pg.all_reduce(t, op=pg.ReduceOp.MAX)
             wall = float(t.item())
-        h2d = guess.nbytes // max(world, 1)
+        h2d = gsl.nbytes * world  # every rank moves its own block
         line["e2e"] = {"value": per_iter * rep.iterations / wall, "unit": unit,
                        "h2d_bytes_per_step": int(h2d / args.steps),
-                       "d2h_bytes_per_step": int(guess.nbytes / max(world, 1) / args.steps + 8),
+                       "d2h_bytes_per_step": int(osl.nbytes * world / args.steps + 8),
                        "wall_s": wall, "pinned": bool(reg),
                        "what": "atm_setup(provided guess from pinned host) + atm_solve(K iterations) + atm_get_level(level 0) into pinned host"}
         drv2.close()
         if reg:
-            T.lib().atm_host_unregister(guess.ctypes.data)
-            T.lib().atm_host_unregister(out.ctypes.data)
+            T.lib().atm_host_unregister(gsl.ctypes.data)
+            T.lib().atm_host_unregister(osl.ctypes.data)
 
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

@@ -1502,7 +1502,9 @@ void Engine::xfer_level(int level, int which, int first, int count, double* host
     if (count < 0 || first < 0 || first + count > H_.np[level]) config_error("point range out of range");
     if (!to_host) setup();
     CK(cudaStreamSynchronize(st_));
-    if (to_host) std::fill(host, host + static_cast<size_t>(count) * n_, 0.0);
+    // one process sees every shard (world 1): every row is written below;
+    // with one shard per process, points this process does not own read as 0
+    if (to_host && world_ > 1) std::fill(host, host + static_cast<size_t>(count) * n_, 0.0);
     for (Shard& s : sh_) {
         LevelDev& Lv = s.lv[level];
         DArr* a = which == 0 ? &Lv.u : which == 1 ? &Lv.g : which == 2 ? &Lv.v : &Lv.r;
