@@ -362,7 +362,8 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     for (int l = 0; l < H_.L; ++l) {
         int L = 2;
         while (L < 16 && pitch_ / L > 256) L *= 2;
-        if (pitch_ > 2048 && l < H_.coarsest()) L = 32;
+        // (ATM_WIN_L32: also the coarsest level -- measured slower, 0.79 vs 0.72 ms)
+        if (pitch_ > 2048 && (l < H_.coarsest() || std::getenv("ATM_WIN_L32"))) L = 32;
         if (const char* e = std::getenv("ATM_HEAT_L")) L = std::atoi(e);
         if (ac_) L = 8;
         Lvl_[l] = L;

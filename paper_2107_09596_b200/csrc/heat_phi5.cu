@@ -988,12 +988,16 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     char* base = smem_base(smem_raw);
     const int pitch = a.co.pitch;
     const int rb = row_bytes_al(pitch);
+    // r-row stream depth: 2 buffers, or 1 for L = 32 (three 128-thread CTAs
+    // per SM need <= 75 KB each; every consume is followed by a Phi that
+    // hides the next load except at window starts)
+    constexpr int NB = (L == 32) ? 1 : 2;
     char* bufA0 = base;
-    char* bufA1 = base + rb;
-    char* bufS = base + 2 * rb;
-    Tabs& tb = *reinterpret_cast<Tabs*>(base + 3 * rb);
-    Slots& sl = *reinterpret_cast<Slots*>(base + 3 * rb + sizeof(Tabs));
-    double* ends = reinterpret_cast<double*>(base + 3 * rb + sizeof(Tabs) + sizeof(Slots));
+    char* bufA1 = base + (NB - 1) * rb;
+    char* bufS = base + NB * rb;
+    Tabs& tb = *reinterpret_cast<Tabs*>(base + (NB + 1) * rb);
+    Slots& sl = *reinterpret_cast<Slots*>(base + (NB + 1) * rb + sizeof(Tabs));
+    double* ends = reinterpret_cast<double*>(base + (NB + 1) * rb + sizeof(Tabs) + sizeof(Slots));
     uint64_t* barA0 = &sl.bar[0];
     uint64_t* barA1 = &sl.bar[1];
     uint64_t* barS = &sl.bar[2];
@@ -1049,7 +1053,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     };
     if (t == 0) {
         issue_next(0);
-        issue_next(1);
+        if (NB == 2) issue_next(1);
     }
     int cb = 0;  // buffer of the next row to consume
     double x[L];
@@ -1067,7 +1071,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         fence_proxy_async();  // generic reads before the TMA refill (WAR)
         __syncthreads();
         if (t == 0) issue_next(cb);
-        cb ^= 1;
+        if (NB == 2) cb ^= 1;
     };
 
     for (int q = blockIdx.x; q < Nj; q += G) {
@@ -1283,7 +1287,7 @@ size_t heat_sweep_smem(const SweepArgs& a) {
 
 size_t heat_window_smem(const WindowArgs& a) {
     int rows;
-    if (a.kind == WK_LINEAR) rows = 3;
+    if (a.kind == WK_LINEAR) rows = a.co.L == 32 ? 2 : 3;
     else rows = (a.kind == WK_FAS || a.kind == WK_FAS_RHS) ? 5 : 3;
     return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) +
            sizeof(Slots) + ends_bytes(a.co);
