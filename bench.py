@@ -155,6 +155,29 @@ def dist_env():
     return world, rank, local
 
 
+def time_to_tolerance(T):
+    """Setup + solve to tol 1e-10 on config5r (n=4095, N_t=2^14, t in [0,1],
+    m=16, k=8, u0 = random_state(7, n), guess seed 20), wall clock with the
+    device synchronised (atm_solve reads each iteration's norm back)."""
+    n, npts = 4095, 2 ** 14 + 1
+    ref_it = None
+    try:
+        ref_it = json.load(open(os.path.join(ROOT, "tests", "golden", "cases.json")))["config5r_k8"]["iterations"]
+    except Exception:
+        pass
+    app = T.Heat1D(n, manufactured_forcing=False, initial_condition=T.random_state(7, n))
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, npts), [16], 8)
+    cfg = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=1e-10, max_iters=400,
+                         initial_guess=T.InitialGuess.Random, seed=20)
+    T.solve(app, hier, cfg)  # warm-up (module load, first-touch)
+    t0 = time.perf_counter()
+    res = T.solve(app, hier, cfg)
+    wall = time.perf_counter() - t0
+    return {"config": "config5r: heat1d n=4095, N_t=2^14, t in [0,1], m=16, k=8, tol 1e-10",
+            "iterations": res.report.iterations, "reference_iterations": ref_it,
+            "converged": bool(res.report.converged), "seconds": wall}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -327,10 +350,24 @@ def main():
             T.lib().atm_host_unregister(gsl.ctypes.data)
             T.lib().atm_host_unregister(osl.ctypes.data)
 
+    # ---- time-to-tolerance (BASELINE metric, second half) on the config-5
+    # shape at N_t = 2^14 (t in [0,1], k = 8), where the compiled reference's
+    # iteration count is pinned (tests/golden/cases.json config5r_k8)
+    ttt = None
+    if world == 1:
+        try:
+            ttt = time_to_tolerance(T)
+            line["time_to_tolerance"] = ttt
+        except Exception as e:  # reported, not fatal
+            line["time_to_tolerance"] = {"unavailable": str(e)}
+
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             cb = cpu_reference_run(3)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            if ttt and "iterations" in ttt:
+                # same N_t = 2^14 sizes: reference seconds per iteration x its iteration count
+                ttt["reference_seconds_estimate"] = cb["seconds_per_iteration"] * ttt["reference_iterations"]
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "unit": unit, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
