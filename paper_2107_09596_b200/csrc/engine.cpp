@@ -405,6 +405,7 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     const int np0 = H_.np[0];
     d_sq_full_ = dalloc(sizeof(double) * np0);
     d_sq_c_ = dalloc(sizeof(double) * np0);
+    if (world_ > 1) d_sq_all_ = dalloc(sizeof(double) * np0);
     d_norm_ = dalloc(sizeof(double) * 300);
     d_fmax_ = dalloc(sizeof(double) * std::max(1, G_));
     d_prevf_ = dalloc(sizeof(double) * np0);
@@ -935,9 +936,15 @@ void Engine::window_exchange(int level, DArr LevelDev::*arr) {
 }
 
 double Engine::reduce_norm(double* sq, int count) {
-    if (world_ > 1)
-        nccl_->check(nccl_->AllReduce(sq, sq, count, ncclFloat64, ncclSum,
+    // world > 1: each rank's per-point array holds only its own points (the
+    // rest stay 0 and are never written), so the element-wise sum is exact.
+    // The sum goes to a separate buffer: reducing in place would leave the
+    // other ranks' values in this rank's array for the next iteration.
+    if (world_ > 1) {
+        nccl_->check(nccl_->AllReduce(sq, d_sq_all_, count, ncclFloat64, ncclSum,
                                       static_cast<ncclComm_t>(comm_), st_), "allreduce squares");
+        sq = d_sq_all_;
+    }
     check_launch(launch_norm_from_squares(sq, count, d_norm_, st_), "norm");
     double out = 0.0;
     CK(cudaMemcpyAsync(&out, d_norm_, sizeof(double), cudaMemcpyDeviceToHost, st_));

@@ -198,6 +198,7 @@ private:
     // global reduction arrays (per point of level 0)
     double* d_sq_full_ = nullptr;
     double* d_sq_c_ = nullptr;
+    double* d_sq_all_ = nullptr;  // world > 1: all-reduced per-point squares
     double* d_norm_ = nullptr;
     double* d_prevf_ = nullptr;
     double* d_fmax_ = nullptr;
