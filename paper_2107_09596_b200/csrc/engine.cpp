@@ -101,7 +101,11 @@ struct NcclApi {
 
     bool load() {
         if (h) return true;
-        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // ATM_NCCL_LIB: an alternative implementation of the same entry
+        // points (tests/mocknccl: host-mediated transport for several
+        // processes on one GPU)
+        if (const char* alt = std::getenv("ATM_NCCL_LIB")) h = dlopen(alt, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         if (!h) return false;
 #define SYM(f, n) f = reinterpret_cast<decltype(f)>(dlsym(h, n)); if (!f) return false

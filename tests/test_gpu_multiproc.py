@@ -1,0 +1,58 @@
+"""The engine's one-shard-per-process path (atm_runtime.world_size > 1: NCCL
+halo / window payload / norm all-reduce / nested chain) run as 2-3 processes
+on the single GPU, with the host-mediated NCCL stand-in tests/mocknccl (real
+NCCL needs one GPU per rank).  Histories must be bitwise those of the
+single-process solve (the reference's contract across rank counts,
+test_runtime.cpp:194-228) and the assembled level-0 state bitwise equal."""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+import paper_2107_09596_b200 as T
+from mp_cases import build_case
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+MOCK = os.path.join(HERE, "mocknccl", "libmocknccl.so")
+
+
+def _mock_lib():
+    subprocess.check_call(["make", "-s", "-C", os.path.join(HERE, "mocknccl")])
+    return MOCK
+
+
+@pytest.mark.parametrize("case,world", [("two_level", 2), ("two_level", 3), ("fas_vcycle", 2),
+                                        ("nested_fcf", 3), ("global_coarse", 2)])
+def test_multiprocess_solve_bitwise_equals_single_process(case, world):
+    lib = _mock_lib()
+    app, hier, cfg = build_case(case)
+    ref = T.solve(app, hier, cfg)
+    tmp = tempfile.mkdtemp(prefix="mp_")
+    try:
+        idfile = os.path.join(tmp, "nccl.id")
+        env = dict(os.environ, ATM_NCCL_LIB=lib)
+        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), case, str(r),
+                                   str(world), idfile, os.path.join(tmp, f"r{r}.npz")], env=env)
+                 for r in range(world)]
+        for p in procs:
+            assert p.wait(timeout=600) == 0
+        u = np.zeros_like(ref.state)
+        for r in range(world):
+            d = np.load(os.path.join(tmp, f"r{r}.npz"))
+            assert int(d["iterations"]) == ref.report.iterations
+            assert np.array_equal(d["norms"], np.array(ref.report.residual_norms)), (r, d["norms"])
+            u[int(d["lo"]):int(d["hi"]) + 1] = d["u"]
+        assert np.array_equal(u, ref.state)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+        for f in os.listdir("/dev/shm"):
+            if f.startswith("mocknccl_"):
+                shutil.rmtree(os.path.join("/dev/shm", f), ignore_errors=True)
