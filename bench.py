@@ -226,6 +226,9 @@ def main():
 
     nccl_id = None
     pg = None
+    # one GPU per rank; BENCH_SHARE_DEVICE=1 puts every rank on device 0 (only
+    # for exercising this path with the tests/mocknccl transport)
+    dev = 0 if (world == 1 or os.environ.get("BENCH_SHARE_DEVICE") == "1") else local
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -243,7 +246,7 @@ def main():
     cfg = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=W["tol"],
                          max_iters=1_000_000, initial_guess=T.InitialGuess.Random, seed=W["guess_seed"])
     app = T.Heat1D(n, manufactured_forcing=False, initial_condition=ic)
-    drv = T.CycleDriver(app, hier, cfg, device=local if world > 1 else 0, trace=True,
+    drv = T.CycleDriver(app, hier, cfg, device=dev, trace=True,
                         world_size=world, rank=rank, nccl_id=nccl_id)
     drv.setup()
     drv.iterate(args.warmup)
@@ -251,7 +254,7 @@ def main():
     launches = drv.last_iteration_launches()
     if pg:
         pg.barrier()
-    sampler = ClockSampler(local) if rank == 0 else None
+    sampler = ClockSampler(dev) if rank == 0 else None
     if sampler:
         sampler.__enter__()
     norms, ms = drv.iterate_timed(args.steps)
@@ -325,7 +328,7 @@ def main():
         cfg2 = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=1e-300,
                               max_iters=args.steps, initial_guess=T.InitialGuess.Provided,
                               provided=guess)
-        drv2 = T.CycleDriver(app, hier, cfg2, device=local if world > 1 else 0,
+        drv2 = T.CycleDriver(app, hier, cfg2, device=dev,
                              world_size=world, rank=rank, nccl_id=nccl_id)
         if pg:
             pg.barrier()
