@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define ATM_ABI_VERSION 1
+#define ATM_ABI_VERSION 2
 #define ATM_MAX_LEVELS 8
 
 typedef enum {
@@ -40,7 +40,9 @@ typedef enum {
     ATM_PHI_DAHLQUIST = 2,  /* problems::Dahlquist, dahlquist.hpp:12-50                */
     ATM_PHI_SCALAR = 3,     /* tests/support.hpp:19-60 ScalarLinear fixture           */
     ATM_PHI_ALLEN_CAHN = 4, /* new: BASELINE config 3 (no reference counterpart)       */
-    ATM_PHI_HEAT2D = 5      /* new: BASELINE configs 2, 4 (no reference counterpart)   */
+    ATM_PHI_HEAT2D = 5,     /* new: BASELINE configs 2, 4 (no reference counterpart)   */
+    ATM_PHI_GRAY_SCOTT = 6  /* problems::GrayScott, gray_scott.hpp:12-68 (Newton +
+                               Jacobi-preconditioned BiCGSTAB; nx = cells per side) */
 } atm_phi_kind;
 
 typedef enum { ATM_TWO_LEVEL = 0, ATM_VCYCLE = 1, ATM_NESTED_V = 2 } atm_mode;   /* CycleMode   */
@@ -69,6 +71,11 @@ typedef struct atm_problem {
     int cg_max;
     const double* source;  /* heat2d f (nx*nx) or NULL                               */
     const double* ic;      /* optional initial_condition() override (n values)       */
+    /* gray-scott (GrayScott::Options, gray_scott.hpp:24-38); n = 2 nx^2, state
+     * [u; v]; newton_tol / newton_max shared with allen-cahn                 */
+    double gs_domain, gs_feed, gs_kill, gs_du, gs_dv, gs_linear_tol;
+    int gs_reaction, gs_bounds_check;
+    double gs_bound_lo, gs_bound_hi;
 } atm_problem;
 
 /* Time grid + hierarchy: TimeGrid::make (time_grid.hpp:14-23) and

@@ -85,6 +85,7 @@ struct orc_driver {
     double* v[ORC_MAXL];
     double* r[ORC_MAXL];
     double* rs;            /* level-0 residual scratch                 */
+    double* gs_work;       /* gray-scott Newton / BiCGSTAB scratch     */
     double* prevf;         /* functional-change history per C-point    */
     int setup_done;
     int newton_fail;
@@ -329,6 +330,190 @@ static int h2_propagate(orc_driver* d, int level, const double* in, double* out,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Gray-Scott (gray_scott.cpp:16-190): periodic n x n cells on [0, domain]^2,  */
+/* state [u; v]; backward Euler, Newton with the analytic Jacobian and an     */
+/* inner BiCGSTAB with diagonal (Jacobi) preconditioning, right-              */
+/* preconditioned, x0 = 0, |r|^2 <= tol^2 |b|^2, at most 2 dim iterations, a  */
+/* restart when rho degenerates -- the published algorithm the reference      */
+/* delegates to Eigen::BiCGSTAB (Eigen >= 3.3, absent here: parity unpinned). */
+
+static int gs_nb(int n, int i, int j) { return ((i + n) % n) * n + (j + n) % n; }
+
+/* reaction_terms (gray_scott.cpp:63-88) */
+static void gs_rhs(const orc_driver* d, const double* w, double* f) {
+    const int n = d->p.nx, cells = n * n;
+    const double h = d->p.gs_domain / n, ih2 = 1.0 / (h * h);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            const int c = i * n + j;
+            const int N = gs_nb(n, i + 1, j), S = gs_nb(n, i - 1, j), E = gs_nb(n, i, j + 1),
+                      W = gs_nb(n, i, j - 1);
+            const double u = w[c], v = w[cells + c];
+            const double lu = (w[N] + w[S] + w[E] + w[W] - 4.0 * u) * ih2;
+            const double lv = (w[cells + N] + w[cells + S] + w[cells + E] + w[cells + W] - 4.0 * v) * ih2;
+            double fu = d->p.gs_du * lu, fv = d->p.gs_dv * lv;
+            if (d->p.gs_reaction) {
+                const double uvv = u * v * v;
+                fu += -uvv + d->p.gs_feed * (1.0 - u);
+                fv += uvv - (d->p.gs_feed + d->p.gs_kill) * v;
+            }
+            f[c] = fu;
+            f[cells + c] = fv;
+        }
+}
+
+/* y = J x, J = I - dt f'(w) (the Jacobian of gray_scott.cpp:114-139) */
+static void gs_jac(const orc_driver* d, double dt, const double* w, const double* x, double* y,
+                   double* diag) {
+    const int n = d->p.nx, cells = n * n;
+    const double h = d->p.gs_domain / n, ih2 = 1.0 / (h * h);
+    const double off = -dt * d->p.gs_du * ih2, offv = -dt * d->p.gs_dv * ih2;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            const int c = i * n + j;
+            const int N = gs_nb(n, i + 1, j), S = gs_nb(n, i - 1, j), E = gs_nb(n, i, j + 1),
+                      W = gs_nb(n, i, j - 1);
+            const double u = w[c], v = w[cells + c];
+            double duu = 1.0 + dt * 4.0 * d->p.gs_du * ih2, dvv = 1.0 + dt * 4.0 * d->p.gs_dv * ih2;
+            double cuv = 0.0, cvu = 0.0;
+            if (d->p.gs_reaction) {
+                duu += dt * (v * v + d->p.gs_feed);
+                dvv += dt * (d->p.gs_feed + d->p.gs_kill) - dt * 2.0 * u * v;
+                cuv = dt * 2.0 * u * v;
+                cvu = -dt * v * v;
+            }
+            if (diag) {
+                diag[c] = duu;
+                diag[cells + c] = dvv;
+            }
+            if (x) {
+                y[c] = duu * x[c] + off * (x[N] + x[S] + x[E] + x[W]) + cuv * x[cells + c];
+                y[cells + c] = dvv * x[cells + c] +
+                               offv * (x[cells + N] + x[cells + S] + x[cells + E] + x[cells + W]) +
+                               cvu * x[c];
+            }
+        }
+}
+
+static double gs_dot(int m, const double* a, const double* b) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += a[i] * b[i];
+    return s;
+}
+
+/* BiCGSTAB for J x = b, x0 = 0; returns 0 on convergence */
+static int gs_bicgstab(const orc_driver* d, double dt, const double* w, const double* b, double* x,
+                       double* ws) {
+    const int m = 2 * d->p.nx * d->p.nx;
+    double *r = ws, *r0 = r + m, *p = r0 + m, *v = p + m, *s = v + m, *t = s + m, *y = t + m,
+           *z = y + m, *dg = z + m;
+    gs_jac(d, dt, w, NULL, NULL, dg);
+    for (int i = 0; i < m; ++i) {
+        x[i] = 0.0;
+        r[i] = b[i];
+        r0[i] = b[i];
+        p[i] = v[i] = 0.0;
+    }
+    const double bb = gs_dot(m, b, b);
+    const double tol2 = d->p.gs_linear_tol * d->p.gs_linear_tol * bb;
+    double rr = gs_dot(m, r, r);
+    if (rr <= tol2) return 0;
+    double r0n = rr, rho = 1.0, alpha = 1.0, om = 1.0;
+    const double eps2 = 1e-30;  /* NumTraits<double>::epsilon()^2, rounded */
+    int it = 0, restarts = 0;
+    const int maxit = 2 * m;
+    while (rr > tol2 && it < maxit) {
+        const double rho_old = rho;
+        rho = gs_dot(m, r0, r);
+        if (fabs(rho) < eps2 * r0n) {
+            for (int i = 0; i < m; ++i) r0[i] = r[i];
+            rho = r0n = gs_dot(m, r, r);
+            if (restarts++ == 0) it = 0;
+        }
+        const double beta = (rho / rho_old) * (alpha / om);
+        for (int i = 0; i < m; ++i) p[i] = r[i] + beta * (p[i] - om * v[i]);
+        for (int i = 0; i < m; ++i) y[i] = p[i] / dg[i];
+        gs_jac(d, dt, w, y, v, NULL);
+        alpha = rho / gs_dot(m, r0, v);
+        for (int i = 0; i < m; ++i) s[i] = r[i] - alpha * v[i];
+        for (int i = 0; i < m; ++i) z[i] = s[i] / dg[i];
+        gs_jac(d, dt, w, z, t, NULL);
+        const double tt = gs_dot(m, t, t);
+        om = tt > 0.0 ? gs_dot(m, t, s) / tt : 0.0;
+        for (int i = 0; i < m; ++i) x[i] += alpha * y[i] + om * z[i];
+        for (int i = 0; i < m; ++i) r[i] = s[i] - om * t[i];
+        rr = gs_dot(m, r, r);
+        ++it;
+    }
+    return rr <= tol2 ? 0 : 1;
+}
+
+/* backward_euler_solve (gray_scott.cpp:91-172) + step's bounds check (:174-190) */
+static int gs_step(orc_driver* d, int level, const double* in, double* out) {
+    const int m = 2 * d->p.nx * d->p.nx;
+    /* own scratch: callers hand step() output slots inside d->work */
+    double* f = d->gs_work;
+    double* res = f + m;
+    double* delta = res + m;
+    double* prev = delta + m;
+    double* ws = prev + m;
+    if (out != in) memcpy(out, in, sizeof(double) * (size_t)m);
+    for (int s = 1; s <= d->sub[level]; ++s) {
+        const double dt = d->sdt[level];
+        memcpy(prev, out, sizeof(double) * (size_t)m);
+        gs_rhs(d, out, f);
+        for (int i = 0; i < m; ++i) res[i] = out[i] - prev[i] - dt * f[i];
+        const double norm0 = sqrt(gs_dot(m, res, res));
+        const double stop = fmax(d->p.newton_tol, d->p.newton_tol * norm0);
+        if (norm0 <= stop) continue;
+        int ok = 0;
+        for (int it = 0; it < d->p.newton_max; ++it) {
+            if (gs_bicgstab(d, dt, out, res, delta, ws) != 0) {
+                d->newton_fail = 1;
+                return fail(d, ORC_NONLINEAR, "gray-scott: inner linear solve failed (dt = %g)", dt);
+            }
+            for (int i = 0; i < m; ++i) out[i] -= delta[i];
+            gs_rhs(d, out, f);
+            for (int i = 0; i < m; ++i) res[i] = out[i] - prev[i] - dt * f[i];
+            if (sqrt(gs_dot(m, res, res)) <= stop) {
+                ok = 1;
+                break;
+            }
+        }
+        if (!ok) {
+            d->newton_fail = 1;
+            return fail(d, ORC_NONLINEAR, "gray-scott: Newton did not reach %g within %d iterations",
+                        d->p.newton_tol, d->p.newton_max);
+        }
+    }
+    if (d->p.gs_bounds_check)
+        for (int i = 0; i < m; ++i)
+            if (!(out[i] >= d->p.gs_bound_lo && out[i] <= d->p.gs_bound_hi))
+                return fail(d, ORC_NONLINEAR, "gray-scott: concentration left the bounding box");
+    return ORC_OK;
+}
+
+/* initial_condition (gray_scott.cpp:38-61): u = 1, v = 0 plus a bump */
+static void gs_initial(const orc_driver* d, double* w) {
+    const int n = d->p.nx, cells = n * n;
+    const double h = d->p.gs_domain / n;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            const int c = i * n + j;
+            const double x = (j + 0.5) * h, y = (i + 0.5) * h;
+            double u = 1.0, v = 0.0;
+            if (x >= 1.0 && x <= 1.5 && y >= 1.0 && y <= 1.5) {
+                const double sx = sin(4.0 * kPi * x), sy = sin(4.0 * kPi * y);
+                const double bump = 0.25 * sx * sx * sy * sy;
+                u = 1.0 - 2.0 * bump;
+                v = bump;
+            }
+            w[c] = u;
+            w[cells + c] = v;
+        }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Application::step / forcing / initial_condition                          */
 
 static double dahl_mult(const orc_driver* d, int level) {
@@ -358,6 +543,8 @@ int orc_step(orc_driver* d, int level, int index, const double* in, double* out)
             return ac_step(d, level, in, out);
         case ORC_HEAT2D:
             return h2_propagate(d, level, in, out, d->p.folded);
+        case ORC_GRAY_SCOTT:
+            return gs_step(d, level, in, out);
     }
     return fail(d, ORC_CONFIG, "unknown problem kind");
 }
@@ -427,7 +614,8 @@ orc_driver* orc_create(const orc_problem* p, const orc_grid* g, const orc_solver
     d->s = *s;
     d->L = g->n_m + 1;
     const int scalar = (p->kind == ORC_DAHLQUIST || p->kind == ORC_SCALAR);
-    d->n = scalar ? 1 : (p->kind == ORC_HEAT2D ? p->nx * p->nx : p->n);
+    d->n = scalar ? 1 : (p->kind == ORC_HEAT2D ? p->nx * p->nx
+                         : p->kind == ORC_GRAY_SCOTT ? 2 * p->nx * p->nx : p->n);
     const int n = d->n;
     if (n < 1) { fail(NULL, 2, "problem: need at least one spatial unknown"); free(d); return NULL; }
 
@@ -441,7 +629,7 @@ orc_driver* orc_create(const orc_problem* p, const orc_grid* g, const orc_solver
     }
 
     d->ic = (double*)calloc((size_t)n, sizeof(double));
-    d->work = (double*)calloc((size_t)n * 8, sizeof(double));
+    d->work = (double*)calloc((size_t)n * 16, sizeof(double));
     if (p->kind == ORC_HEAT1D) {
         /* heat1d.cpp:13-22 mesh and sin profile; :24-45 factorization */
         if (!(p->x1 > p->x0)) { fail(NULL, 2, "heat1d: x1 must exceed x0"); orc_destroy(d); return NULL; }
@@ -474,6 +662,12 @@ orc_driver* orc_create(const orc_problem* p, const orc_grid* g, const orc_solver
         if (p->n_mult < d->L) { fail(NULL, 2, "scalar: one multiplier per level"); orc_destroy(d); return NULL; }
     } else if (p->kind == ORC_ALLEN_CAHN) {
         if (!(p->eps > 0.0) || !(p->length > 0.0)) { fail(NULL, 2, "allen-cahn: bad eps/length"); orc_destroy(d); return NULL; }
+    } else if (p->kind == ORC_GRAY_SCOTT) {
+        /* gray_scott.cpp:16-36 */
+        if (p->nx < 4) { fail(NULL, 2, "gray-scott: grid must be at least 4x4"); orc_destroy(d); return NULL; }
+        if (!(p->gs_domain > 0.0)) { fail(NULL, 2, "gray-scott: domain size must be positive"); orc_destroy(d); return NULL; }
+        gs_initial(d, d->ic);
+        d->gs_work = (double*)calloc((size_t)n * 13, sizeof(double));
     } else if (p->kind == ORC_HEAT2D) {
         if (p->source) {
             d->src = (double*)calloc((size_t)n, sizeof(double));
@@ -532,7 +726,7 @@ void orc_destroy(orc_driver* d) {
         free(d->cpr[l]); free(d->inv[l]);
         free(d->u[l]); free(d->gg[l]); free(d->v[l]); free(d->r[l]);
     }
-    free(d->work); free(d->ic); free(d->ff); free(d->fw); free(d->cval); free(d->prov);
+    free(d->work); free(d->gs_work); free(d->ic); free(d->ff); free(d->fw); free(d->cval); free(d->prov);
     free(d->src); free(d->rs); free(d->prevf);
     free(d);
 }

@@ -30,7 +30,7 @@ enum { ORC_OK = 0, ORC_NOT_CONVERGED = 1, ORC_CONFIG = 2, ORC_FAULT = 3,
        ORC_DIVERGED = 4, ORC_NONLINEAR = 5 };
 
 enum { ORC_HEAT1D = 1, ORC_DAHLQUIST = 2, ORC_SCALAR = 3, ORC_ALLEN_CAHN = 4,
-       ORC_HEAT2D = 5 };
+       ORC_HEAT2D = 5, ORC_GRAY_SCOTT = 6 };
 
 enum { ORC_TWO_LEVEL = 0, ORC_VCYCLE = 1, ORC_NESTED_V = 2 };
 enum { ORC_RELAX_F = 0, ORC_RELAX_FCF = 1 };
@@ -62,6 +62,10 @@ typedef struct orc_problem {
     const double* source;  /* f on the interior grid, nx*nx (may be NULL)   */
     /* optional initial-condition override (n values)                       */
     const double* ic;
+    /* gray-scott (gray_scott.hpp:24-38): n = nx cells per side, state [u; v]  */
+    double gs_domain, gs_feed, gs_kill, gs_du, gs_dv, gs_linear_tol;
+    int gs_reaction, gs_bounds_check;
+    double gs_bound_lo, gs_bound_hi;
 } orc_problem;
 
 typedef struct orc_grid {

@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 REF_BIN = os.path.join(HERE, "_ref", "tempo_ref")
 
-HEAT1D, DAHLQUIST, SCALAR, ALLEN_CAHN, HEAT2D = 1, 2, 3, 4, 5
+HEAT1D, DAHLQUIST, SCALAR, ALLEN_CAHN, HEAT2D, GRAY_SCOTT = 1, 2, 3, 4, 5, 6
 TWO_LEVEL, VCYCLE, NESTED_V = 0, 1, 2
 RELAX_F, RELAX_FCF = 0, 1
 NORM_L2, NORM_FUNCTIONAL = 0, 1
@@ -40,6 +40,10 @@ class Problem(C.Structure):
         ("newton_tol", C.c_double), ("newton_max", C.c_int),
         ("nx", C.c_int), ("cg_rtol", C.c_double), ("cg_max", C.c_int),
         ("source", _DP), ("ic", _DP),
+        ("gs_domain", C.c_double), ("gs_feed", C.c_double), ("gs_kill", C.c_double),
+        ("gs_du", C.c_double), ("gs_dv", C.c_double), ("gs_linear_tol", C.c_double),
+        ("gs_reaction", C.c_int), ("gs_bounds_check", C.c_int),
+        ("gs_bound_lo", C.c_double), ("gs_bound_hi", C.c_double),
     ]
 
 
@@ -130,6 +134,14 @@ class Driver:
         p.eps, p.length = problem.get("eps", 0.02), problem.get("length", 1.0)
         p.newton_tol, p.newton_max = problem.get("newton_tol", 1e-12), problem.get("newton_max", 30)
         p.nx, p.cg_rtol, p.cg_max = problem.get("nx", 0), problem.get("cg_rtol", 1e-12), problem.get("cg_max", 10000)
+        # gray-scott (gray_scott.hpp:24-38 defaults)
+        p.gs_domain, p.gs_feed = problem.get("domain", 2.5), problem.get("feed", 0.024)
+        p.gs_kill, p.gs_du, p.gs_dv = problem.get("kill", 0.06), problem.get("du", 8e-5), problem.get("dv", 4e-5)
+        p.gs_linear_tol = problem.get("linear_tol", 1e-10)
+        p.gs_reaction, p.gs_bounds_check = int(problem.get("reaction", 1)), int(problem.get("bounds_check", 1))
+        p.gs_bound_lo, p.gs_bound_hi = problem.get("bound_lo", -1.0), problem.get("bound_hi", 3.0)
+        if problem["kind"] == GRAY_SCOTT and "newton_tol" not in problem:
+            p.newton_tol = 1e-10
         for key, field, cnt in (("fine_forcing", "fine_forcing", "n_ff"), ("source", "source", None),
                                 ("ic", "ic", None)):
             if problem.get(key) is not None:

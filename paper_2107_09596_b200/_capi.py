@@ -26,6 +26,10 @@ class atm_problem(C.Structure):
         ("newton_tol", C.c_double), ("newton_max", C.c_int),
         ("nx", C.c_int), ("cg_rtol", C.c_double), ("cg_max", C.c_int),
         ("source", _DP), ("ic", _DP),
+        ("gs_domain", C.c_double), ("gs_feed", C.c_double), ("gs_kill", C.c_double),
+        ("gs_du", C.c_double), ("gs_dv", C.c_double), ("gs_linear_tol", C.c_double),
+        ("gs_reaction", C.c_int), ("gs_bounds_check", C.c_int),
+        ("gs_bound_lo", C.c_double), ("gs_bound_hi", C.c_double),
     ]
 
 

@@ -362,6 +362,48 @@ class AllenCahn(Application):
         return p
 
 
+class GrayScott(Application):
+    """problems::GrayScott (gray_scott.hpp:12-68): 2D Gray-Scott reaction-
+    diffusion on [0, domain]^2, periodic, n x n cells, state [u; v], backward
+    Euler with Newton (stop = max(tol, tol |F_0|), cap) and Jacobi-
+    preconditioned BiCGSTAB inner solves; the bounds check of step().
+    Forcing is folded.  The reference delegates BiCGSTAB to Eigen (absent
+    here); the oracle restates the published algorithm (parity unpinned)."""
+    kind = 6
+
+    def __init__(self, n=32, domain=2.5, feed=0.024, kill=0.06, du=8e-5, dv=4e-5, newton_tol=1e-10,
+                 newton_max_iters=30, linear_tol=1e-10, reaction=True, bounds_check=True,
+                 bound_lo=-1.0, bound_hi=3.0, initial_condition=None):
+        if n < 4:
+            raise ConfigError("gray-scott: grid must be at least 4x4")
+        if not domain > 0.0:
+            raise ConfigError("gray-scott: domain size must be positive")
+        self.n, self.domain, self.feed, self.kill, self.du, self.dv = n, domain, feed, kill, du, dv
+        self.newton_tol, self.newton_max_iters, self.linear_tol = newton_tol, newton_max_iters, linear_tol
+        self.reaction, self.bounds_check = reaction, bounds_check
+        self.bound_lo, self.bound_hi = bound_lo, bound_hi
+        self.ic = None if initial_condition is None else np.ascontiguousarray(initial_condition, np.float64).ravel()
+
+    def vector_size(self):
+        return 2 * self.n * self.n
+
+    def forcing_folded(self):
+        return True
+
+    def c_problem(self, keep):
+        p = _capi.atm_problem()
+        p.kind, p.n, p.folded, p.nx = self.kind, 2 * self.n * self.n, 1, self.n
+        p.newton_tol, p.newton_max = self.newton_tol, self.newton_max_iters
+        p.gs_domain, p.gs_feed, p.gs_kill = self.domain, self.feed, self.kill
+        p.gs_du, p.gs_dv, p.gs_linear_tol = self.du, self.dv, self.linear_tol
+        p.gs_reaction, p.gs_bounds_check = int(self.reaction), int(self.bounds_check)
+        p.gs_bound_lo, p.gs_bound_hi = self.bound_lo, self.bound_hi
+        if self.ic is not None:
+            keep.append(self.ic)
+            p.ic = ptr(self.ic)
+        return p
+
+
 class Heat2D(Application):
     """2D heat u_t = Lap(u) + f on the unit square, nx x nx interior points,
     5-point stencil, zero Dirichlet (BASELINE configs 2 and 4; no reference

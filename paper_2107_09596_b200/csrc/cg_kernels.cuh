@@ -30,6 +30,13 @@ struct CgCoefDev {
     double* xg;           // global scratch: x, r rows per cluster slot
     int E;                // 0: generic kernel; > 0: register variant, E elements per thread
     int nt;               // threads per CTA
+    // Gray-Scott (prob == 1): periodic nx x nx cells, state [u; v]; one CTA
+    // per system, every work vector in shared memory
+    int prob;
+    double gs_h2inv, gs_du, gs_dv, gs_feed, gs_kill, gs_linear_tol;
+    int gs_reaction, gs_bounds_check;
+    double gs_bound_lo, gs_bound_hi, newton_tol;
+    int newton_max;
 };
 
 // same job semantics as ScalarSweepArgs / the heat sweep kernel
@@ -56,6 +63,9 @@ struct CgWindowArgs {
 
 // host: cluster geometry for an nx x nx system (cs, R, E, nt, x placement)
 void cg_geometry(int nx, CgCoefDev& co);
+// host: Gray-Scott geometry (one CTA, 10 state-size vectors in smem); false
+// when 2 nx^2 does not fit
+bool gs_geometry(int nx, CgCoefDev& co);
 size_t cg_smem_bytes(const CgCoefDev& co);
 // clusters that can be resident at once (the number of x scratch rows needed)
 int cg_max_clusters(const CgCoefDev& co);

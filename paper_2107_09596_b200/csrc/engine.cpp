@@ -297,6 +297,18 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
             ac_ = true;
             folded_ = true;
             break;
+        case ATM_PHI_GRAY_SCOTT:
+            // problems::GrayScott (gray_scott.cpp:16-190): runs on the cluster
+            // CG machinery with a single-CTA Newton + BiCGSTAB Phi
+            if (p.nx < 4) config_error("gray-scott: grid must be at least 4x4");
+            if (!(p.gs_domain > 0.0)) config_error("gray-scott: domain size must be positive");
+            if (!(p.newton_tol > 0.0) || p.newton_max < 1 || !(p.gs_linear_tol > 0.0))
+                config_error("gray-scott: newton_tol, linear_tol > 0 and newton_max >= 1 required");
+            n_ = 2 * p.nx * p.nx;
+            h2d_ = true;
+            gs_ = true;
+            folded_ = true;
+            break;
         case ATM_PHI_HEAT2D:
             // BASELINE configs 2, 4 (no reference Phi; oracle/atm_oracle.c h2_solve)
             if (p.nx < 1) config_error("heat2d: need at least one interior point per side");
@@ -336,7 +348,28 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     } else if (!ac_ && !h2d_) {
         ic_[0] = p.u0;
     }
-    if (h2d_ && p.source) src_.assign(p.source, p.source + n_);
+    if (h2d_ && !gs_ && p.source) src_.assign(p.source, p.source + n_);
+    if (gs_) {
+        // GrayScott::initial_condition (gray_scott.cpp:38-61): u = 1, v = 0
+        // plus the sin^2 bump on [1, 1.5]^2, cell centres (j + 1/2) h
+        const int nx = p.nx, cells = nx * nx;
+        const double h = p.gs_domain / nx;
+        for (int i = 0; i < nx; ++i)
+            for (int j = 0; j < nx; ++j) {
+                const int c = i * nx + j;
+                const double x = (j + 0.5) * h, y = (i + 0.5) * h;
+                double u = 1.0, v = 0.0;
+                if (x >= 1.0 && x <= 1.5 && y >= 1.0 && y <= 1.5) {
+                    const double sx = std::sin(4.0 * kPi * x), sy = std::sin(4.0 * kPi * y);
+                    const double bump = 0.25 * sx * sx * sy * sy;
+                    u = 1.0 - 2.0 * bump;
+                    v = bump;
+                }
+                ic_[c] = u;
+                ic_[cells + c] = v;
+            }
+        if (p.ic) ic_.assign(p.ic, p.ic + n_);
+    }
     if (p.ic) ic_.assign(p.ic, p.ic + n_);
     if (kind_ == ATM_PHI_SCALAR && p.fine_forcing && p.n_ff > 0)
         ff_.assign(p.fine_forcing, p.fine_forcing + p.n_ff);
@@ -592,6 +625,27 @@ void Engine::build_coefs(Shard& s) {
                 for (int i = 0; i < n_; ++i) prof[i] = sinp_[i];
                 c.prof = up(prof);
             }
+        } else if (gs_) {
+            CgCoefDev& c = Lv.gco;
+            c.pitch = pitch_;
+            if (!gs_geometry(prob_.nx, c))
+                config_error("gray-scott: 2 nx^2 state exceeds the single-CTA kernel (nx <= 36)");
+            const double h = prob_.gs_domain / prob_.nx;
+            c.gs_h2inv = 1.0 / (h * h);
+            c.gs_du = prob_.gs_du;
+            c.gs_dv = prob_.gs_dv;
+            c.gs_feed = prob_.gs_feed;
+            c.gs_kill = prob_.gs_kill;
+            c.gs_linear_tol = prob_.gs_linear_tol;
+            c.gs_reaction = prob_.gs_reaction;
+            c.gs_bounds_check = prob_.gs_bounds_check;
+            c.gs_bound_lo = prob_.gs_bound_lo;
+            c.gs_bound_hi = prob_.gs_bound_hi;
+            c.newton_tol = prob_.newton_tol;
+            c.newton_max = prob_.newton_max;
+            c.sdt = sub_dt;
+            c.substeps = S;
+            c.fail = d_fail_;
         } else if (h2d_) {
             CgCoefDev& c = Lv.gco;
             c.pitch = pitch_;
@@ -1298,6 +1352,9 @@ void Engine::check_newton() {
     CK(cudaStreamSynchronize(st_));
     if (f) {
         CK(cudaMemsetAsync(d_fail_, 0, sizeof(int), st_));
+        if (gs_)
+            throw Error(ATM_NONLINEAR_FAIL, f == 2 ? "gray-scott: concentration left the bounding box"
+                                                   : "gray-scott: Newton or the inner BiCGSTAB failed");
         if (h2d_)
             throw Error(ATM_NONLINEAR_FAIL, "heat2d: CG did not converge in " +
                                                 std::to_string(prob_.cg_max) + " iterations");

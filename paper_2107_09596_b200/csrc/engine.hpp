@@ -184,7 +184,7 @@ private:
     Hier H_;
     Layout lay_;
     int n_ = 1, pitch_ = 1, kind_ = 0;
-    bool folded_ = false, heat_ = false, ac_ = false, h2d_ = false;
+    bool folded_ = false, heat_ = false, ac_ = false, h2d_ = false, gs_ = false;
     bool phi_forced_ = false;
     std::vector<int> Lvl_;   // row-kernel chunk length per level
     int sms_ = 148;

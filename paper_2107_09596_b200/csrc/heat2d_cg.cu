@@ -298,11 +298,218 @@ __device__ void cg_phi_reg(const CgCoefDev& co, Ctx& cx, double* xb, int band, b
     }
 }
 
+// ---------------------------------------------------------------------------
+// Gray-Scott Phi (gray_scott.cpp:91-190): backward Euler sub-steps, Newton
+// on F(w) = w - w_prev - dt f(w) with stop = max(tol, tol |F_0|), the
+// Jacobian J = I - dt f'(w) applied matrix-free, J delta = F by BiCGSTAB with
+// diagonal (Jacobi) right preconditioning from delta = 0 to |r|^2 <= tol^2
+// |F|^2 within 2 dim iterations (restart when rho degenerates) -- the
+// published algorithm behind the reference's Eigen::BiCGSTAB, restated in
+// oracle/atm_oracle.c gs_bicgstab; then the bounds check of step().  One CTA
+// per system; w and the nine work vectors live in shared memory; CTA
+// reductions in a fixed order.
+
+struct GsVec {
+    double *w, *prev, *x, *r, *r0, *p, *v, *s, *t, *yz;
+};
+
+__device__ __forceinline__ void gs_nbrs(int idx, int n, int cells, int& base, int& c, int& N,
+                                        int& S, int& E, int& W) {
+    base = idx >= cells ? cells : 0;
+    c = idx - base;
+    const int i = c / n, j = c - (c / n) * n;
+    N = ((i + 1 == n) ? 0 : i + 1) * n + j;
+    S = ((i == 0) ? n - 1 : i - 1) * n + j;
+    E = i * n + ((j + 1 == n) ? 0 : j + 1);
+    W = i * n + ((j == 0) ? n - 1 : j - 1);
+}
+
+// diagonal of J at element idx
+__device__ __forceinline__ double gs_diag(const CgCoefDev& co, const double* w, int idx, int cells,
+                                          double dt) {
+    const int c = idx >= cells ? idx - cells : idx;
+    const double u = w[c], v = w[cells + c];
+    if (idx < cells) {
+        double d = 1.0 + dt * 4.0 * co.gs_du * co.gs_h2inv;
+        if (co.gs_reaction) d += dt * (v * v + co.gs_feed);
+        return d;
+    }
+    double d = 1.0 + dt * 4.0 * co.gs_dv * co.gs_h2inv;
+    if (co.gs_reaction) d += dt * (co.gs_feed + co.gs_kill) - dt * 2.0 * u * v;
+    return d;
+}
+
+// (J x)[idx]
+__device__ __forceinline__ double gs_jx(const CgCoefDev& co, const double* w, const double* x,
+                                        int idx, int n, int cells, double dt) {
+    int base, c, N, S, E, W;
+    gs_nbrs(idx, n, cells, base, c, N, S, E, W);
+    const double u = w[c], v = w[cells + c];
+    const double nb = x[base + N] + x[base + S] + x[base + E] + x[base + W];
+    if (idx < cells) {
+        const double off = -dt * co.gs_du * co.gs_h2inv;
+        double r = gs_diag(co, w, idx, cells, dt) * x[idx] + off * nb;
+        if (co.gs_reaction) r += dt * 2.0 * u * v * x[cells + c];
+        return r;
+    }
+    const double offv = -dt * co.gs_dv * co.gs_h2inv;
+    double r = gs_diag(co, w, idx, cells, dt) * x[idx] + offv * nb;
+    if (co.gs_reaction) r += -dt * v * v * x[c];
+    return r;
+}
+
+// F[idx] = w - prev - dt f(w) (reaction_terms, gray_scott.cpp:63-88)
+__device__ __forceinline__ double gs_res(const CgCoefDev& co, const double* w, const double* prev,
+                                         int idx, int n, int cells, double dt) {
+    int base, c, N, S, E, W;
+    gs_nbrs(idx, n, cells, base, c, N, S, E, W);
+    const double u = w[c], v = w[cells + c];
+    const double lap = (w[base + N] + w[base + S] + w[base + E] + w[base + W] - 4.0 * w[idx]) * co.gs_h2inv;
+    double f;
+    if (idx < cells) {
+        f = co.gs_du * lap;
+        if (co.gs_reaction) f += -u * v * v + co.gs_feed * (1.0 - u);
+    } else {
+        f = co.gs_dv * lap;
+        if (co.gs_reaction) f += u * v * v - (co.gs_feed + co.gs_kill) * v;
+    }
+    return w[idx] - prev[idx] - dt * f;
+}
+
+__device__ void gs_phi(const CgCoefDev& co, Ctx& cx, const GsVec& g) {
+    const int n = co.nx, cells = n * n, m = 2 * cells;
+    const double dt = co.sdt;
+    auto loop = [&](auto&& f) {
+        for (int idx = cx.t; idx < m; idx += cx.nt) f(idx);
+    };
+    bool failed = false;
+    for (int sub = 0; sub < co.substeps && !failed; ++sub) {
+        loop([&](int i) { g.prev[i] = g.w[i]; });
+        __syncthreads();
+        double nr[1] = {0.0};
+        loop([&](int i) {
+            const double F = gs_res(co, g.w, g.prev, i, n, cells, dt);
+            g.r[i] = F;
+            nr[0] = fma(F, F, nr[0]);
+        });
+        cluster_sum<1>(nr, cx);
+        const double norm0 = sqrt(nr[0]);
+        const double stop = fmax(co.newton_tol, co.newton_tol * norm0);
+        if (norm0 <= stop) continue;
+        bool ok = false;
+        for (int it = 0; it < co.newton_max; ++it) {
+            // ---- BiCGSTAB: J x = b (b = F in r), x0 = 0
+            double bb[1] = {0.0};
+            loop([&](int i) {
+                const double b = g.r[i];
+                g.r0[i] = b;
+                g.x[i] = 0.0;
+                g.p[i] = 0.0;
+                g.v[i] = 0.0;
+                bb[0] = fma(b, b, bb[0]);
+            });
+            cluster_sum<1>(bb, cx);
+            const double tol2 = co.gs_linear_tol * co.gs_linear_tol * bb[0];
+            double rr = bb[0], r0n = bb[0];
+            double rho = 1.0, alpha = 1.0, om = 1.0;
+            const int maxit = 2 * m;
+            int lit = 0, restarts = 0;
+            while (rr > tol2 && lit < maxit) {
+                const double rho_old = rho;
+                double d1[1] = {0.0};
+                loop([&](int i) { d1[0] = fma(g.r0[i], g.r[i], d1[0]); });
+                cluster_sum<1>(d1, cx);
+                rho = d1[0];
+                if (fabs(rho) < 1e-30 * r0n) {
+                    loop([&](int i) { g.r0[i] = g.r[i]; });
+                    rho = r0n = rr;
+                    if (restarts++ == 0) lit = 0;
+                }
+                const double beta = (rho / rho_old) * (alpha / om);
+                loop([&](int i) {
+                    const double pi = g.r[i] + beta * (g.p[i] - om * g.v[i]);
+                    g.p[i] = pi;
+                    g.yz[i] = pi / gs_diag(co, g.w, i, cells, dt);
+                });
+                __syncthreads();
+                double d2[1] = {0.0};
+                loop([&](int i) {
+                    const double vi = gs_jx(co, g.w, g.yz, i, n, cells, dt);
+                    g.v[i] = vi;
+                    d2[0] = fma(g.r0[i], vi, d2[0]);
+                });
+                cluster_sum<1>(d2, cx);
+                alpha = rho / d2[0];
+                loop([&](int i) {
+                    g.x[i] += alpha * g.yz[i];
+                    const double si = g.r[i] - alpha * g.v[i];
+                    g.s[i] = si;
+                });
+                __syncthreads();
+                loop([&](int i) { g.yz[i] = g.s[i] / gs_diag(co, g.w, i, cells, dt); });
+                __syncthreads();
+                double d3[2] = {0.0, 0.0};
+                loop([&](int i) {
+                    const double ti = gs_jx(co, g.w, g.yz, i, n, cells, dt);
+                    g.t[i] = ti;
+                    d3[0] = fma(ti, ti, d3[0]);
+                    d3[1] = fma(ti, g.s[i], d3[1]);
+                });
+                cluster_sum<2>(d3, cx);
+                om = d3[0] > 0.0 ? d3[1] / d3[0] : 0.0;
+                double d4[1] = {0.0};
+                loop([&](int i) {
+                    g.x[i] += om * g.yz[i];
+                    const double ri = g.s[i] - om * g.t[i];
+                    g.r[i] = ri;
+                    d4[0] = fma(ri, ri, d4[0]);
+                });
+                cluster_sum<1>(d4, cx);
+                rr = d4[0];
+                ++lit;
+            }
+            if (!(rr <= tol2)) break;  // inner linear solve failed
+            // ---- Newton update and residual
+            loop([&](int i) { g.w[i] -= g.x[i]; });
+            __syncthreads();
+            double nn[1] = {0.0};
+            loop([&](int i) {
+                const double F = gs_res(co, g.w, g.prev, i, n, cells, dt);
+                g.r[i] = F;
+                nn[0] = fma(F, F, nn[0]);
+            });
+            cluster_sum<1>(nn, cx);
+            if (sqrt(nn[0]) <= stop) {
+                ok = true;
+                break;
+            }
+        }
+        if (!ok) failed = true;
+    }
+    if (failed) {
+        if (cx.t == 0) atomicExch(co.fail, 1);
+    } else if (co.gs_bounds_check) {
+        bool bad = false;
+        loop([&](int i) { bad = bad || !(g.w[i] >= co.gs_bound_lo && g.w[i] <= co.gs_bound_hi); });
+        if (bad) atomicExch(co.fail, 2);
+    }
+    __syncthreads();
+}
+
 template <int E>
 __device__ __forceinline__ void cg_phi_any(const CgCoefDev& co, Ctx& cx, double* xb, double* rb,
                                            int band, bool forced) {
-    if constexpr (E > 0) cg_phi_reg<E>(co, cx, xb, band, forced);
-    else cg_phi(co, cx, xb, rb, band, forced);
+    if constexpr (E < 0) {
+        // Gray-Scott: xb is vector 0 of the CTA's ten state-size vectors
+        const int m = 2 * co.nx * co.nx;
+        GsVec g{xb, xb + m, xb + 2 * m, xb + 3 * m, xb + 4 * m, xb + 5 * m, xb + 6 * m, xb + 7 * m,
+                xb + 8 * m, xb + 9 * m};
+        gs_phi(co, cx, g);
+    } else if constexpr (E > 0) {
+        cg_phi_reg<E>(co, cx, xb, band, forced);
+    } else {
+        cg_phi(co, cx, xb, rb, band, forced);
+    }
 }
 
 __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned char* smem) {
@@ -310,6 +517,10 @@ __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned 
     cx.q = (co.cs > 1) ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
     cx.rows = max(0, min(co.R, co.nx - cx.q * co.R));
     cx.own = cx.rows * co.nx;
+    if (co.prob == 1) {  // Gray-Scott: the whole [u; v] state is this CTA's band
+        cx.rows = 2 * co.nx;
+        cx.own = 2 * co.nx * co.nx;
+    }
     cx.W = co.nx + 2;
     cx.t = threadIdx.x;
     cx.nt = blockDim.x;
@@ -319,7 +530,7 @@ __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned 
     cx.dr = cx.nt - cx.dq * co.nx;
     cx.sh = reinterpret_cast<CgShared*>(smem);
     cx.ps = reinterpret_cast<double*>(smem + sizeof(CgShared));
-    const size_t psn = static_cast<size_t>(co.R + 2) * cx.W;
+    const size_t psn = co.prob == 1 ? 0 : static_cast<size_t>(co.R + 2) * cx.W;
     cx.xs = co.x_smem ? cx.ps + psn : nullptr;
     cx.rs = co.x_smem ? cx.ps + psn + static_cast<size_t>(co.R) * co.nx : nullptr;
     cx.par = 0;
@@ -526,6 +737,7 @@ CgKernels cg_k() {
 // E = 0: generic (x, r via pointers, A p recomputed); E > 0: register variant
 CgKernels cg_kernels(int E) {
     switch (E) {
+        case -1: return cg_k<-1>();
         case 1: return cg_k<1>();
         case 2: return cg_k<2>();
         case 4: return cg_k<4>();
@@ -611,7 +823,20 @@ void cg_geometry(int nx, CgCoefDev& co) {
     }
 }
 
+bool gs_geometry(int nx, CgCoefDev& co) {
+    co.nx = nx;
+    co.n = 2 * nx * nx;
+    co.prob = 1;
+    co.cs = 1;
+    co.R = 2 * nx;
+    co.E = -1;
+    co.x_smem = 1;
+    co.nt = std::min(kMaxCgThreads, std::max(64, (co.n + 31) / 32 * 32));
+    return cg_smem_bytes(co) <= kCgSmemCap;
+}
+
 size_t cg_smem_bytes(const CgCoefDev& co) {
+    if (co.prob == 1) return sizeof(CgShared) + 10 * static_cast<size_t>(co.n) * 8;
     size_t b = sizeof(CgShared) + static_cast<size_t>(co.R + 2) * (co.nx + 2) * 8;
     if (co.x_smem) b += 2 * static_cast<size_t>(co.R) * co.nx * 8;
     return b;

@@ -1,0 +1,79 @@
+"""Gray-Scott (the paper's flagship experiment) on the
+device vs the C oracle.  The reference delegates the inner linear solve to
+Eigen::BiCGSTAB (Eigen >= 3.3, absent here), so the oracle restates the
+published Jacobi-preconditioned BiCGSTAB and Newton of gray_scott.cpp:91-190
+(parity unpinned against the reference itself); the device runs the same
+algorithm per CTA (heat2d_cg.cu gs_phi) with different summation order."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2107_09596_b200 as T
+from helpers import rel_l2
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(n, n_points, tf, ms, k, mode="nested-v", tol=1e-7, max_iters=60, substeps=1, reaction=True):
+    app = T.GrayScott(n, reaction=reaction)
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, tf, n_points), ms, k)
+    cm = {"v-cycle": T.CycleMode.VCycle, "nested-v": T.CycleMode.NestedV}[mode]
+    cfg = T.SolverConfig(mode=cm, max_iters=max_iters, tol=tol, coarse_substeps=substeps)
+    orc = O.Driver(dict(kind=O.GRAY_SCOTT, nx=n, reaction=int(reaction)),
+                   dict(tf=tf, n_points=n_points, m=list(ms), k=k),
+                   dict(mode={"v-cycle": O.VCYCLE, "nested-v": O.NESTED_V}[mode], max_iters=max_iters,
+                        tol=tol, coarse_substeps=substeps))
+    return app, hier, cfg, orc
+
+
+@pytest.mark.parametrize("n", [8, 16, 32])
+@pytest.mark.parametrize("level", [0, 1])
+def test_gs_phi_matches_oracle(n, level):
+    app, hier, cfg, orc = _pair(n, 65, 8.0, [8], 4)
+    drv = T.CycleDriver(app, hier, cfg)
+    orc.setup()
+    w0 = orc.initial_condition()
+    rng = np.random.default_rng(n + level)
+    xs = np.stack([w0, w0 + 0.01 * rng.standard_normal(w0.size)])
+    got = drv.apply_phi(level, 1, xs)
+    for j in range(xs.shape[0]):
+        want = orc.step(level, 1 + j, xs[j])
+        assert rel_l2(got[j], want) <= 1e-9, (j, rel_l2(got[j], want))
+
+
+def test_gs_initial_condition_matches_oracle():
+    app, hier, cfg, orc = _pair(32, 65, 8.0, [8], 4)
+    drv = T.CycleDriver(app, hier, cfg)
+    drv.setup()
+    assert np.array_equal(drv.get_level(0)[0], orc.initial_condition())
+
+
+def test_gs_desk_config_matches_oracle():
+    # configs/grayscott_desk.cfg: n = 32, 512 points over [0, 64], nested-v,
+    # m = 16, k = 16, tol 1e-7
+    app, hier, cfg, orc = _pair(32, 512, 64.0, [16], 16)
+    res = T.solve(app, hier, cfg)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"], (res.report.iterations, ref["iterations"])
+    hist = np.array(res.report.residual_norms)
+    assert np.all(np.abs(hist - ref["history"]) <= 1e-6 * np.abs(ref["history"]) + 1e-12)
+    assert rel_l2(res.state, orc.array(0)) <= 1e-9
+
+
+def test_gs_pure_diffusion_vcycle_matches_oracle():
+    app, hier, cfg, orc = _pair(16, 129, 16.0, [4, 4], 3, mode="v-cycle", reaction=False, substeps=2,
+                                tol=1e-9)
+    res = T.solve(app, hier, cfg)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"]
+    assert rel_l2(res.state, orc.array(0)) <= 1e-9
+
+
+def test_gs_bounds_check_raises():
+    app, hier, cfg, _ = _pair(8, 17, 8.0, [4], 2)
+    drv = T.CycleDriver(app, hier, cfg)
+    bad = np.full(2 * 64, 5.0)  # outside [-1, 3]
+    with pytest.raises(T.NonlinearSolveError):
+        drv.apply_phi(0, 1, bad[None, :])
