@@ -8,9 +8,8 @@
 // total_seconds` summary, `sweep-k` writes `m,k,k_over_ncpoints,iterations,
 // parareal_equivalent` rows (k = 0 selects the full coarse grid).  Exit codes
 // 0 converged / 1 not converged / 2 config error / 3 runtime fault.
-// Problems: dahlquist, heat1d (the reference's) plus allencahn, heat2d (the
-// BASELINE configs 2-4 families); grayscott needs Eigen's BiCGSTAB and is not
-// available.
+// Problems: dahlquist, heat1d, grayscott (the reference's) plus allencahn,
+// heat2d (the BASELINE configs 2-4 families).
 //
 //   tempo_b200 solve CONFIG [--out PATH] [--workers N]
 //   tempo_b200 sweep-k CONFIG [--out PATH] [--workers N]
@@ -146,8 +145,9 @@ std::vector<std::string> problem_keys(const std::string& p) {
                 "allencahn.newton_max_iters", "allencahn.ic_seed", "allencahn.ic_amplitude"};
     if (p == "heat2d") return {"heat2d.nx", "heat2d.cg_rtol", "heat2d.cg_max_iters"};
     if (p == "grayscott")
-        throw ConfigErr("config: problem 'grayscott' needs Eigen's BiCGSTAB and is not available "
-                        "on the GPU path");
+        return {"grayscott.n",    "grayscott.domain",     "grayscott.feed",
+                "grayscott.kill", "grayscott.du",         "grayscott.dv",
+                "grayscott.newton_tol", "grayscott.newton_max_iters"};
     throw ConfigErr("config: unknown problem '" + p + "'");
 }
 
@@ -216,6 +216,24 @@ Built build(const Config& c, const std::vector<int>& m, int k, int workers) {
         atm_random_state(static_cast<uint64_t>(c.integer("allencahn.ic_seed", 3)), b.p.n, b.ic.data());
         const double amp = c.num("allencahn.ic_amplitude", 0.05);
         for (double& v : b.ic) v *= amp;
+    } else if (prob == "grayscott") {
+        // GrayScott::Options defaults (gray_scott.hpp:24-38)
+        b.p.kind = ATM_PHI_GRAY_SCOTT;
+        b.p.nx = c.integer("grayscott.n", 32);
+        b.p.n = 2 * b.p.nx * b.p.nx;
+        b.p.gs_domain = c.num("grayscott.domain", 2.5);
+        b.p.gs_feed = c.num("grayscott.feed", 0.024);
+        b.p.gs_kill = c.num("grayscott.kill", 0.06);
+        b.p.gs_du = c.num("grayscott.du", 8e-5);
+        b.p.gs_dv = c.num("grayscott.dv", 4e-5);
+        b.p.newton_tol = c.num("grayscott.newton_tol", 1e-10);
+        b.p.newton_max = c.integer("grayscott.newton_max_iters", 30);
+        b.p.gs_linear_tol = 1e-10;
+        b.p.gs_reaction = 1;
+        b.p.gs_bounds_check = 1;
+        b.p.gs_bound_lo = -1.0;
+        b.p.gs_bound_hi = 3.0;
+        b.p.folded = 1;
     } else if (prob == "heat2d") {
         b.p.kind = ATM_PHI_HEAT2D;
         b.p.nx = c.integer("heat2d.nx", 127);

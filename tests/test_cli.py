@@ -35,7 +35,7 @@ def run(tmp_path, text, cmd="solve", *extra):
     ("problem = heat1d\nsolver.m = 4\nsolver.k = 2\ngrid.n_points = 33\nsolver.tol = 1e-9\n"
      "grid.tf = 1\nsolver.mode = w-cycle\n", "solver.mode must be"),
     ("problem = lorenz\n", "unknown problem 'lorenz'"),
-    ("problem = grayscott\n", "not available"),
+    ("problem = grayscott\ngrayscott.bogus = 1\n", "unknown key 'grayscott.bogus'"),
 ])
 def test_cli_config_errors_exit_2(tmp_path, text, needle):
     code, _, err = run(tmp_path, text)
@@ -113,3 +113,20 @@ def test_cli_not_converged_exit_1(tmp_path):
     assert code == 1
     _, conv, iters = _rows(out)
     assert conv == 0 and iters == 3
+
+
+@pytest.mark.gpu
+def test_cli_grayscott_desk_matches_oracle(tmp_path):
+    # configs/grayscott_desk.cfg (the paper's desk-scale run); iteration
+    # count from the oracle restatement (the reference needs Eigen)
+    from oracle import oracle as O
+    orc = O.Driver(dict(kind=O.GRAY_SCOTT, nx=32), dict(tf=64.0, n_points=512, m=[16], k=16),
+                   dict(mode=O.NESTED_V, tol=1e-7, max_iters=60))
+    want = orc.drive()
+    code, out, err = run(tmp_path, "problem = grayscott\ngrayscott.n = 32\ngrid.tf = 64.0\n"
+                         "grid.n_points = 512\nsolver.mode = nested-v\nsolver.m = 16\nsolver.k = 16\n"
+                         "solver.tol = 1e-7\nsolver.max_iters = 60\nruntime.workers = 1\n")
+    assert code == 0, err
+    hist, conv, iters = _rows(out)
+    assert conv == 1 and iters == want["iterations"]
+    np.testing.assert_allclose(hist, want["history"], rtol=1e-6)
