@@ -338,6 +338,9 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
         config_error("provided initial guess has the wrong number of points");
 
     pitch_ = (heat_ || h2d_) ? ((n_ + 15) / 16) * 16 : 1;
+    // L = 32 row kernels (pitch > 2048): a thread's chunk must not straddle
+    // the row end, so rows are whole 32-element chunks
+    if (heat_ && !ac_ && pitch_ > 2048) pitch_ = ((n_ + 31) / 32) * 32;
     // host copies of caller-owned inputs
     ic_.assign(n_, 0.0);
     if (heat_ && !ac_) {

@@ -295,3 +295,31 @@ def test_config5_shape_bitwise_across_shard_counts():
             continue
         assert np.array_equal(norms, base[0]), workers
         assert np.array_equal(u, base[1]), workers
+
+
+@pytest.mark.parametrize("n", [2047, 2048, 2049, 3001, 4096])
+def test_two_level_solve_across_chunk_lengths(n):
+    # n around the L = 16 / L = 32 switch (pitch > 2048) and the exact fit
+    # (dt/h^2 ~ 1000, the stiffness of the BASELINE configs; at 1e4 the
+    # reference's own fp64 Thomas error alone reaches ~1e-10 of the state)
+    args = dict(problem="heat1d", n=n, tf=1.0 / 64, n_points=257, m=8, k=4, manufactured=1,
+                guess="random", seed=13, max_iters=60, tol=1e-9)
+    app, hier, cfg = device_objects(args)
+    res = T.solve(app, hier, cfg)
+    orc = oracle_driver(args)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"]
+    assert rel_l2(res.state, orc.array(0)) <= SOLVE_RTOL
+
+
+def test_fas_vcycle_mixed_chunk_lengths_matches_oracle():
+    # n = 4095: levels 0-1 run L = 32 sweeps, the coarsest level L = 16
+    # windows; level-l sweeps store restriction tails into level l+1 arrays
+    args = dict(problem="heat1d", n=4095, folded=1, tf=1.0 / 32, n_points=513, m="4,4", k=3,
+                mode="v-cycle", manufactured=1, guess="random", seed=17, max_iters=40, tol=1e-9)
+    app, hier, cfg = device_objects(args)
+    res = T.solve(app, hier, cfg)
+    orc = oracle_driver(args)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"]
+    assert rel_l2(res.state, orc.array(0)) <= SOLVE_RTOL
