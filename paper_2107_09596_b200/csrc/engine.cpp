@@ -482,6 +482,7 @@ Engine::~Engine() {
         cudaEventDestroy(pe.second.second);
     }
     for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (comm_ && nccl_) nccl_->CommDestroy(static_cast<ncclComm_t>(comm_));
     if (st_) cudaStreamDestroy(st_);
 }
@@ -1337,11 +1338,46 @@ void Engine::two_level_cycle() {
     phase_end();
 }
 
+// One cycle = a fixed launch sequence on one stream: captured once into a
+// CUDA graph and replayed (small configs are launch-bound).
+// Not with phase tracing (host-side event bookkeeping), multi-process NCCL,
+// or the Newton / CG families (their failure flag is read back every cycle).
+bool Engine::use_graphs() const {
+    if (world_ > 1 || trace_ || ac_ || h2d_) return false;
+    return !std::getenv("ATM_NO_GRAPH") && !std::getenv("ATM_DEBUG_DUMP") &&
+           !std::getenv("ATM_SYNC_PHASES");
+}
+
 void Engine::cycle() {
     setup();
     launches_ = 0;
-    if (sol_.mode == ATM_TWO_LEVEL) two_level_cycle();
-    else v_cycle(0);
+    const bool graphs = use_graphs();
+    if (graphs && graph_exec_) {
+        CK(cudaGraphLaunch(graph_exec_, st_));
+        last_launches_ = graph_launches_;
+        return;
+    }
+    if (graphs) CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    try {
+        if (sol_.mode == ATM_TWO_LEVEL) two_level_cycle();
+        else v_cycle(0);
+    } catch (...) {
+        if (graphs) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(st_, &g);
+            if (g) cudaGraphDestroy(g);
+        }
+        throw;
+    }
+    if (graphs) {
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamEndCapture(st_, &g));
+        const cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+        graph_launches_ = launches_;
+        CK(cudaGraphLaunch(graph_exec_, st_));
+    }
     last_launches_ = launches_;
     check_newton();
 }

@@ -228,6 +228,10 @@ private:
     cudaEvent_t cur_ev_ = nullptr;
     std::vector<cudaEvent_t> ev_pool_;
     int launches_ = 0, last_launches_ = 0;
+    // CUDA graph of one cycle (captured on the first cycle, then replayed)
+    bool use_graphs() const;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    int graph_launches_ = 0;
     double last_sweep_ms_ = 0.0;
 };
 

@@ -323,3 +323,17 @@ def test_fas_vcycle_mixed_chunk_lengths_matches_oracle():
     ref = orc.drive()
     assert res.report.iterations == ref["iterations"]
     assert rel_l2(res.state, orc.array(0)) <= SOLVE_RTOL
+
+
+def test_cuda_graph_replay_bitwise_equals_direct_launches(monkeypatch):
+    # cycles replayed from the captured CUDA graph produce bitwise the
+    # directly launched cycles' histories and states
+    args = dict(problem="heat1d", n=255, tf=1.0, n_points=1025, m=16, k=4, manufactured=1,
+                guess="random", seed=3, max_iters=30, tol=1e-12)
+    app, hier, cfg = device_objects(args)
+    a = T.solve(app, hier, cfg)
+    monkeypatch.setenv("ATM_NO_GRAPH", "1")
+    b = T.solve(app, hier, cfg)
+    assert a.report.iterations == b.report.iterations
+    assert np.array_equal(np.array(a.report.residual_norms), np.array(b.report.residual_norms))
+    assert np.array_equal(a.state, b.state)
