@@ -49,6 +49,13 @@ def configs():
                              initial_condition=T.fourier_ic(511)),
         grid=(0.0, 4.0 * 4096 / 65536, 4097, [8, 8, 8], 2), mode=T.CycleMode.VCycle, relax=T.Relaxation.F,
         iters=1)
+    # Gray-Scott desk run (configs/grayscott_desk.cfg; the paper's flagship
+    # problem): n = 32, 512 points over [0, 64], nested-v, m = k = 16
+    c[6] = dict(
+        name="grayscott_desk_n32_512pts_m16_k16_nested",
+        app=lambda: T.GrayScott(32),
+        grid=(0.0, 64.0, 512, [16], 16), mode=T.CycleMode.NestedV, relax=T.Relaxation.F, iters=2,
+        guess=T.InitialGuess.Constant, tol=1e-7)
     return c
 
 
@@ -69,8 +76,8 @@ def run(cfg):
     app = cfg["app"]()
     t0, tf, npts, ms, k = cfg["grid"]
     hier = T.build_hierarchy(T.TimeGrid.make(t0, tf, npts), ms, k)
-    sc = T.SolverConfig(mode=cfg["mode"], relaxation=cfg["relax"], max_iters=100, tol=1e-10,
-                        initial_guess=T.InitialGuess.Random, seed=20)
+    sc = T.SolverConfig(mode=cfg["mode"], relaxation=cfg["relax"], max_iters=100, tol=cfg.get("tol", 1e-10),
+                        initial_guess=cfg.get("guess", T.InitialGuess.Random), seed=20)
     drv = T.CycleDriver(app, hier, sc)
     w0 = time.perf_counter()
     drv.setup()
@@ -89,7 +96,7 @@ def run(cfg):
 # per-level dt at reduced N_t: one cycle each
 # (config 4: two levels, m = 8, at 17 points -- its four-level hierarchy
 # needs >= 513 points, hours of single-thread CG)
-CPU_SAMPLES = {1: (1025, None), 2: (257, None), 3: (1025, None), 4: (17, [8])}
+CPU_SAMPLES = {1: (1025, None), 2: (257, None), 3: (1025, None), 4: (17, [8]), 6: (512, None)}
 
 
 def run_cpu(i, cfg):
@@ -103,18 +110,24 @@ def run_cpu(i, cfg):
     hier = T.build_hierarchy(T.TimeGrid.make(t0, tf_s, sp), ms, k)
     keep = []
     p = app.c_problem(keep)
-    kind = {T.Heat1D: O.HEAT1D, T.Heat2D: O.HEAT2D, T.AllenCahn: O.ALLEN_CAHN}[type(app)]
+    kind = {T.Heat1D: O.HEAT1D, T.Heat2D: O.HEAT2D, T.AllenCahn: O.ALLEN_CAHN,
+            T.GrayScott: O.GRAY_SCOTT}[type(app)]
     prob = dict(kind=kind, n=app.vector_size(), folded=int(p.folded), manufactured=int(p.manufactured),
                 eps=p.eps, length=p.length, newton_tol=p.newton_tol, newton_max=p.newton_max,
                 nx=p.nx, cg_rtol=p.cg_rtol, cg_max=p.cg_max,
                 source=getattr(app, "source", None), ic=getattr(app, "ic", None))
-    mode = {T.CycleMode.TwoLevel: O.TWO_LEVEL, T.CycleMode.VCycle: O.VCYCLE}[cfg["mode"]]
+    mode = {T.CycleMode.TwoLevel: O.TWO_LEVEL, T.CycleMode.VCycle: O.VCYCLE,
+            T.CycleMode.NestedV: O.NESTED_V}[cfg["mode"]]
     if len(ms) == 1 and mode == O.VCYCLE:
         mode = O.VCYCLE  # FAS two-grid (folded)
     orc = O.Driver(prob, dict(t0=t0, tf=tf_s, n_points=sp, m=list(ms), k=k),
                    dict(mode=mode, relaxation=O.RELAX_FCF if cfg["relax"] == T.Relaxation.FCF else O.RELAX_F,
-                        max_iters=100, tol=1e-10, initial_guess=O.GUESS_RANDOM, seed=20))
+                        max_iters=100, tol=cfg.get("tol", 1e-10),
+                        initial_guess=O.GUESS_CONSTANT if cfg.get("guess") == T.InitialGuess.Constant
+                        else O.GUESS_RANDOM, seed=20))
     orc.setup()
+    if mode == O.NESTED_V:
+        orc.nested_init()
     w0 = time.perf_counter()
     orc.cycle()
     dt = time.perf_counter() - w0
@@ -126,7 +139,7 @@ def run_cpu(i, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
-    ap.add_argument("--only", default="1,2,3,4")
+    ap.add_argument("--only", default="1,2,3,4,6")
     ap.add_argument("--cpu", action="store_true")
     a = ap.parse_args()
     res = []
