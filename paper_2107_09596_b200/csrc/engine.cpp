@@ -607,8 +607,6 @@ void Engine::build_coefs(Shard& s) {
             c.cneg_c = hh.cneg_c;
             c.sigma = hh.sigma;
             c.ncw = hh.ncw;
-            // timing experiments only (wrong numerics): drop the boundary correction
-            if (std::getenv("ATM_DEBUG_NOCORR")) c.ncw = 0;
             c.n = n_;
             c.pitch = pitch_;
             c.nt = hh.nt;
@@ -1238,24 +1236,8 @@ void Engine::windows(int kind) {
         const int forced = phi_forced_;
         if (kind == WK_LINEAR) {
             LevelDev& F = s.lv[0];
-            const char* dump = std::getenv("ATM_DEBUG_DUMP");
-            auto dump_rows = [&](const char* tag) {
-                CK(cudaStreamSynchronize(st_));
-                std::vector<double> h(static_cast<size_t>(C.r.rows) * pitch_);
-                CK(cudaMemcpy(h.data(), C.r.p, h.size() * 8, cudaMemcpyDeviceToHost));
-                FILE* f = std::fopen((std::string(dump) + "_r_" + tag).c_str(), "wb");
-                std::fwrite(h.data(), 8, h.size(), f);
-                std::fclose(f);
-                std::vector<double> u(static_cast<size_t>(F.u.rows) * pitch_);
-                CK(cudaMemcpy(u.data(), F.u.p, u.size() * 8, cudaMemcpyDeviceToHost));
-                f = std::fopen((std::string(dump) + "_u_" + tag).c_str(), "wb");
-                std::fwrite(u.data(), 8, u.size(), f);
-                std::fclose(f);
-            };
-            if (dump) dump_rows("before");
             window_launch(s, lc, WK_LINEAR, 0, pre_e0, pre_e1, p0, p1, C.r, C.r, C.r, F.u, H_.m[0],
                           forced, 0, 0, 0);
-            if (dump) dump_rows("after");
         } else if (kind == WK_FAS) {
             // Psi(v_{j-1}) once per coarse point, shared by every window
             const int a0 = std::max(1, C.base + 1);
@@ -1344,8 +1326,7 @@ void Engine::two_level_cycle() {
 // or the Newton / CG families (their failure flag is read back every cycle).
 bool Engine::use_graphs() const {
     if (world_ > 1 || trace_ || ac_ || h2d_) return false;
-    return !std::getenv("ATM_NO_GRAPH") && !std::getenv("ATM_DEBUG_DUMP") &&
-           !std::getenv("ATM_SYNC_PHASES");
+    return !std::getenv("ATM_NO_GRAPH") && !std::getenv("ATM_SYNC_PHASES");
 }
 
 void Engine::cycle() {
@@ -1594,14 +1575,6 @@ int Engine::solve(atm_report* rep, double* norms) {
 
 // ---------------------------------------------------------------------------
 // state access and kernel-level entry points
-
-static LevelDev* owner_level(std::vector<Shard>& sh, int level, int i) {
-    for (Shard& s : sh) {
-        LevelDev& Lv = s.lv[level];
-        if (i >= Lv.lo && i <= Lv.hi) return &Lv;
-    }
-    return nullptr;
-}
 
 // copy [first, first+count) of one array kind between host and device,
 // one 2D copy per owning shard

@@ -1,20 +1,25 @@
-// heat_phi5.cu -- Heat1D Phi chains for sm_100a.
+// heat_phi5.cu -- 1D row Phi chains for sm_100a: Heat1D and Allen-Cahn.
 //
 // One CTA owns one state vector (a time point) in registers, blocked
-// (thread t holds elements [t*L, t*L+L)).  Rows move HBM <-> smem by TMA
-// (cp.async.bulk.tensor, 128B-swizzled so the blocked register view reads
-// and writes smem conflict-free); produced rows leave through TMA-store
-// staging so stores overlap the next Phi.
+// (thread t holds elements [t*L, t*L+L); L = 32 / 128 threads for the level-0
+// sweeps of 2048 < n <= 4096, L <= 16 otherwise).  Rows move HBM -> smem by
+// TMA (cp.async.bulk.tensor, 128B-swizzled so the blocked register view reads
+// and writes smem conflict-free); produced rows leave by per-warp TMA stores
+// of 1024-byte-aligned slices, so a stored row needs no CTA barrier and the
+// stores overlap the next Phi.
 //
 // One Phi sub-step solves (I + sub_dt L) x = b, T = tridiag(a, b0, a) with
 // a = -r, b0 = 1 + 2r (heat1d.cpp:24-60).  With (c*, d*) the fixed point of
 // the Thomas recurrence, T = L_c U_c + delta e0 e0^T (delta = a c*), so
-//     x = M^{-1} b - sigma (g . b) w,   M = L_c U_c, w = M^{-1} e0, g = M^{-T} e0
+//     x = M^{-1} b - sigma x0 w,   M = L_c U_c, w = M^{-1} e0, x0 = (M^{-1} b)_0
 // (Sherman-Morrison).  Every thread runs the constant-coefficient recurrences
-// from registers; g and w decay geometrically from the boundary and only
-// touch the first `ncw` warps, as independent FMAs.  (In fp64 this is more
-// accurate than the serial Thomas sweep with its non-converged leading
-// factors; see tests/test_gpu_parity.py.)
+// from registers.  On every chunk w lies in span{q, p_b}, the two vectors the
+// blocked solve combines anyway, so the correction is two extra terms in the
+// chunk's carry coefficients (only in the first `ncw` warps, where w is not
+// negligible).  The periodic (Allen-Cahn) matrix adds the corner entries: a
+// rank-2 Woodbury term with the right-end vector folded the same way.  (In
+// fp64 this is more accurate than the serial Thomas sweep with its
+// non-converged leading factors; see tests/test_gpu_parity.py.)
 //
 // M^{-1} b is evaluated with ONE CTA barrier:
 //   1. forward local pass      y_loc = L^{-1} b on the chunk (zero carry-in)
@@ -22,9 +27,9 @@
 //   3. backward local pass     z_loc = U^{-1} y_loc   (the forward carry c_f
 //      enters linearly as c_f q with q = U^{-1} p_f, precomputed)
 //   4. backward warp scan of a = z_loc[0] + E q0 -> RA, warp total TA
-//   5. publish (Tf, TA, g.b partials), bar.sync, cross-warp carries as fixed
-//      weighted sums (lane-parallel + xor tree)
-//   6. x = z_loc + c_f q + c_b p_b - s w
+//   5. publish (Tf, TA and the correction pick-ups), bar.sync, cross-warp
+//      carries as fixed weighted sums (lane-parallel + xor tree)
+//   6. x = z_loc + c_f q + c_b p_b (c_f, c_b include the correction)
 // All multipliers are precomputed on the host (heat_level_host).
 //
 // Proxy rule: a buffer filled by TMA and read with ld.shared is handed back
