@@ -284,22 +284,56 @@ void check(atm_status st, atm_ctx* ctx) {
     throw Fault(msg);
 }
 
-// drive (solver.cpp:398-435) one iteration at a time for per-iteration seconds
-RunResult run(const Built& b) {
+// per-phase device seconds since setup, by name (atm_phase_times)
+std::map<std::string, double> phase_seconds(atm_ctx* ctx) {
+    char names[2048];
+    double secs[64];
+    const int k = atm_phase_times(ctx, names, sizeof(names), secs, 64);
+    std::map<std::string, double> out;
+    std::stringstream ss(names);
+    std::string nm;
+    for (int i = 0; i < k && std::getline(ss, nm, ','); ++i) out[nm] = secs[i];
+    return out;
+}
+
+// drive (solver.cpp:398-435) one iteration at a time for per-iteration
+// seconds; with a trace path, per-iteration phase rows `iter,rank,phase,
+// seconds` like the reference's TraceSink (run_config.cpp:272-283), timed on
+// the device with CUDA events
+RunResult run(const Built& b, const std::string& trace_path = "") {
     RunResult r;
     atm_ctx* ctx = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
-    check(atm_create(&b.p, &b.g, &b.s, &b.rt, &ctx), nullptr);
+    std::ofstream trace;
+    Built bt = b;
+    if (!trace_path.empty()) {
+        trace.open(trace_path);
+        if (!trace) throw ConfigErr("cannot open trace file '" + trace_path + "'");
+        trace << "iter,rank,phase,seconds\n";
+        trace.precision(17);
+        bt.rt.trace = 1;
+    }
+    check(atm_create(&bt.p, &bt.g, &bt.s, &bt.rt, &ctx), nullptr);
     struct Guard {
         atm_ctx* c;
         ~Guard() { atm_destroy(c); }
     } guard{ctx};
     check(atm_setup(ctx), ctx);
     if (b.s.mode == ATM_NESTED_V) check(atm_nested_init(ctx), ctx);
+    std::map<std::string, double> before;
+    if (trace.is_open()) before = phase_seconds(ctx);
     for (int it = 1; it <= b.s.max_iters; ++it) {
         const auto a = std::chrono::steady_clock::now();
         double v = 0.0;
         check(atm_iterate(ctx, 1, &v), ctx);
+        if (trace.is_open()) {
+            const std::map<std::string, double> now = phase_seconds(ctx);
+            for (const auto& kv : now) {
+                const double d = kv.second - (before.count(kv.first) ? before[kv.first] : 0.0);
+                if (d > 0.0) trace << it << ",0," << kv.first << ',' << d << '\n';
+            }
+            before = now;
+        }
         r.secs.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count());
         r.norms.push_back(v);
         r.iterations = it;
@@ -322,7 +356,7 @@ int cmd_solve(const Config& c, const std::string& out_path, int workers_override
     c.only(allowed);
     const int workers = workers_override > 0 ? workers_override : c.integer("runtime.workers", 1);
     const Built b = build(c, c.ints("solver.m"), c.integer("solver.k"), workers);
-    const RunResult r = run(b);
+    const RunResult r = run(b, c.str("runtime.trace", ""));
     std::ofstream file;
     const std::string path = !out_path.empty() ? out_path : c.str("output.path", "");
     if (!path.empty()) {

@@ -130,3 +130,23 @@ def test_cli_grayscott_desk_matches_oracle(tmp_path):
     hist, conv, iters = _rows(out)
     assert conv == 1 and iters == want["iterations"]
     np.testing.assert_allclose(hist, want["history"], rtol=1e-6)
+
+
+@pytest.mark.gpu
+def test_cli_trace_rows(tmp_path):
+    trace = tmp_path / "trace.csv"
+    code, out, err = run(tmp_path, "problem = heat1d\nheat1d.dof = 63\ngrid.tf = 1.0\n"
+                         "grid.n_points = 257\nsolver.m = 16\nsolver.k = 2\nsolver.tol = 1e-9\n"
+                         "solver.initial_guess = random\nsolver.seed = 20\nsolver.max_iters = 50\n"
+                         f"runtime.trace = {trace}\n")
+    assert code == 0, err
+    _, _, iters = _rows(out)
+    rows = trace.read_text().strip().splitlines()
+    assert rows[0] == "iter,rank,phase,seconds"
+    phases = {}
+    for r in rows[1:]:
+        it, rank, ph, sec = r.split(",")
+        assert 1 <= int(it) <= iters and rank == "0" and float(sec) > 0.0
+        phases.setdefault(ph, set()).add(int(it))
+    for ph in ("relax", "restrict", "coarse", "correct", "norm"):
+        assert phases.get(ph) == set(range(1, iters + 1)), ph
