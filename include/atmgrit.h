@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define ATM_ABI_VERSION 2
+#define ATM_ABI_VERSION 3
 #define ATM_MAX_LEVELS 8
 
 typedef enum {
@@ -111,6 +111,9 @@ typedef struct atm_runtime {
     const void* nccl_id; /* 128-byte ncclUniqueId (world_size > 1)                 */
     int storage;       /* atm_storage                                              */
     int trace;         /* record per-phase cudaEvent timings                       */
+    int reuse_relax;   /* two-level F-relaxation: skip a cycle's opening F-sweep,
+                          whose results the previous correction F-sweep already
+                          produced (bitwise the same cycle; opt-in)                */
 } atm_runtime;
 
 /* ConvergenceReport (solver_config.hpp:57-64). */

@@ -48,7 +48,7 @@ class atm_solver(C.Structure):
 class atm_runtime(C.Structure):
     _fields_ = [("device", C.c_int), ("n_shards", C.c_int), ("world_size", C.c_int),
                 ("rank", C.c_int), ("nccl_id", C.c_void_p), ("storage", C.c_int),
-                ("trace", C.c_int)]
+                ("trace", C.c_int), ("reuse_relax", C.c_int)]
 
 
 class atm_report(C.Structure):

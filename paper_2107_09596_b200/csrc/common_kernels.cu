@@ -249,8 +249,8 @@ __global__ void scalar_sweep_kernel(ScalarSweepArgs a) {
         if (a.add_g) r += a.g[ti - a.g_base];
         r -= a.u[ti - a.u_base];
         const int ci = ti / m;
-        if (a.tail == TAIL_STORE) a.out[ci - a.out_base] = r;
-        else a.sq[ti - a.sq_base] = r * r;
+        if (a.tail == TAIL_STORE || a.tail == TAIL_BOTH) a.out[ci - a.out_base] = r;
+        if (a.tail == TAIL_SQ || a.tail == TAIL_BOTH) a.sq[ti - a.sq_base] = r * r;
     }
 }
 

@@ -751,7 +751,8 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
     LevelDev& Lv = s.lv[level];
     const int m = m_override > 0 ? m_override : H_.m[level];
     const bool add_g = Lv.g_full;
-    LevelDev* out_lv = (tail == TAIL_STORE && m_override <= 0) ? &s.lv[level + 1] : nullptr;
+    LevelDev* out_lv =
+        ((tail == TAIL_STORE || tail == TAIL_BOTH) && m_override <= 0) ? &s.lv[level + 1] : nullptr;
     if (heat_) {
         SweepArgs a{};
         a.co = Lv.hco;
@@ -1122,14 +1123,16 @@ void Engine::point0_residual(Shard& s, int level, double* r_out, double* sq_out)
 // F-relaxation over own intervals (kernels.cpp:7-17) with optional tail
 void Engine::f_sweep(int level, int tail, int store) {
     halo(level, &LevelDev::u);
-    const char* tag = level != 0 ? nullptr : tail == TAIL_SQ ? "sweep_correct"
-                                           : tail == TAIL_STORE ? "sweep_relax" : "sweep_f";
+    const char* tag = level != 0 ? nullptr
+                      : (tail == TAIL_SQ || tail == TAIL_BOTH) ? "sweep_correct"
+                      : tail == TAIL_STORE                     ? "sweep_relax"
+                                                               : "sweep_f";
     if (tag) phase_begin(tag);
     for (Shard& s : sh_) {
         LevelDev& Lv = s.lv[level];
         if (Lv.iv_count == 0) continue;
         sweep_jobs(s, level, SW_F, Lv.iv_first, Lv.iv_first + Lv.iv_count, tail, 0,
-                   tail == TAIL_SQ ? d_sq_c_ : nullptr, 0, store);
+                   (tail == TAIL_SQ || tail == TAIL_BOTH) ? d_sq_c_ : nullptr, 0, store);
     }
     if (tag) phase_end();
 }
@@ -1304,10 +1307,21 @@ void Engine::v_cycle(int level) {
     phase_end();
 }
 
+// Relax reuse (opt-in, atm_runtime.reuse_relax): with F-relaxation in the
+// two-level cycle, a cycle's opening F-sweep recomputes from the same C
+// points exactly what the previous cycle's correction F-sweep computed, and
+// its only consumed output is the restriction residual at the C points.  The
+// correction sweep then also stores those residuals (TAIL_BOTH) and the next
+// cycle skips its F-sweep -- bitwise the same cycle.
+bool Engine::reuse_possible() const {
+    return rt_.reuse_relax && sol_.mode == ATM_TWO_LEVEL && sol_.relaxation == ATM_RELAX_F;
+}
+
 void Engine::two_level_cycle() {
     // solver.cpp:305-320
+    const bool reuse = reuse_possible();
     phase_begin("relax");
-    relax_level(0, sol_.relaxation == ATM_RELAX_F, true);
+    if (!(reuse && relax_valid_)) relax_level(0, sol_.relaxation == ATM_RELAX_F, true);
     phase_end();
     phase_begin("restrict");
     if (sol_.relaxation != ATM_RELAX_F) resid_c(0);
@@ -1315,9 +1329,10 @@ void Engine::two_level_cycle() {
     phase_end();
     coarsest_linear();
     phase_begin("correct");
-    f_sweep(0, TAIL_SQ);
+    f_sweep(0, reuse ? TAIL_BOTH : TAIL_SQ);
     for (Shard& s : sh_) point0_residual(s, 0, d_row_, d_sq_c_);
     phase_end();
+    relax_valid_ = reuse;
 }
 
 // One cycle = a fixed launch sequence on one stream: captured once into a
@@ -1332,7 +1347,9 @@ bool Engine::use_graphs() const {
 void Engine::cycle() {
     setup();
     launches_ = 0;
-    const bool graphs = use_graphs();
+    // with relax reuse the first cycle (which still runs the opening F-sweep)
+    // is not the steady-state launch sequence: capture from the second on
+    const bool graphs = use_graphs() && (!reuse_possible() || relax_valid_);
     if (graphs && graph_exec_) {
         CK(cudaGraphLaunch(graph_exec_, st_));
         last_launches_ = graph_launches_;
@@ -1386,6 +1403,7 @@ void Engine::check_newton() {
 void Engine::nested_init() {
     // solver.cpp:331-368
     setup();
+    relax_valid_ = false;
     const int lc = H_.coarsest();
     for (int l = 0; l < lc; ++l) {
         const int m = H_.m[l];
@@ -1546,9 +1564,11 @@ int Engine::solve(atm_report* rep, double* norms) {
         if (norms) norms[it - 1] = v;
         r.iterations = it;
         // relaxation Phi applications: every F-point twice per level visit
+        // (once when the opening F-sweep is reused)
+        const bool reused = reuse_possible() && it > 1;
         for (int l = 0; l + 1 < H_.L; ++l) {
             const double F = static_cast<double>(H_.np[l] - H_.n_c(l));
-            double per = 2.0 * F;
+            double per = reused ? F : 2.0 * F;
             if (sol_.relaxation == ATM_RELAX_FCF) per += sol_.nu * (F + H_.n_c(l) - 1);
             dof_steps += per * n_;
         }
@@ -1581,7 +1601,10 @@ int Engine::solve(atm_report* rep, double* norms) {
 void Engine::xfer_level(int level, int which, int first, int count, double* host, bool to_host) {
     if (level < 0 || level >= H_.L) config_error("level out of range");
     if (count < 0 || first < 0 || first + count > H_.np[level]) config_error("point range out of range");
-    if (!to_host) setup();
+    if (!to_host) {
+        setup();
+        relax_valid_ = false;
+    }
     CK(cudaStreamSynchronize(st_));
     // one process sees every shard (world 1): every row is written below;
     // with one shard per process, points this process does not own read as 0
@@ -1651,6 +1674,7 @@ void Engine::apply_phi(int level, int first, int count, const double* in, double
 }
 
 void Engine::kernel_f_relax(int level, int first_iv, int count) {
+    relax_valid_ = false;
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
     sweep_jobs(sh_[0], level, SW_F, first_iv, first_iv + count, TAIL_NONE, 0, nullptr, 0);
@@ -1659,6 +1683,7 @@ void Engine::kernel_f_relax(int level, int first_iv, int count) {
 }
 
 void Engine::kernel_c_relax(int level, int first_c, int count) {
+    relax_valid_ = false;
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
     sweep_jobs(sh_[0], level, SW_CRELAX, std::max(1, first_c), first_c + count, TAIL_NONE, 0,

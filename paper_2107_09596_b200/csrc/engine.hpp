@@ -230,6 +230,8 @@ private:
     int launches_ = 0, last_launches_ = 0;
     // CUDA graph of one cycle (captured on the first cycle, then replayed)
     bool use_graphs() const;
+    bool reuse_possible() const;
+    bool relax_valid_ = false;  // level-1 r holds the residuals of the current C points
     cudaGraphExec_t graph_exec_ = nullptr;
     int graph_launches_ = 0;
     double last_sweep_ms_ = 0.0;

@@ -599,14 +599,15 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kerne
             cg_phi_any<E>(a.co, cx, xb, rb, band, a.forced);
             const double* g = a.add_g ? crow(a.g, ti, a.g_base) : nullptr;
             const double* uc = crow(a.u, ti, a.u_base);
-            if (a.tail == TAIL_STORE) {
+            if (a.tail == TAIL_STORE || a.tail == TAIL_BOTH) {
                 double* dst = row(a.out, ti / m, a.out_base);
                 for_own(cx, [&](int idx, int) {
                     double v = xb[idx];
                     if (g) v += g[idx];
                     dst[idx] = v - uc[idx];
                 });
-            } else {
+            }
+            if (a.tail == TAIL_SQ || a.tail == TAIL_BOTH) {
                 double s2[1] = {0.0};
                 for_own(cx, [&](int idx, int) {
                     double v = xb[idx];

@@ -74,7 +74,9 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double r, double shift, i
 
 // Job kinds of the sweep kernel (one job per C-point index J of a level).
 enum SweepKind { SW_F = 0, SW_FCF = 1, SW_CRELAX = 2, SW_RESID = 3 };
-enum TailKind { TAIL_NONE = 0, TAIL_STORE = 1, TAIL_SQ = 2 };
+// TAIL_BOTH: the residual row is stored (next cycle's restriction input)
+// and its square sum written (this cycle's stopping norm)
+enum TailKind { TAIL_NONE = 0, TAIL_STORE = 1, TAIL_SQ = 2, TAIL_BOTH = 3 };
 enum StoreKind { STORE_NONE = 0, STORE_ALL = 1, STORE_CF = 2 };
 __host__ __device__ inline bool store_row(int mode, int i, int m) {
     return mode == STORE_ALL || (mode == STORE_CF && (i % m == 0 || (i + 1) % m == 0));

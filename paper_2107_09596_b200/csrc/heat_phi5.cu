@@ -965,9 +965,9 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             phS ^= 1;
             row_acc<L>(bufS, x, ln, true);
             if (a.kind == SW_F && J + 1 < je) seed_ready = true;  // S holds u[c_{J+1}]
-            if (a.tail == TAIL_STORE) {
+            if (a.tail == TAIL_STORE || a.tail == TAIL_BOTH)
                 stage_out(tail_i / m - a.out_base, &tm_out, &tm_outw);
-            } else {
+            if (a.tail == TAIL_SQ || a.tail == TAIL_BOTH) {
                 const double tot = cta_sum_squares<L>(x, ln, sl);
                 if (t == 0) a.sq[tail_i - a.sq_base] = tot;
             }

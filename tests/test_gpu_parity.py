@@ -337,3 +337,36 @@ def test_cuda_graph_replay_bitwise_equals_direct_launches(monkeypatch):
     assert a.report.iterations == b.report.iterations
     assert np.array_equal(np.array(a.report.residual_norms), np.array(b.report.residual_norms))
     assert np.array_equal(a.state, b.state)
+
+
+@pytest.mark.parametrize("workers", [1, 3])
+def test_relax_reuse_bitwise_equals_full_cycles(workers):
+    # opt-in reuse of the correction sweep's C-point residuals as the next
+    # cycle's restriction input: bitwise the same histories and states
+    args = dict(problem="heat1d", n=1025, tf=1.0, n_points=2049, m=16, k=4, manufactured=1,
+                guess="random", seed=21, max_iters=80, tol=1e-10)
+    app, hier, cfg = device_objects(args)
+    a = T.solve(app, hier, cfg, workers=workers)
+    b = T.solve(app, hier, cfg, workers=workers, reuse_relax=True)
+    assert a.report.iterations == b.report.iterations
+    assert np.array_equal(np.array(a.report.residual_norms), np.array(b.report.residual_norms))
+    assert np.array_equal(a.state, b.state)
+    # reused cycles count one F-sweep of Phi applications, not two
+    assert b.report.dof_steps < a.report.dof_steps
+
+
+def test_relax_reuse_invalidated_by_set_level():
+    args = dict(problem="heat1d", n=63, tf=1.0, n_points=257, m=8, k=3, manufactured=0,
+                guess="random", seed=4, max_iters=20, tol=1e-14)
+    app, hier, cfg = device_objects(args)
+    drv_a = T.CycleDriver(app, hier, cfg)
+    drv_b = T.CycleDriver(app, hier, cfg, reuse_relax=True)
+    for d in (drv_a, drv_b):
+        d.setup()
+        d.iterate(2)
+        u = d.get_level(0)
+        u[5:40] *= 0.5  # perturb F and C points between cycles
+        d.set_level(0, u)
+    na, nb = drv_a.iterate(3), drv_b.iterate(3)
+    assert np.array_equal(na, nb)
+    assert np.array_equal(drv_a.get_level(0), drv_b.get_level(0))
