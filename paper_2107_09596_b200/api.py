@@ -487,7 +487,8 @@ class CycleDriver:
 
     def __init__(self, app: Application, hier: Hierarchy, cfg: SolverConfig, workers: int = 1,
                  device: int = 0, trace: bool = False, world_size: int = 1, rank: int = 0,
-                 nccl_id: Optional[bytes] = None, reuse_relax: bool = False):
+                 nccl_id: Optional[bytes] = None, reuse_relax: bool = False,
+                 cpoint_storage: bool = False):
         self.app, self.hier, self.cfg = app, hier, cfg
         self._keep = []
         p = app.c_problem(self._keep)
@@ -509,6 +510,7 @@ class CycleDriver:
         rt.device, rt.n_shards, rt.world_size, rt.rank = device, workers, world_size, rank
         rt.trace = int(trace)
         rt.reuse_relax = int(reuse_relax)
+        rt.storage = int(bool(cpoint_storage))  # ATM_STORE_CPOINTS
         if nccl_id is not None:
             self._nid = C.create_string_buffer(bytes(nccl_id), 128)
             rt.nccl_id = C.cast(self._nid, C.c_void_p)

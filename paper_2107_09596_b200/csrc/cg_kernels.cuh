@@ -48,6 +48,7 @@ struct CgSweepArgs {
     int forced, store, tail;
     double* out; int out_base;
     double* sq; int sq_base;
+    int u_div;  // > 1: C-point-only u array
 };
 
 struct CgWindowArgs {

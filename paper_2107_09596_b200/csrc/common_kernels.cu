@@ -19,26 +19,29 @@ __device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-__global__ void fill_random_kernel(double* u, int base, int pitch, int n, int i0, int i1,
-                                   uint64_t seed) {
-    const long long total = static_cast<long long>(i1 - i0) * n;
+__global__ void fill_random_kernel(double* u, int base, int pitch, int n, int i0, int rows,
+                                   int step, uint64_t seed) {
+    const long long total = static_cast<long long>(rows) * n;
     for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
          idx < total; idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int i = i0 + static_cast<int>(idx / n);
+        const int r = static_cast<int>(idx / n);
+        const int i = i0 + r * step;
         const int q = static_cast<int>(idx % n);
         const uint64_t st = (seed + static_cast<uint64_t>(i)) +
                             static_cast<uint64_t>(q + 1) * 0x9E3779B97F4A7C15ULL;
         const double unit = static_cast<double>(sm64_mix(st) >> 11) * 0x1.0p-53;
-        u[static_cast<size_t>(i - base) * pitch + q] = 2.0 * unit - 1.0;
+        u[static_cast<size_t>((i - base) / step) * pitch + q] = 2.0 * unit - 1.0;
     }
 }
 
+// rows i = i0, i0 + step, ... < i1 (step > 1: C-point-only arrays, row (i - base) / step)
 int launch_fill_random(double* u, int base, int pitch, int n, int i0, int i1, uint64_t seed,
-                       cudaStream_t s) {
+                       cudaStream_t s, int step) {
     if (i1 <= i0) return 0;
-    const long long total = static_cast<long long>(i1 - i0) * n;
+    const int rows = (i1 - i0 + step - 1) / step;
+    const long long total = static_cast<long long>(rows) * n;
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 16));
-    fill_random_kernel<<<blocks, 256, 0, s>>>(u, base, pitch, n, i0, i1, seed);
+    fill_random_kernel<<<blocks, 256, 0, s>>>(u, base, pitch, n, i0, rows, step, seed);
     return static_cast<int>(cudaGetLastError());
 }
 
@@ -237,7 +240,8 @@ __global__ void scalar_sweep_kernel(ScalarSweepArgs a) {
         default: start = c; end = min(c + m - 1, last); store_from = c + 1; break;
     }
     if (end < start) end = start;
-    double x = a.u[start - a.u_base];
+    const int ud = a.u_div > 1 ? a.u_div : 1;
+    double x = a.u[(start - a.u_base) / ud];
     for (int i = start + 1; i <= end; ++i) {
         x = sc_phi(a.co, i, x);
         if (a.add_g) x += a.g[i - a.g_base];
@@ -247,7 +251,7 @@ __global__ void scalar_sweep_kernel(ScalarSweepArgs a) {
         const int ti = end + 1;
         double r = sc_phi(a.co, ti, x);
         if (a.add_g) r += a.g[ti - a.g_base];
-        r -= a.u[ti - a.u_base];
+        r -= a.u[(ti - a.u_base) / ud];
         const int ci = ti / m;
         if (a.tail == TAIL_STORE || a.tail == TAIL_BOTH) a.out[ci - a.out_base] = r;
         if (a.tail == TAIL_SQ || a.tail == TAIL_BOTH) a.sq[ti - a.sq_base] = r * r;

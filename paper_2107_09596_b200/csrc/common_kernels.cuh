@@ -23,6 +23,7 @@ struct ScalarSweepArgs {
     int store, tail;
     double* out; int out_base;
     double* sq; int sq_base;
+    int u_div;  // > 1: C-point-only u array
 };
 
 struct ScalarWindowArgs {
@@ -42,7 +43,7 @@ int launch_scalar_window(const ScalarWindowArgs& a, cudaStream_t s);
 // u[row i][q] = random_state(seed + i, n)[q] for i in [i0, i1) (i >= 1),
 // bitwise equal to state_vector.hpp:108-118.
 int launch_fill_random(double* u, int base, int pitch, int n, int i0, int i1, uint64_t seed,
-                       cudaStream_t s);
+                       cudaStream_t s, int step = 1);
 // rows [i0,i1) := v (n values, device)
 int launch_fill_rows(double* u, int base, int pitch, int n, int i0, int i1, const double* v,
                      cudaStream_t s);

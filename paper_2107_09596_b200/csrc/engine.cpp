@@ -336,6 +336,21 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
         config_error("functional-change stopping norm needs a functional");
     if (s.initial_guess == ATM_GUESS_PROVIDED && !s.provided)
         config_error("provided initial guess has the wrong number of points");
+    // C-point storage (atm_storage): level 0 keeps only its
+    // C points; F values are the F-relaxation of their interval's C point
+    // (recomputed on read).  Every level-0 F row must then be a pure function
+    // of the C rows: F-relaxation only, and no stored level-0 forcing.
+    if (rt.storage != ATM_STORE_FULL && rt.storage != ATM_STORE_CPOINTS)
+        config_error("runtime: unknown storage mode");
+    if (rt.storage == ATM_STORE_CPOINTS) {
+        if (H_.L < 2) config_error("C-point storage needs at least two levels");
+        if (s.relaxation != ATM_RELAX_F) config_error("C-point storage needs F-relaxation");
+        const bool g0_full = !folded_ && ((heat_ && !ac_ && p.manufactured) ||
+                                          (h2d_ && !gs_ && p.source) ||
+                                          (kind_ == ATM_PHI_SCALAR && p.fine_forcing && p.n_ff > 0));
+        if (g0_full) config_error("C-point storage needs the forcing folded into Phi");
+        cpts_ = true;
+    }
 
     pitch_ = (heat_ || h2d_) ? ((n_ + 15) / 16) * 16 : 1;
     // L = 32 row kernels (pitch > 2048): a thread's chunk must not straddle
@@ -525,7 +540,14 @@ void Engine::alloc_shard(Shard& s) {
         if (l == lc && l >= 1) base = std::min(base, std::max(0, Lv.lo - H_.k + 1));
         Lv.base = base;
         const int rows = Lv.hi - base + 1;
-        Lv.u = alloc_arr(Lv, base, rows, true, Lvl_.empty() ? 0 : Lvl_[l]);
+        if (l == 0 && cpts_) {
+            // base (0 or the left shard's last point) is a C point
+            const int m0 = H_.m[0];
+            Lv.u = alloc_arr(Lv, base, Lv.hi / m0 - base / m0 + 1, true, Lvl_.empty() ? 0 : Lvl_[l]);
+            Lv.u.div = m0;
+        } else {
+            Lv.u = alloc_arr(Lv, base, rows, true, Lvl_.empty() ? 0 : Lvl_[l]);
+        }
         // g: full per-point array where forcing is stored, else point 0 only
         bool g_full = false;
         if (l == 0 && !folded_) {
@@ -762,6 +784,7 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.j0 = j0;
         a.j1 = j1;
         a.u_base = Lv.u.base;
+        a.u_div = Lv.u.div;
         a.g_base = add_g ? Lv.g.base : 0;
         a.add_g = add_g;
         a.forced = phi_forced_;
@@ -790,6 +813,7 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.j1 = j1;
         a.u = Lv.u.p;
         a.u_base = Lv.u.base;
+        a.u_div = Lv.u.div;
         a.g = add_g ? Lv.g.p : nullptr;
         a.g_base = add_g ? Lv.g.base : 0;
         a.add_g = add_g;
@@ -811,6 +835,7 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.j1 = j1;
         a.u = Lv.u.p;
         a.u_base = Lv.u.base;
+        a.u_div = Lv.u.div;
         a.g = add_g ? Lv.g.p : nullptr;
         a.g_base = add_g ? Lv.g.base : 0;
         a.add_g = add_g;
@@ -925,8 +950,8 @@ void Engine::halo(int level, DArr LevelDev::*arr) {
             const DArr& src = sh_[Lv.left].lv[level].*arr;
             const DArr& dst = Lv.*arr;
             const int i = Lv.lo - 1;
-            CK(cudaMemcpyAsync(dst.p + static_cast<size_t>(i - dst.base) * pitch_,
-                               src.p + static_cast<size_t>(i - src.base) * pitch_, bytes,
+            CK(cudaMemcpyAsync(dst.p + dst.off(i, pitch_),
+                               src.p + src.off(i, pitch_), bytes,
                                cudaMemcpyDeviceToDevice, st_));
         }
         return;
@@ -938,10 +963,10 @@ void Engine::halo(int level, DArr LevelDev::*arr) {
     ncclComm_t c = static_cast<ncclComm_t>(comm_);
     nccl_->check(nccl_->GroupStart(), "group");
     if (Lv.right >= 0)
-        nccl_->check(nccl_->Send(a.p + static_cast<size_t>(Lv.hi - a.base) * pitch_, pitch_,
+        nccl_->check(nccl_->Send(a.p + a.off(Lv.hi, pitch_), pitch_,
                                  ncclFloat64, Lv.right, c, st_), "send halo");
     if (Lv.lo > 0 && Lv.left >= 0)
-        nccl_->check(nccl_->Recv(a.p + static_cast<size_t>(Lv.lo - 1 - a.base) * pitch_, pitch_,
+        nccl_->check(nccl_->Recv(a.p + a.off(Lv.lo - 1, pitch_), pitch_,
                                  ncclFloat64, Lv.left, c, st_), "recv halo");
     nccl_->check(nccl_->GroupEnd(), "group");
 }
@@ -961,8 +986,8 @@ void Engine::window_exchange(int level, DArr LevelDev::*arr) {
                 const int o = lay_.owner_of_coarse(j);
                 const DArr& src = sh_[o].lv[level].*arr;
                 const DArr& dst = Lv.*arr;
-                CK(cudaMemcpyAsync(dst.p + static_cast<size_t>(j - dst.base) * pitch_,
-                                   src.p + static_cast<size_t>(j - src.base) * pitch_, rowb,
+                CK(cudaMemcpyAsync(dst.p + dst.off(j, pitch_),
+                                   src.p + src.off(j, pitch_), rowb,
                                    cudaMemcpyDeviceToDevice, st_));
             }
         }
@@ -981,14 +1006,14 @@ void Engine::window_exchange(int level, DArr LevelDev::*arr) {
         const int q_need_lo = std::max(0, q_lo - k + 1), q_need_hi = q_lo - 1;
         const int a0 = std::max(q_need_lo, Lv.lo), a1 = std::min(q_need_hi, Lv.hi);
         if (a1 >= a0 && Lv.hi >= Lv.lo)
-            nccl_->check(nccl_->Send(a.p + static_cast<size_t>(a0 - a.base) * pitch_,
+            nccl_->check(nccl_->Send(a.p + a.off(a0, pitch_),
                                      static_cast<size_t>(a1 - a0 + 1) * pitch_, ncclFloat64, q, c,
                                      st_), "send window");
         // what I need from q
         const int my_need_lo = std::max(0, Lv.lo - k + 1), my_need_hi = Lv.lo - 1;
         const int b0 = std::max(my_need_lo, rq.lo[level]), b1 = std::min(my_need_hi, rq.hi[level]);
         if (b1 >= b0 && Lv.hi >= Lv.lo)
-            nccl_->check(nccl_->Recv(a.p + static_cast<size_t>(b0 - a.base) * pitch_,
+            nccl_->check(nccl_->Recv(a.p + a.off(b0, pitch_),
                                      static_cast<size_t>(b1 - b0 + 1) * pitch_, ncclFloat64, q, c,
                                      st_), "recv window");
     }
@@ -1020,7 +1045,10 @@ void Engine::fill_initial_guess() {
     for (Shard& s : sh_) {
         LevelDev& Lv = s.lv[0];
         if (Lv.hi < Lv.lo) continue;
-        const int i0 = std::max(1, Lv.lo), i1 = Lv.hi + 1;
+        const int dv = Lv.u.div;
+        // C-point storage: the held points i0, i0 + dv, ... < i1
+        const int i0 = (std::max(1, Lv.lo) + dv - 1) / dv * dv, i1 = Lv.hi + 1;
+        const int nrows = i1 > i0 ? (i1 - i0 + dv - 1) / dv : 0;
         if (Lv.lo == 0)
             check_launch(launch_fill_rows(Lv.u.p, Lv.u.base, pitch_, n_, 0, 1, d_ic_, st_), "fill ic");
         switch (sol_.initial_guess) {
@@ -1033,18 +1061,20 @@ void Engine::fill_initial_guess() {
                     CK(cudaMemcpy(p, cval_.data(), sizeof(double) * n_, cudaMemcpyHostToDevice));
                     v = static_cast<double*>(p);
                 }
-                check_launch(launch_fill_rows(Lv.u.p, Lv.u.base, pitch_, n_, i0, i1, v, st_), "fill const");
+                if (nrows > 0)
+                    check_launch(launch_fill_rows(Lv.u.p + Lv.u.off(i0, pitch_), 0, pitch_, n_, 0, nrows,
+                                                  v, st_), "fill const");
                 break;
             }
             case ATM_GUESS_RANDOM:
-                check_launch(launch_fill_random(Lv.u.p, Lv.u.base, pitch_, n_, i0, i1, sol_.seed, st_),
+                check_launch(launch_fill_random(Lv.u.p, Lv.u.base, pitch_, n_, i0, i1, sol_.seed, st_, dv),
                              "fill random");
                 break;
             case ATM_GUESS_PROVIDED:
-                if (i1 > i0)
-                    CK(cudaMemcpy2DAsync(Lv.u.p + static_cast<size_t>(i0 - Lv.u.base) * pitch_,
+                if (nrows > 0)
+                    CK(cudaMemcpy2DAsync(Lv.u.p + Lv.u.off(i0, pitch_),
                                          sizeof(double) * pitch_, prov_ptr_ + static_cast<size_t>(i0) * n_,
-                                         sizeof(double) * n_, sizeof(double) * n_, i1 - i0,
+                                         sizeof(double) * n_ * dv, sizeof(double) * n_, nrows,
                                          cudaMemcpyHostToDevice, st_));
                 break;
         }
@@ -1062,7 +1092,7 @@ void Engine::fill_level_rhs(int level) {
         const int i0 = std::max(1, Lv.lo), i1 = Lv.hi;
         if (folded_) {
             if (i1 >= i0)
-                CK(cudaMemsetAsync(Lv.g.p + static_cast<size_t>(i0 - Lv.g.base) * pitch_, 0,
+                CK(cudaMemsetAsync(Lv.g.p + Lv.g.off(i0, pitch_), 0,
                                    sizeof(double) * pitch_ * (i1 - i0 + 1), st_));
         } else if (heat_) {
             // forcing(level, i) = propagate(zero, with forcing) (heat1d.cpp:97-100)
@@ -1074,7 +1104,7 @@ void Engine::fill_level_rhs(int level) {
                 window_launch(s, level, WK_APPLY, 0, 0, -1, i0, i0, Lv.g, Lv.g, Lv.g, Lv.g, 1, 1, 1, 0, 0);
                 if (i1 > i0)
                     check_launch(launch_fill_rows(Lv.g.p, Lv.g.base, pitch_, n_, i0 + 1, i1 + 1,
-                                                  Lv.g.p + static_cast<size_t>(i0 - Lv.g.base) * pitch_,
+                                                  Lv.g.p + Lv.g.off(i0, pitch_),
                                                   st_), "g rows");
             }
         } else {
@@ -1099,7 +1129,8 @@ void Engine::setup() {
         for (Shard& s : sh_) {
             LevelDev& Lv = s.lv[0];
             if (Lv.c_count > 0)
-                check_launch(launch_functional_init(Lv.u.p, Lv.u.base, H_.m[0], pitch_, n_, d_fw_,
+                check_launch(launch_functional_init(Lv.u.p, Lv.u.base / Lv.u.div, H_.m[0] / Lv.u.div,
+                                                    pitch_, n_, d_fw_,
                                                     d_prevf_, Lv.c_first, Lv.c_first + Lv.c_count, st_),
                              "functional init");
         }
@@ -1122,6 +1153,12 @@ void Engine::point0_residual(Shard& s, int level, double* r_out, double* sq_out)
 
 // F-relaxation over own intervals (kernels.cpp:7-17) with optional tail
 void Engine::f_sweep(int level, int tail, int store) {
+    if (level == 0 && cpts_) {
+        // C-point storage: level-0 F rows are never stored, so a sweep
+        // without a tail has no observable result
+        if (tail == TAIL_NONE) return;
+        store = STORE_NONE;
+    }
     halo(level, &LevelDev::u);
     const char* tag = level != 0 ? nullptr
                       : (tail == TAIL_SQ || tail == TAIL_BOTH) ? "sweep_correct"
@@ -1204,13 +1241,13 @@ void Engine::restrict_to(int level) {
         const int j0 = F.c_first, cnt = F.c_count;
         // injection: coarse u = coarse v = fine u at C-points (kernels.cpp:45-51)
         const size_t rowb = sizeof(double) * pitch_;
-        const double* src = F.u.p + static_cast<size_t>(j0 * m - F.u.base) * pitch_;
+        const double* src = F.u.p + F.u.off(j0 * m, pitch_);
         for (DArr* dst : {&C.u, &C.v})
-            CK(cudaMemcpy2DAsync(dst->p + static_cast<size_t>(j0 - dst->base) * pitch_, rowb, src,
-                                 rowb * m, rowb, cnt, cudaMemcpyDeviceToDevice, st_));
+            CK(cudaMemcpy2DAsync(dst->p + dst->off(j0, pitch_), rowb, src,
+                                 rowb * (m / F.u.div), rowb, cnt, cudaMemcpyDeviceToDevice, st_));
         if (j0 > 0 && C.v.valid(j0 - 1) && F.u.valid((j0 - 1) * m))
-            CK(cudaMemcpyAsync(C.v.p + static_cast<size_t>(j0 - 1 - C.v.base) * pitch_,
-                               F.u.p + static_cast<size_t>((j0 - 1) * m - F.u.base) * pitch_, rowb,
+            CK(cudaMemcpyAsync(C.v.p + C.v.off(j0 - 1, pitch_),
+                               F.u.p + F.u.off((j0 - 1) * m, pitch_), rowb,
                                cudaMemcpyDeviceToDevice, st_));
         if (j0 == 0) point0_residual(s, level, C.r.p, nullptr);
         if (relaxed) {
@@ -1238,9 +1275,12 @@ void Engine::windows(int kind) {
         const int p0 = std::max(plo, k), p1 = phi;
         const int forced = phi_forced_;
         if (kind == WK_LINEAR) {
-            LevelDev& F = s.lv[0];
-            window_launch(s, lc, WK_LINEAR, 0, pre_e0, pre_e1, p0, p1, C.r, C.r, C.r, F.u, H_.m[0],
-                          forced, 0, 0, 0);
+            // the corrections land on level-0 C rows: row p * m - base, or
+            // p - base / m with C-point storage
+            DArr out = s.lv[0].u;
+            out.base /= out.div;
+            window_launch(s, lc, WK_LINEAR, 0, pre_e0, pre_e1, p0, p1, C.r, C.r, C.r, out,
+                          H_.m[0] / s.lv[0].u.div, forced, 0, 0, 0);
         } else if (kind == WK_FAS) {
             // Psi(v_{j-1}) once per coarse point, shared by every window
             const int a0 = std::max(1, C.base + 1);
@@ -1281,8 +1321,8 @@ void Engine::correct_from(int level) {
         LevelDev& F = s.lv[level];
         LevelDev& C = s.lv[level + 1];
         if (F.c_count == 0) continue;
-        check_launch(launch_c_correct(F.u.p, F.u.base, m, C.u.p, C.v.p, C.u.base, pitch_, n_,
-                                      F.c_first, F.c_first + F.c_count, st_), "c_correct");
+        check_launch(launch_c_correct(F.u.p, F.u.base / F.u.div, m / F.u.div, C.u.p, C.v.p, C.u.base,
+                                      pitch_, n_, F.c_first, F.c_first + F.c_count, st_), "c_correct");
     }
     f_sweep(level, level == 0 ? TAIL_SQ : TAIL_NONE);
     if (level == 0)
@@ -1412,9 +1452,9 @@ void Engine::nested_init() {
             LevelDev& C = s.lv[l + 1];
             if (F.c_count == 0) continue;
             const size_t rowb = sizeof(double) * pitch_;
-            CK(cudaMemcpy2DAsync(C.u.p + static_cast<size_t>(F.c_first - C.u.base) * pitch_, rowb,
-                                 F.u.p + static_cast<size_t>(F.c_first * m - F.u.base) * pitch_,
-                                 rowb * m, rowb, F.c_count, cudaMemcpyDeviceToDevice, st_));
+            CK(cudaMemcpy2DAsync(C.u.p + C.u.off(F.c_first, pitch_), rowb,
+                                 F.u.p + F.u.off(F.c_first * m, pitch_),
+                                 rowb * (m / F.u.div), rowb, F.c_count, cudaMemcpyDeviceToDevice, st_));
         }
         fill_level_rhs(l + 1);
     }
@@ -1427,11 +1467,11 @@ void Engine::nested_init() {
             if (C.hi < C.lo) continue;
             if (world_ == 1 && C.lo > 0) {
                 const DArr& src = sh_[C.left].lv[lc].u;
-                CK(cudaMemcpyAsync(C.u.p + static_cast<size_t>(C.lo - 1 - C.u.base) * pitch_,
-                                   src.p + static_cast<size_t>(C.lo - 1 - src.base) * pitch_,
+                CK(cudaMemcpyAsync(C.u.p + C.u.off(C.lo - 1, pitch_),
+                                   src.p + src.off(C.lo - 1, pitch_),
                                    sizeof(double) * pitch_, cudaMemcpyDeviceToDevice, st_));
             } else if (world_ > 1 && C.lo > 0) {
-                nccl_->check(nccl_->Recv(C.u.p + static_cast<size_t>(C.lo - 1 - C.u.base) * pitch_,
+                nccl_->check(nccl_->Recv(C.u.p + C.u.off(C.lo - 1, pitch_),
                                          pitch_, ncclFloat64, C.left, static_cast<ncclComm_t>(comm_), st_),
                              "chain recv");
             }
@@ -1439,7 +1479,7 @@ void Engine::nested_init() {
             window_launch(s, lc, WK_FORWARD, from, std::max(1, C.lo), C.hi, 1, 0, C.u, C.u, C.u,
                           C.u, 1, forced, 0, 0, 0);
             if (world_ > 1 && C.right >= 0)
-                nccl_->check(nccl_->Send(C.u.p + static_cast<size_t>(C.hi - C.u.base) * pitch_, pitch_,
+                nccl_->check(nccl_->Send(C.u.p + C.u.off(C.hi, pitch_), pitch_,
                                          ncclFloat64, C.right, static_cast<ncclComm_t>(comm_), st_),
                              "chain send");
         }
@@ -1447,8 +1487,8 @@ void Engine::nested_init() {
         for (Shard& s : sh_) {
             LevelDev& C = s.lv[lc];
             if (C.hi < C.lo) continue;
-            CK(cudaMemcpyAsync(C.x.p + static_cast<size_t>(C.lo - C.x.base) * pitch_,
-                               C.u.p + static_cast<size_t>(C.lo - C.u.base) * pitch_,
+            CK(cudaMemcpyAsync(C.x.p + C.x.off(C.lo, pitch_),
+                               C.u.p + C.u.off(C.lo, pitch_),
                                sizeof(double) * pitch_ * (C.hi - C.lo + 1), cudaMemcpyDeviceToDevice, st_));
         }
         window_exchange(lc, &LevelDev::x);
@@ -1461,8 +1501,8 @@ void Engine::nested_init() {
             LevelDev& C = s.lv[l + 1];
             if (F.c_count == 0) continue;
             const size_t rowb = sizeof(double) * pitch_;
-            CK(cudaMemcpy2DAsync(F.u.p + static_cast<size_t>(F.c_first * m - F.u.base) * pitch_,
-                                 rowb * m, C.u.p + static_cast<size_t>(F.c_first - C.u.base) * pitch_,
+            CK(cudaMemcpy2DAsync(F.u.p + F.u.off(F.c_first * m, pitch_),
+                                 rowb * (m / F.u.div), C.u.p + C.u.off(F.c_first, pitch_),
                                  rowb, rowb, F.c_count, cudaMemcpyDeviceToDevice, st_));
         }
         f_sweep(l, TAIL_NONE);
@@ -1480,7 +1520,15 @@ double Engine::residual_norm() {
     for (Shard& s : sh_) {
         LevelDev& Lv = s.lv[0];
         if (Lv.hi < Lv.lo) continue;
-        sweep_jobs(s, 0, SW_RESID, std::max(1, Lv.lo), Lv.hi + 1, TAIL_SQ, 1, d_sq_full_, 0);
+        if (cpts_) {
+            // held F values are by definition the F-relaxation of their C
+            // point (zero residual): only the C-point residuals remain
+            if (Lv.iv_count > 0)
+                sweep_jobs(s, 0, SW_F, Lv.iv_first, Lv.iv_first + Lv.iv_count, TAIL_SQ, 0, d_sq_full_, 0,
+                           STORE_NONE);
+        } else {
+            sweep_jobs(s, 0, SW_RESID, std::max(1, Lv.lo), Lv.hi + 1, TAIL_SQ, 1, d_sq_full_, 0);
+        }
         point0_residual(s, 0, d_row_, d_sq_full_);
     }
     const double v = reduce_norm(d_sq_full_, H_.np[0]);
@@ -1493,7 +1541,8 @@ double Engine::functional_change() {
     for (size_t i = 0; i < sh_.size(); ++i) {
         LevelDev& Lv = sh_[i].lv[0];
         if (Lv.c_count == 0) continue;
-        check_launch(launch_functional_change(Lv.u.p, Lv.u.base, H_.m[0], pitch_, n_, d_fw_,
+        check_launch(launch_functional_change(Lv.u.p, Lv.u.base / Lv.u.div, H_.m[0] / Lv.u.div,
+                                              pitch_, n_, d_fw_,
                                               d_prevf_, Lv.c_first, Lv.c_first + Lv.c_count,
                                               d_fmax_ + i, st_), "functional");
     }
@@ -1606,6 +1655,10 @@ void Engine::xfer_level(int level, int which, int first, int count, double* host
         relax_valid_ = false;
     }
     CK(cudaStreamSynchronize(st_));
+    if (to_host && level == 0 && which == 0 && cpts_) {
+        get_level0_cpts(first, count, host);
+        return;
+    }
     // one process sees every shard (world 1): every row is written below;
     // with one shard per process, points this process does not own read as 0
     if (to_host && world_ > 1) std::fill(host, host + static_cast<size_t>(count) * n_, 0.0);
@@ -1613,22 +1666,69 @@ void Engine::xfer_level(int level, int which, int first, int count, double* host
         LevelDev& Lv = s.lv[level];
         DArr* a = which == 0 ? &Lv.u : which == 1 ? &Lv.g : which == 2 ? &Lv.v : &Lv.r;
         if (!a->p) continue;
-        // owned points (plus, for writes, any allocated row such as halos)
+        // owned points (plus, for writes, any allocated row such as halos);
+        // with C-point storage (div > 1) writes reach only the held C points
+        const int dv = a->div, top = a->base + (a->rows - 1) * dv;
         int lo = to_host ? std::max(Lv.lo, a->base) : a->base;
-        int hi = to_host ? std::min(Lv.hi, a->base + a->rows - 1) : a->base + a->rows - 1;
+        int hi = to_host ? std::min(Lv.hi, top) : top;
         lo = std::max(lo, first);
         hi = std::min(hi, first + count - 1);
         if (hi < lo) continue;
+        lo = a->base + (lo - a->base + dv - 1) / dv * dv;
+        hi = a->base + (hi - a->base) / dv * dv;
+        if (hi < lo) continue;
+        const int nrow = (hi - lo) / dv + 1;
         double* h = host + static_cast<size_t>(lo - first) * n_;
-        double* d = a->p + static_cast<size_t>(lo - a->base) * pitch_;
+        double* d = a->p + a->off(lo, pitch_);
         if (to_host)
-            CK(cudaMemcpy2DAsync(h, sizeof(double) * n_, d, sizeof(double) * pitch_,
-                                 sizeof(double) * n_, hi - lo + 1, cudaMemcpyDeviceToHost, st_));
+            CK(cudaMemcpy2DAsync(h, sizeof(double) * n_ * dv, d, sizeof(double) * pitch_,
+                                 sizeof(double) * n_, nrow, cudaMemcpyDeviceToHost, st_));
         else
-            CK(cudaMemcpy2DAsync(d, sizeof(double) * pitch_, h, sizeof(double) * n_,
-                                 sizeof(double) * n_, hi - lo + 1, cudaMemcpyHostToDevice, st_));
+            CK(cudaMemcpy2DAsync(d, sizeof(double) * pitch_, h, sizeof(double) * n_ * dv,
+                                 sizeof(double) * n_, nrow, cudaMemcpyHostToDevice, st_));
     }
     CK(cudaStreamSynchronize(st_));
+}
+
+// Level-0 u with C-point storage: the requested points are rebuilt chunk by
+// chunk of whole intervals -- the held C rows copied into a full-row scratch
+// block whose F rows an F-sweep (STORE_ALL) recomputes -- then copied out.
+// Scratch is bounded (~1 GiB), so any N_t can be read back.
+void Engine::get_level0_cpts(int first, int count, double* out) {
+    const int m = H_.m[0], last = H_.np[0] - 1;
+    const size_t rowb = sizeof(double) * pitch_;
+    if (world_ > 1) std::fill(out, out + static_cast<size_t>(count) * n_, 0.0);
+    const int ivc = static_cast<int>(std::max<size_t>(1, (size_t(1) << 30) / (rowb * m)));
+    for (Shard& s : sh_) {
+        LevelDev& Lv = s.lv[0];
+        const int lo = std::max(Lv.lo, first), hi = std::min(Lv.hi, first + count - 1);
+        if (hi < lo) continue;
+        const int nJ = hi / m - lo / m + 1;
+        LevelDev tmp;
+        DArr T = alloc_arr(tmp, 0, std::min(nJ, ivc) * m + 1, true, Lvl_[0]);
+        for (int J0 = lo / m; J0 * m <= hi; J0 += ivc) {
+            const int J1 = std::min(hi / m + 1, J0 + ivc);  // intervals [J0, J1)
+            const int cb = J0 * m, ce = std::min(last, J1 * m - 1);
+            T.base = cb;
+            CK(cudaMemcpy2DAsync(T.p, rowb * m, Lv.u.p + Lv.u.off(cb, pitch_), rowb, rowb, J1 - J0,
+                                 cudaMemcpyDeviceToDevice, st_));
+            std::swap(Lv.u, T);
+            try {
+                sweep_jobs(s, 0, SW_F, J0, J1, TAIL_NONE, 0, nullptr, 0, STORE_ALL);
+            } catch (...) {
+                std::swap(Lv.u, T);
+                throw;
+            }
+            std::swap(Lv.u, T);
+            const int r0 = std::max(lo, cb), r1 = std::min(hi, ce);
+            CK(cudaMemcpy2DAsync(out + static_cast<size_t>(r0 - first) * n_, sizeof(double) * n_,
+                                 T.p + T.off(r0, pitch_), rowb, sizeof(double) * n_, r1 - r0 + 1,
+                                 cudaMemcpyDeviceToHost, st_));
+        }
+        CK(cudaStreamSynchronize(st_));
+        for (void* p : tmp.allocs) cudaFree(p);
+    }
+    check_newton();
 }
 
 void Engine::get_level(int level, int which, int first, int count, double* out) {
@@ -1674,6 +1774,8 @@ void Engine::apply_phi(int level, int first, int count, const double* in, double
 }
 
 void Engine::kernel_f_relax(int level, int first_iv, int count) {
+    if (level == 0 && cpts_)
+        config_error("kernel-level entry points need full level-0 storage");
     relax_valid_ = false;
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
@@ -1683,6 +1785,8 @@ void Engine::kernel_f_relax(int level, int first_iv, int count) {
 }
 
 void Engine::kernel_c_relax(int level, int first_c, int count) {
+    if (level == 0 && cpts_)
+        config_error("kernel-level entry points need full level-0 storage");
     relax_valid_ = false;
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
@@ -1693,6 +1797,8 @@ void Engine::kernel_c_relax(int level, int first_c, int count) {
 }
 
 void Engine::kernel_residual(int level, int first, int count, double* out) {
+    if (level == 0 && cpts_)
+        config_error("kernel-level entry points need full level-0 storage");
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
     Shard& s = sh_[0];

@@ -81,7 +81,14 @@ struct DArr {
     CUtensorMap tm{};   // one point row per box
     CUtensorMap tmw{};  // one warp slice of a row per box (per-warp stores)
     bool has_tm = false;
-    bool valid(int i) const { return p && i >= base && i < base + rows; }
+    int div = 1;        // > 1: only every div-th point is held (C-point storage)
+    bool valid(int i) const {
+        return p && i >= base && (i - base) % div == 0 && (i - base) / div < rows;
+    }
+    // element offset of point i's row
+    size_t off(int i, int pitch) const {
+        return static_cast<size_t>((i - base) / div) * static_cast<size_t>(pitch);
+    }
 };
 
 struct LevelDev {
@@ -186,6 +193,8 @@ private:
     int n_ = 1, pitch_ = 1, kind_ = 0;
     bool folded_ = false, heat_ = false, ac_ = false, h2d_ = false, gs_ = false;
     bool phi_forced_ = false;
+    bool cpts_ = false;      // level-0 u holds only the C points (ATM_STORE_CPOINTS)
+    void get_level0_cpts(int first, int count, double* out);
     std::vector<int> Lvl_;   // row-kernel chunk length per level
     int sms_ = 148;
     int world_ = 1, rank_ = 0, G_ = 1;

@@ -565,6 +565,7 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kerne
         return base + static_cast<size_t>(i - b0) * P + band;
     };
     const int m = a.m, last = a.np - 1;
+    const int ud = a.u_div > 1 ? a.u_div : 1;
     for (int J = a.j0 + cid; J < a.j1; J += ncl) {
         const int c = J * m;
         int start, end, store_from;
@@ -580,7 +581,7 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kerne
         }
         if (end < start) end = start;
         {
-            const double* src = crow(a.u, start, a.u_base);
+            const double* src = crow(a.u, a.u_base + (start - a.u_base) / ud, a.u_base);
             for_own(cx, [&](int idx, int) { xb[idx] = src[idx]; });
         }
         for (int i = start + 1; i <= end; ++i) {
@@ -598,7 +599,7 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kerne
             const int ti = end + 1;
             cg_phi_any<E>(a.co, cx, xb, rb, band, a.forced);
             const double* g = a.add_g ? crow(a.g, ti, a.g_base) : nullptr;
-            const double* uc = crow(a.u, ti, a.u_base);
+            const double* uc = crow(a.u, a.u_base + (ti - a.u_base) / ud, a.u_base);
             if (a.tail == TAIL_STORE || a.tail == TAIL_BOTH) {
                 double* dst = row(a.out, ti / m, a.out_base);
                 for_own(cx, [&](int idx, int) {

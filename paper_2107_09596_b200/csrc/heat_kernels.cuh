@@ -99,6 +99,7 @@ struct SweepArgs {
     double* sq;        // per-point squares (TAIL_SQ), indexed by tail point - sq_base
     int sq_base;
     int n_out;         // output staging buffers (1 or 2)
+    int u_div;         // > 1: the u array holds only the C points (row = (i - u_base) / u_div)
 };
 
 enum WindowKind { WK_LINEAR = 0, WK_FAS = 1, WK_FORWARD = 2, WK_APPLY = 3, WK_FAS_RHS = 4 };

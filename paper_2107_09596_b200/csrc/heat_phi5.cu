@@ -846,6 +846,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     const int jb = a.j0 + static_cast<int>(Nj * blockIdx.x / gridDim.x);
     const int je = a.j0 + static_cast<int>(Nj * (blockIdx.x + 1) / gridDim.x);
     const int m = a.m, last = a.np - 1;
+    const int ud = a.u_div > 1 ? a.u_div : 1;
     bool seed_ready = false;
     double x[L];
 
@@ -912,7 +913,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (!seed_ready) {
             if (t == 0) {
                 mbar_expect_tx(barS, bytes);
-                tma_load_2d(bufS, &tm_u, 0, (start - a.u_base) * R, barS);
+                tma_load_2d(bufS, &tm_u, 0, (start - a.u_base) / ud * R, barS);
             }
             mbar_wait(barS, phS);
             phS ^= 1;
@@ -923,7 +924,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         seed_ready = false;
         if (tail_i >= 0 && t == 0) {
             mbar_expect_tx(barS, bytes);
-            tma_load_2d(bufS, &tm_u, 0, (tail_i - a.u_base) * R, barS);
+            tma_load_2d(bufS, &tm_u, 0, (tail_i - a.u_base) / ud * R, barS);
         }
 
         // ---- chain steps u_i = Phi_i(u_{i-1}) (+ g_i)
