@@ -49,6 +49,14 @@ def configs():
                              initial_condition=T.fourier_ic(511)),
         grid=(0.0, 4.0 * 4096 / 65536, 4097, [8, 8, 8], 2), mode=T.CycleMode.VCycle, relax=T.Relaxation.F,
         iters=1)
+    # 4 at the full N_t = 65536 on one GPU: level 0 with C-point storage
+    # (17 GB instead of 137 GB; ~95 GB of level arrays in all); one cycle
+    c[7] = dict(
+        name="config4_heat2d_511x511_Nt65536_m8x8x8_k2_cpoint_storage",
+        app=lambda: T.Heat2D(511, folded=True, source=None, cg_rtol=1e-12,
+                             initial_condition=T.fourier_ic(511)),
+        grid=(0.0, 4.0, 65537, [8, 8, 8], 2), mode=T.CycleMode.VCycle, relax=T.Relaxation.F,
+        iters=1, warm=0, cpts=True)
     # Gray-Scott desk run (configs/grayscott_desk.cfg; the paper's flagship
     # problem): n = 32, 512 points over [0, 64], nested-v, m = k = 16
     c[6] = dict(
@@ -78,12 +86,12 @@ def run(cfg):
     hier = T.build_hierarchy(T.TimeGrid.make(t0, tf, npts), ms, k)
     sc = T.SolverConfig(mode=cfg["mode"], relaxation=cfg["relax"], max_iters=100, tol=cfg.get("tol", 1e-10),
                         initial_guess=cfg.get("guess", T.InitialGuess.Random), seed=20)
-    drv = T.CycleDriver(app, hier, sc)
+    drv = T.CycleDriver(app, hier, sc, cpoint_storage=cfg.get("cpts", False))
     w0 = time.perf_counter()
     drv.setup()
     if cfg["mode"] == T.CycleMode.NestedV:
         drv.nested_init()
-    drv.iterate(1)
+    drv.iterate(cfg.get("warm", 1))
     setup_s = time.perf_counter() - w0
     norms, ms_dev = drv.iterate_timed(cfg["iters"])
     ds = dof_steps(hier, app.vector_size(), cfg["relax"]) * cfg["iters"]
