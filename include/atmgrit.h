@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define ATM_ABI_VERSION 3
+#define ATM_ABI_VERSION 4
 #define ATM_MAX_LEVELS 8
 
 typedef enum {
@@ -189,6 +189,11 @@ int atm_phase_counts(const atm_ctx* ctx, int* counts, int cap);
 /* Last-iteration kernel launch count and device time of the dominant kernel
  * (bench helpers). */
 atm_status atm_last_iteration_stats(const atm_ctx* ctx, int* launches, double* sweep_ms);
+
+/* Inner linear-solver iterations run since creation (2D heat: CG; Gray-Scott:
+ * BiCGSTAB; 0 for the other families) -- the SURVEY 8(d) DOF*CG-iterations
+ * unit of the inner-solver configs. */
+atm_status atm_inner_iterations(atm_ctx* ctx, unsigned long long* out);
 
 /* `count` cycles + stopping norms, timed on the context's stream with CUDA
  * events (device milliseconds into *device_ms). */

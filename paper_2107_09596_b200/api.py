@@ -622,6 +622,13 @@ class CycleDriver:
         self._check(lib().atm_forcing(self._h, level, first_index, count, ptr(out)))
         return out
 
+    def inner_iterations(self) -> int:
+        """Inner linear-solver iterations run so far (2D heat CG, Gray-Scott
+        BiCGSTAB; 0 for the other families)."""
+        v = C.c_ulonglong(0)
+        self._check(lib().atm_inner_iterations(self._h, C.byref(v)))
+        return int(v.value)
+
     def f_relax(self, level, first_interval, count):
         self._check(lib().atm_kernel_f_relax(self._h, level, first_interval, count))
 

@@ -170,6 +170,11 @@ atm_status atm_last_iteration_stats(const atm_ctx* c, int* launches, double* swe
     return ATM_OK;
 }
 
+atm_status atm_inner_iterations(atm_ctx* c, unsigned long long* out) {
+    if (!c || !c->eng || !out) return ATM_CONFIG_ERROR;
+    return guard(c, [&] { *out = c->eng->inner_iterations(); return 0; });
+}
+
 // ---- host-only helpers ------------------------------------------------------
 
 void atm_random_state(uint64_t seed, int n, double* out) {

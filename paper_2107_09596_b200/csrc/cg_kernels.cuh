@@ -26,6 +26,7 @@ struct CgCoefDev {
     double rtol;
     int cg_max;
     int* fail;            // set to 1 when CG hits cg_max
+    unsigned long long* iters;  // running count of inner (CG / BiCGSTAB) iterations, or null
     int x_smem;           // x and r in shared memory (else xg)
     double* xg;           // global scratch: x, r rows per cluster slot
     int E;                // 0: generic kernel; > 0: register variant, E elements per thread

@@ -467,6 +467,7 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     d_ic_ = dalloc(sizeof(double) * pitch_);
     d_row_ = dalloc(sizeof(double) * pitch_);
     d_fail_ = reinterpret_cast<int*>(dalloc(sizeof(int) * 4));
+    d_inner_ = reinterpret_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
     if (!src_.empty()) {
         d_src_ = dalloc(sizeof(double) * n_);
         CK(cudaMemcpy(d_src_, src_.data(), sizeof(double) * n_, cudaMemcpyHostToDevice));
@@ -670,6 +671,7 @@ void Engine::build_coefs(Shard& s) {
             c.sdt = sub_dt;
             c.substeps = S;
             c.fail = d_fail_;
+            c.iters = d_inner_;
         } else if (h2d_) {
             CgCoefDev& c = Lv.gco;
             c.pitch = pitch_;
@@ -684,6 +686,7 @@ void Engine::build_coefs(Shard& s) {
             c.rtol = prob_.cg_rtol;
             c.cg_max = prob_.cg_max;
             c.fail = d_fail_;
+            c.iters = d_inner_;
             if (!c.x_smem) {
                 // x and r rows per cluster that can be resident at once
                 const int ncl = cg_max_clusters(c);
@@ -1869,6 +1872,13 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
                          count, cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
     for (void* p : tmp.allocs) cudaFree(p);
+}
+
+unsigned long long Engine::inner_iterations() {
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, d_inner_, sizeof(v), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    return v;
 }
 
 int Engine::phase_times(char* names, int cap_names, double* secs, int cap, int* counts) const {

@@ -140,6 +140,7 @@ public:
     int phase_times(char* names, int cap_names, double* secs, int cap, int* counts = nullptr) const;
     int last_launches() const { return last_launches_; }
     double last_sweep_ms() const { return last_sweep_ms_; }
+    unsigned long long inner_iterations();
 
 private:
     // setup helpers
@@ -217,6 +218,7 @@ private:
     double* d_ff_ = nullptr;
     double* d_prof_ = nullptr;
     int* d_fail_ = nullptr;   // Allen-Cahn Newton / heat2d CG failure flag
+    unsigned long long* d_inner_ = nullptr;  // inner CG / BiCGSTAB iterations run so far
     double* d_src_ = nullptr; // heat2d source f
     double* d_xg_ = nullptr;  // heat2d CG x scratch (one row per resident cluster)
     void check_newton();

@@ -206,6 +206,7 @@ __device__ void cg_phi(const CgCoefDev& co, Ctx& cx, double* xb, double* rb, int
             for_own(cx, [&](int idx, int off) { cx.ps[off] = rb[idx] + beta * cx.ps[off]; });
             ++it;
         }
+        if (co.iters && cx.t == 0 && cx.q == 0) atomicAdd(co.iters, static_cast<unsigned long long>(it));
     }
 }
 
@@ -295,6 +296,7 @@ __device__ void cg_phi_reg(const CgCoefDev& co, Ctx& cx, double* xb, int band, b
                 if (ok[k]) cx.ps[off[k]] = r[k] + beta * cx.ps[off[k]];
             ++it;
         }
+        if (co.iters && cx.t == 0 && cx.q == 0) atomicAdd(co.iters, static_cast<unsigned long long>(it));
     }
 }
 
@@ -413,7 +415,7 @@ __device__ void gs_phi(const CgCoefDev& co, Ctx& cx, const GsVec& g) {
             double rr = bb[0], r0n = bb[0];
             double rho = 1.0, alpha = 1.0, om = 1.0;
             const int maxit = 2 * m;
-            int lit = 0, restarts = 0;
+            int lit = 0, restarts = 0, done_it = 0;
             while (rr > tol2 && lit < maxit) {
                 const double rho_old = rho;
                 double d1[1] = {0.0};
@@ -467,7 +469,9 @@ __device__ void gs_phi(const CgCoefDev& co, Ctx& cx, const GsVec& g) {
                 cluster_sum<1>(d4, cx);
                 rr = d4[0];
                 ++lit;
+                ++done_it;
             }
+            if (co.iters && cx.t == 0) atomicAdd(co.iters, static_cast<unsigned long long>(done_it));
             if (!(rr <= tol2)) break;  // inner linear solve failed
             // ---- Newton update and residual
             loop([&](int i) { g.w[i] -= g.x[i]; });

@@ -140,3 +140,22 @@ def test_heat2d_config4_grid_cluster11_cycles():
         # the second cycle is at rounding level (k = 2 is exact after 2 cycles)
         assert abs(got - want) <= 1e-9 * abs(want) + 1e-12 * r0
     assert rel_l2(drv.get_level(0), orc.array(0)) <= 1e-10
+
+
+def test_heat2d_inner_iteration_counter():
+    # DOF x CG-iterations unit; one Phi = one CG solve whose
+    # iterations the counter adds up (0 for families without an inner solve)
+    app, hier, cfg, _ = _pair(31, 33, 1.0, [4], 2)
+    drv = T.CycleDriver(app, hier, cfg)
+    assert drv.inner_iterations() == 0
+    x = np.random.default_rng(0).standard_normal((3, 31 * 31))
+    drv.apply_phi(0, 1, x[:1])
+    one = drv.inner_iterations()
+    assert 1 <= one <= 10000
+    drv.apply_phi(0, 1, np.repeat(x[:1], 3, axis=0))
+    assert drv.inner_iterations() == 4 * one  # identical systems, identical CG runs
+    h = T.CycleDriver(T.Heat1D(63), T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, 33), [4], 2),
+                      T.SolverConfig())
+    h.setup()
+    h.iterate(1)
+    assert h.inner_iterations() == 0

@@ -93,11 +93,21 @@ def run(cfg):
         drv.nested_init()
     drv.iterate(cfg.get("warm", 1))
     setup_s = time.perf_counter() - w0
+    it0 = drv.inner_iterations()
     norms, ms_dev = drv.iterate_timed(cfg["iters"])
+    inner = drv.inner_iterations() - it0
     ds = dof_steps(hier, app.vector_size(), cfg["relax"]) * cfg["iters"]
-    return dict(config=cfg["name"], n=app.vector_size(), iterations_timed=cfg["iters"],
-                ms_per_iteration=ms_dev / cfg["iters"], dof_steps_per_s=ds / (ms_dev * 1e-3),
-                setup_plus_first_iteration_s=setup_s, norms=[float(v) for v in norms])
+    r = dict(config=cfg["name"], n=app.vector_size(), iterations_timed=cfg["iters"],
+             ms_per_iteration=ms_dev / cfg["iters"], dof_steps_per_s=ds / (ms_dev * 1e-3),
+             setup_plus_first_iteration_s=setup_s, norms=[float(v) for v in norms])
+    if inner:
+        # SURVEY 8(d) second unit for the inner-solver configs: DOF x CG
+        # iterations per second, and the 2-pass fused-CG floor of 64 B per
+        # DOF per CG iteration against the measured HBM peak
+        rate = app.vector_size() * inner / (ms_dev * 1e-3)
+        r.update(inner_iterations=inner, dof_inner_iterations_per_s=rate,
+                 cg_2pass_equiv_GBps=64.0 * rate / 1e9, cg_2pass_equiv_frac_of_hbm=64.0 * rate / 6534.5e9)
+    return r
 
 
 # bounded CPU samples (C oracle restatement, one thread) of the same n and
