@@ -19,7 +19,7 @@ __device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-__global__ void fill_random_kernel(double* u, int base, int pitch, int n, int i0, int rows,
+__global__ void fill_random_kernel(double* u, int row0, int pitch, int n, int i0, int rows,
                                    int step, uint64_t seed) {
     const long long total = static_cast<long long>(rows) * n;
     for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -30,7 +30,7 @@ __global__ void fill_random_kernel(double* u, int base, int pitch, int n, int i0
         const uint64_t st = (seed + static_cast<uint64_t>(i)) +
                             static_cast<uint64_t>(q + 1) * 0x9E3779B97F4A7C15ULL;
         const double unit = static_cast<double>(sm64_mix(st) >> 11) * 0x1.0p-53;
-        u[static_cast<size_t>((i - base) / step) * pitch + q] = 2.0 * unit - 1.0;
+        u[static_cast<size_t>(row0 + r) * pitch + q] = 2.0 * unit - 1.0;
     }
 }
 
@@ -41,7 +41,7 @@ int launch_fill_random(double* u, int base, int pitch, int n, int i0, int i1, ui
     const int rows = (i1 - i0 + step - 1) / step;
     const long long total = static_cast<long long>(rows) * n;
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 16));
-    fill_random_kernel<<<blocks, 256, 0, s>>>(u, base, pitch, n, i0, rows, step, seed);
+    fill_random_kernel<<<blocks, 256, 0, s>>>(u, (i0 - base) / step, pitch, n, i0, rows, step, seed);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -846,7 +846,9 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     const int jb = a.j0 + static_cast<int>(Nj * blockIdx.x / gridDim.x);
     const int je = a.j0 + static_cast<int>(Nj * (blockIdx.x + 1) / gridDim.x);
     const int m = a.m, last = a.np - 1;
-    const int ud = a.u_div > 1 ? a.u_div : 1;
+    // C-point-only u (u_div = m, F sweeps only): seed / tail rows J, J + 1
+    const bool cpu = a.u_div > 1;
+    const int ub = cpu ? a.u_base / a.u_div : a.u_base;
     bool seed_ready = false;
     double x[L];
 
@@ -913,7 +915,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (!seed_ready) {
             if (t == 0) {
                 mbar_expect_tx(barS, bytes);
-                tma_load_2d(bufS, &tm_u, 0, (start - a.u_base) / ud * R, barS);
+                tma_load_2d(bufS, &tm_u, 0, ((cpu ? J : start) - ub) * R, barS);
             }
             mbar_wait(barS, phS);
             phS ^= 1;
@@ -924,7 +926,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         seed_ready = false;
         if (tail_i >= 0 && t == 0) {
             mbar_expect_tx(barS, bytes);
-            tma_load_2d(bufS, &tm_u, 0, (tail_i - a.u_base) / ud * R, barS);
+            tma_load_2d(bufS, &tm_u, 0, ((cpu ? J + 1 : tail_i) - ub) * R, barS);
         }
 
         // ---- chain steps u_i = Phi_i(u_{i-1}) (+ g_i)
@@ -966,11 +968,12 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             phS ^= 1;
             row_acc<L>(bufS, x, ln, true);
             if (a.kind == SW_F && J + 1 < je) seed_ready = true;  // S holds u[c_{J+1}]
-            if (a.tail == TAIL_STORE || a.tail == TAIL_BOTH)
+            if (a.tail == TAIL_STORE) {
                 stage_out(tail_i / m - a.out_base, &tm_out, &tm_outw);
-            if (a.tail == TAIL_SQ || a.tail == TAIL_BOTH) {
+            } else {
                 const double tot = cta_sum_squares<L>(x, ln, sl);
                 if (t == 0) a.sq[tail_i - a.sq_base] = tot;
+                if (a.tail == TAIL_BOTH) stage_out(tail_i / m - a.out_base, &tm_out, &tm_outw);
             }
         }
     }
