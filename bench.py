@@ -176,14 +176,17 @@ def time_to_tolerance(T):
 
     def drive_only(reuse, cpts=False):
         drv = T.CycleDriver(app, hier, cfg, reuse_relax=reuse, cpoint_storage=cpts)
+        t0 = time.perf_counter()
         drv.setup()
         t = time.perf_counter()
         rep = drv.drive()
         d = time.perf_counter() - t
         drv.close()
+        drive_only.setup_to_tol = d + (t - t0)
         return rep, d
 
     rep1, d1 = drive_only(False)
+    s2t = drive_only.setup_to_tol
     # opt-in: reuse the correction sweep's C-point residuals as the next
     # cycle's restriction input (bitwise the same iterations)
     rep2, d2 = drive_only(True)
@@ -195,11 +198,13 @@ def time_to_tolerance(T):
     return {"config": "config5r: heat1d n=4095, N_t=2^14, t in [0,1], m=16, k=8, tol 1e-10",
             "iterations": res.report.iterations, "reference_iterations": ref_it,
             "converged": bool(res.report.converged), "seconds": wall,
+            "setup_to_tol_seconds": s2t,
             "drive_seconds": d1, "drive_seconds_reuse_relax": d2,
             "drive_seconds_reuse_relax_cpoint_storage": d3,
             "opt_ins_bitwise_same_history": bool(same),
             "what": "seconds: wall clock of solve() (context + device arrays, setup, drive to tol with "
-                    "one norm readback per iteration, level-0 state read back); drive_seconds: the "
+                    "one norm readback per iteration, level-0 state read back); setup_to_tol_seconds: "
+                    "atm_setup to the converged iteration (SURVEY 8(d)); drive_seconds: the "
                     "iterations alone, without and with the opt-ins (relax reuse; relax reuse + C-point storage)"}
 
 
