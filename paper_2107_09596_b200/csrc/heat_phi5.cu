@@ -852,10 +852,19 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     bool seed_ready = false;
     double x[L];
 
-    // stage x into an output buffer and TMA-store it; the store that last
-    // read that buffer was waited for (bulk_wait_read) before the Phi
+    // stage x into an output buffer and TMA-store it.  Per-warp stores: the
+    // warp's lane 0 waits for the reads of its previous store from that
+    // buffer only now, after the Phi (which the TMA read overlapped), and
+    // __syncwarp hands the slice to the warp's lanes
     auto stage_out = [&](int row, const CUtensorMap* map, const CUtensorMap* mapw) {
         char* o = ob ? bufO1 : bufO0;
+        if constexpr (kWarpStore) {
+            if (ln.lane == 0) {
+                if (nob == 2) bulk_wait_read<1>();
+                else bulk_wait_read<0>();
+            }
+            __syncwarp();
+        }
         row_store<L>(o, x, ln);
         fence_proxy_async();
         if constexpr (kWarpStore) {
@@ -873,10 +882,10 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         }
         ob = (nob == 2) ? ob ^ 1 : 0;
     };
-    // the issuer(s) of the stores that last read the staging buffer about to
-    // be written wait for those reads; the Phi barrier orders the rest
+    // whole-row stores (L = 2): the issuer waits for the reads of the store
+    // that last used the buffer before the Phi, whose barrier orders the rest
     auto release_staging = [&]() {
-        if (kWarpStore ? (ln.lane == 0) : (t == 0)) {
+        if (!kWarpStore && t == 0) {
             if (nob == 2) bulk_wait_read<1>();
             else bulk_wait_read<0>();
         }
