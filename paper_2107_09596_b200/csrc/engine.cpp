@@ -653,8 +653,18 @@ void Engine::build_coefs(Shard& s) {
         } else if (gs_) {
             CgCoefDev& c = Lv.gco;
             c.pitch = pitch_;
-            if (!gs_geometry(prob_.nx, c))
-                config_error("gray-scott: 2 nx^2 state exceeds the single-CTA kernel (nx <= 36)");
+            if (!gs_geometry(prob_.nx, c)) config_error("gray-scott: unsupported grid");
+            if (!c.x_smem) {
+                // ten work vectors per resident CTA in global scratch
+                if (!d_xg_) {
+                    const int ncl = cg_max_clusters(c);
+                    void* p = nullptr;
+                    CK(cudaMalloc(&p, sizeof(double) * 10 * static_cast<size_t>(ncl) * pitch_));
+                    gallocs_.push_back(p);
+                    d_xg_ = static_cast<double*>(p);
+                }
+                c.xg = d_xg_;
+            }
             const double h = prob_.gs_domain / prob_.nx;
             c.gs_h2inv = 1.0 / (h * h);
             c.gs_du = prob_.gs_du;

@@ -308,8 +308,10 @@ __device__ void cg_phi_reg(const CgCoefDev& co, Ctx& cx, double* xb, int band, b
 // |F|^2 within 2 dim iterations (restart when rho degenerates) -- the
 // published algorithm behind the reference's Eigen::BiCGSTAB, restated in
 // oracle/atm_oracle.c gs_bicgstab; then the bounds check of step().  One CTA
-// per system; w and the nine work vectors live in shared memory; CTA
-// reductions in a fixed order.
+// per system; w and the nine work vectors live in shared memory when they
+// fit (n <= 36), else in ten global scratch rows per resident CTA (the
+// paper's 128^2 grid: 2.6 MB per system, L2/HBM-streamed); CTA reductions in
+// a fixed order either way.
 
 struct GsVec {
     double *w, *prev, *x, *r, *r0, *p, *v, *s, *t, *yz;
@@ -546,6 +548,7 @@ __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned 
 // this CTA's band of the cluster's x and r (shared, or two global scratch
 // rows per cluster slot)
 __device__ __forceinline__ double* x_band(const CgCoefDev& co, const Ctx& cx, int slot) {
+    if (co.prob == 1 && !co.x_smem) return co.xg + static_cast<size_t>(10 * slot) * co.pitch;
     return co.x_smem ? cx.xs
                      : co.xg + static_cast<size_t>(2 * slot) * co.pitch + static_cast<size_t>(cx.q) * co.R * co.nx;
 }
@@ -838,11 +841,12 @@ bool gs_geometry(int nx, CgCoefDev& co) {
     co.E = -1;
     co.x_smem = 1;
     co.nt = std::min(kMaxCgThreads, std::max(64, (co.n + 31) / 32 * 32));
-    return cg_smem_bytes(co) <= kCgSmemCap;
+    if (cg_smem_bytes(co) > kCgSmemCap) co.x_smem = 0;  // work vectors in global scratch
+    return true;
 }
 
 size_t cg_smem_bytes(const CgCoefDev& co) {
-    if (co.prob == 1) return sizeof(CgShared) + 10 * static_cast<size_t>(co.n) * 8;
+    if (co.prob == 1) return sizeof(CgShared) + (co.x_smem ? 10 * static_cast<size_t>(co.n) * 8 : 0);
     size_t b = sizeof(CgShared) + static_cast<size_t>(co.R + 2) * (co.nx + 2) * 8;
     if (co.x_smem) b += 2 * static_cast<size_t>(co.R) * co.nx * 8;
     return b;

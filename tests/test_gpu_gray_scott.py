@@ -77,3 +77,28 @@ def test_gs_bounds_check_raises():
     bad = np.full(2 * 64, 5.0)  # outside [-1, 3]
     with pytest.raises(T.NonlinearSolveError):
         drv.apply_phi(0, 1, bad[None, :])
+
+
+# n >= 37: the ten work vectors no longer fit shared memory and live in
+# global scratch rows (the paper's experiment uses n = 128)
+@pytest.mark.parametrize("n", [40, 64, 128])
+def test_gs_phi_global_scratch_matches_oracle(n):
+    app, hier, cfg, orc = _pair(n, 65, 8.0, [8], 4)
+    drv = T.CycleDriver(app, hier, cfg)
+    orc.setup()
+    w0 = orc.initial_condition()
+    rng = np.random.default_rng(n)
+    xs = np.stack([w0, w0 + 0.01 * rng.standard_normal(w0.size), w0])
+    got = drv.apply_phi(0, 1, xs)
+    for j in range(xs.shape[0]):
+        want = orc.step(0, 1 + j, xs[j])
+        assert rel_l2(got[j], want) <= 1e-9, (j, rel_l2(got[j], want))
+    assert np.array_equal(got[0], got[2])  # same input, same CTA program
+
+
+def test_gs_global_scratch_nested_solve_matches_oracle():
+    app, hier, cfg, orc = _pair(48, 129, 32.0, [8], 8)
+    res = T.solve(app, hier, cfg)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"], (res.report.iterations, ref["iterations"])
+    assert rel_l2(res.state, orc.array(0)) <= 1e-9
