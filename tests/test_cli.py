@@ -150,3 +150,17 @@ def test_cli_trace_rows(tmp_path):
         phases.setdefault(ph, set()).add(int(it))
     for ph in ("relax", "restrict", "coarse", "correct", "norm"):
         assert phases.get(ph) == set(range(1, iters + 1)), ph
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,iters", [("grayscott_paper_two_level.cfg", 9),
+                                       ("grayscott_paper_three_level.cfg", 7)])
+def test_cli_grayscott_paper_runs_reproduce_published_iteration_counts(tmp_path, cfg, iters):
+    # PAPER.md tab:gray_two_level (m = 128, k = 64: 9 iterations) and
+    # tab:gray_three_level ((64, 4), k = 32, FCF: 7 iterations), 128^2 grid,
+    # 16 384 time points -- the paper's own experiment, from configs/
+    text = open(os.path.join(ROOT, "configs", cfg)).read()
+    code, out, err = run(tmp_path, text)
+    assert code == 0, err
+    hist, conv, n = _rows(out)
+    assert conv == 1 and n == iters, (n, hist)
