@@ -67,7 +67,9 @@ struct CgWindowArgs {
 void cg_geometry(int nx, CgCoefDev& co);
 // host: Gray-Scott geometry (one CTA, 10 state-size vectors in smem); false
 // when 2 nx^2 does not fit
-bool gs_geometry(int nx, CgCoefDev& co);
+// Gray-Scott; cs: CTAs per system when the work vectors live in global
+// scratch (few concurrent systems: more SMs per Phi)
+bool gs_geometry(int nx, CgCoefDev& co, int cs = 1);
 size_t cg_smem_bytes(const CgCoefDev& co);
 // clusters that can be resident at once (the number of x scratch rows needed)
 int cg_max_clusters(const CgCoefDev& co);

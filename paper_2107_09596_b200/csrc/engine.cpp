@@ -653,17 +653,22 @@ void Engine::build_coefs(Shard& s) {
         } else if (gs_) {
             CgCoefDev& c = Lv.gco;
             c.pitch = pitch_;
-            if (!gs_geometry(prob_.nx, c)) config_error("gray-scott: unsupported grid");
+            // with the work vectors in global scratch, a level with few
+            // concurrent systems (intervals, or windows on the coarsest level)
+            // gives each Phi a cluster of several CTAs
+            const int jobs = (l == H_.coarsest()) ? H_.np[l] : std::max(1, H_.n_iv(l));
+            int cs = 1;
+            while (cs < 8 && jobs * cs * 2 <= sms_) cs *= 2;
+            if (const char* e = std::getenv("ATM_GS_CS")) cs = std::atoi(e);
+            if (!gs_geometry(prob_.nx, c, cs)) config_error("gray-scott: unsupported grid");
             if (!c.x_smem) {
-                // ten work vectors per resident CTA in global scratch
-                if (!d_xg_) {
-                    const int ncl = cg_max_clusters(c);
-                    void* p = nullptr;
-                    CK(cudaMalloc(&p, sizeof(double) * 10 * static_cast<size_t>(ncl) * pitch_));
-                    gallocs_.push_back(p);
-                    d_xg_ = static_cast<double*>(p);
-                }
-                c.xg = d_xg_;
+                // ten work vectors per resident cluster in global scratch
+                // (per level: the cluster size, hence the slot count, differs)
+                const int ncl = cg_max_clusters(c);
+                void* p = nullptr;
+                CK(cudaMalloc(&p, sizeof(double) * 10 * static_cast<size_t>(ncl) * pitch_));
+                Lv.allocs.push_back(p);
+                c.xg = static_cast<double*>(p);
             }
             const double h = prob_.gs_domain / prob_.nx;
             c.gs_h2inv = 1.0 / (h * h);

@@ -67,7 +67,9 @@ __device__ __forceinline__ void csync(const Ctx& cx) {
 // thread sums cs local values (no per-thread DSMEM reads).
 template <int NV>
 __device__ __forceinline__ void cluster_sum(double (&v)[NV], Ctx& cx) {
-    const int lane = cx.t & 31, warp = cx.t >> 5, nw = (cx.nt + 31) >> 5;
+    // local thread index: cx.t spans the whole cluster for Gray-Scott
+    const int lt = threadIdx.x;
+    const int lane = lt & 31, warp = lt >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
     for (int i = 0; i < NV; ++i)
 #pragma unroll
@@ -79,7 +81,7 @@ __device__ __forceinline__ void cluster_sum(double (&v)[NV], Ctx& cx) {
     const int par = cx.par;
     cx.par ^= 1;
     if (cx.cs == 1) {
-        if (cx.t == 0) {
+        if (lt == 0) {
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
                 double s = 0.0;
@@ -93,7 +95,7 @@ __device__ __forceinline__ void cluster_sum(double (&v)[NV], Ctx& cx) {
         return;
     }
     cg::cluster_group cl = cg::this_cluster();
-    if (cx.t < cx.cs) {
+    if (lt < cx.cs) {
         // thread r delivers this CTA's partials to peer r
         double part[NV];
 #pragma unroll
@@ -102,7 +104,7 @@ __device__ __forceinline__ void cluster_sum(double (&v)[NV], Ctx& cx) {
             for (int w = 0; w < nw; ++w) s += cx.sh->wred[w][i];
             part[i] = s;
         }
-        double* dst = cl.map_shared_rank(&cx.sh->cslot[par][cx.q][0], cx.t);
+        double* dst = cl.map_shared_rank(&cx.sh->cslot[par][cx.q][0], lt);
 #pragma unroll
         for (int i = 0; i < NV; ++i) dst[i] = part[i];
     }
@@ -389,7 +391,7 @@ __device__ void gs_phi(const CgCoefDev& co, Ctx& cx, const GsVec& g) {
     bool failed = false;
     for (int sub = 0; sub < co.substeps && !failed; ++sub) {
         loop([&](int i) { g.prev[i] = g.w[i]; });
-        __syncthreads();
+        csync(cx);
         double nr[1] = {0.0};
         loop([&](int i) {
             const double F = gs_res(co, g.w, g.prev, i, n, cells, dt);
@@ -435,7 +437,7 @@ __device__ void gs_phi(const CgCoefDev& co, Ctx& cx, const GsVec& g) {
                     g.p[i] = pi;
                     g.yz[i] = pi / gs_diag(co, g.w, i, cells, dt);
                 });
-                __syncthreads();
+                csync(cx);
                 double d2[1] = {0.0};
                 loop([&](int i) {
                     const double vi = gs_jx(co, g.w, g.yz, i, n, cells, dt);
@@ -449,9 +451,9 @@ __device__ void gs_phi(const CgCoefDev& co, Ctx& cx, const GsVec& g) {
                     const double si = g.r[i] - alpha * g.v[i];
                     g.s[i] = si;
                 });
-                __syncthreads();
+                csync(cx);
                 loop([&](int i) { g.yz[i] = g.s[i] / gs_diag(co, g.w, i, cells, dt); });
-                __syncthreads();
+                csync(cx);
                 double d3[2] = {0.0, 0.0};
                 loop([&](int i) {
                     const double ti = gs_jx(co, g.w, g.yz, i, n, cells, dt);
@@ -477,7 +479,7 @@ __device__ void gs_phi(const CgCoefDev& co, Ctx& cx, const GsVec& g) {
             if (!(rr <= tol2)) break;  // inner linear solve failed
             // ---- Newton update and residual
             loop([&](int i) { g.w[i] -= g.x[i]; });
-            __syncthreads();
+            csync(cx);
             double nn[1] = {0.0};
             loop([&](int i) {
                 const double F = gs_res(co, g.w, g.prev, i, n, cells, dt);
@@ -499,7 +501,7 @@ __device__ void gs_phi(const CgCoefDev& co, Ctx& cx, const GsVec& g) {
         loop([&](int i) { bad = bad || !(g.w[i] >= co.gs_bound_lo && g.w[i] <= co.gs_bound_hi); });
         if (bad) atomicExch(co.fail, 2);
     }
-    __syncthreads();
+    csync(cx);
 }
 
 template <int E>
@@ -523,13 +525,17 @@ __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned 
     cx.q = (co.cs > 1) ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
     cx.rows = max(0, min(co.R, co.nx - cx.q * co.R));
     cx.own = cx.rows * co.nx;
-    if (co.prob == 1) {  // Gray-Scott: the whole [u; v] state is this CTA's band
-        cx.rows = 2 * co.nx;
-        cx.own = 2 * co.nx * co.nx;
-    }
-    cx.W = co.nx + 2;
     cx.t = threadIdx.x;
     cx.nt = blockDim.x;
+    if (co.prob == 1) {
+        // Gray-Scott: the whole [u; v] state is the cluster's; its CTAs act
+        // as one block of cs * nt threads over vectors in global scratch
+        cx.rows = 2 * co.nx;
+        cx.own = 2 * co.nx * co.nx;
+        cx.t = cx.q * blockDim.x + threadIdx.x;
+        cx.nt = co.cs * blockDim.x;
+    }
+    cx.W = co.nx + 2;
     cx.row0 = cx.t / co.nx;
     cx.col0 = cx.t - cx.row0 * co.nx;
     cx.dq = cx.nt / co.nx;
@@ -541,7 +547,7 @@ __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned 
     cx.rs = co.x_smem ? cx.ps + psn + static_cast<size_t>(co.R) * co.nx : nullptr;
     cx.par = 0;
     // zero p (padding columns and the domain-boundary halo rows stay zero)
-    for (size_t i = cx.t; i < psn; i += cx.nt) cx.ps[i] = 0.0;
+    for (size_t i = threadIdx.x; i < psn; i += blockDim.x) cx.ps[i] = 0.0;
     __syncthreads();
 }
 
@@ -563,7 +569,7 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kerne
     Ctx cx;
     ctx_init(cx, a.co, smem);
     const int cid = blockIdx.x / a.co.cs, ncl = gridDim.x / a.co.cs;
-    const int band = cx.q * a.co.R * a.co.nx;
+    const int band = a.co.prob == 1 ? 0 : cx.q * a.co.R * a.co.nx;
     double* xb = x_band(a.co, cx, cid);
     double* rb = r_band(a.co, cx, cid);
     const size_t P = a.co.pitch;
@@ -638,7 +644,7 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_window_kern
     Ctx cx;
     ctx_init(cx, a.co, smem);
     const int cid = blockIdx.x / a.co.cs, ncl = gridDim.x / a.co.cs;
-    const int band = cx.q * a.co.R * a.co.nx;
+    const int band = a.co.prob == 1 ? 0 : cx.q * a.co.R * a.co.nx;
     double* xb = x_band(a.co, cx, cid);
     double* rb = r_band(a.co, cx, cid);
     const size_t P = a.co.pitch;
@@ -832,7 +838,7 @@ void cg_geometry(int nx, CgCoefDev& co) {
     }
 }
 
-bool gs_geometry(int nx, CgCoefDev& co) {
+bool gs_geometry(int nx, CgCoefDev& co, int cs) {
     co.nx = nx;
     co.n = 2 * nx * nx;
     co.prob = 1;
@@ -841,7 +847,10 @@ bool gs_geometry(int nx, CgCoefDev& co) {
     co.E = -1;
     co.x_smem = 1;
     co.nt = std::min(kMaxCgThreads, std::max(64, (co.n + 31) / 32 * 32));
-    if (cg_smem_bytes(co) > kCgSmemCap) co.x_smem = 0;  // work vectors in global scratch
+    if (cg_smem_bytes(co) > kCgSmemCap) {
+        co.x_smem = 0;  // work vectors in global scratch, shared by a cluster of cs CTAs
+        co.cs = std::max(1, std::min(8, cs));
+    }
     return true;
 }
 
