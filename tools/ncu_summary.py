@@ -1,5 +1,8 @@
 """Summarise `ncu --set full` reports into profiles/ncu_*_summary.json.
-usage: python tools/ncu_summary.py out.json name=path.ncu-rep [...] [--alg BYTES]"""
+usage: python tools/ncu_summary.py out.json name=path.ncu-rep [...] [--alg=BYTES] [--dominant=name#i]
+
+--dominant names the kernel whose DRAM read + write bytes become the
+top-level "dram_bytes_per_launch" (bench.py's roofline.traffic)."""
 import csv
 import io
 import json
@@ -30,14 +33,28 @@ def raw(path):
     return res
 
 
+def to_bytes(v):
+    num, _, unit = v.partition(" ")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit.strip() or "byte"]
+    return float(num.replace(",", "")) * scale
+
+
+def dram_bytes(k):
+    return to_bytes(k["dram__bytes_read.sum"]) + to_bytes(k["dram__bytes_write.sum"])
+
+
 def main():
     out = sys.argv[1]
     alg = None
+    dominant = None
     summ = {"what": "ncu --set full --clock-control none, one launch each, config-5 bench workload",
             "kernels": {}}
     for a in sys.argv[2:]:
         if a.startswith("--alg="):
             alg = float(a.split("=", 1)[1])
+            continue
+        if a.startswith("--dominant="):
+            dominant = a.split("=", 1)[1]
             continue
         name, path = a.split("=", 1)
         for i, d in enumerate(raw(path)):
@@ -53,6 +70,9 @@ def main():
             summ["kernels"][f"{name}#{i}"] = k
     if alg:
         summ["algorithmic_bytes_per_launch"] = alg
+    if dominant:
+        summ["dominant"] = dominant
+        summ["dram_bytes_per_launch"] = dram_bytes(summ["kernels"][dominant])
     json.dump(summ, open(out, "w"), indent=1)
     print(json.dumps(summ, indent=1)[:3000])
 
