@@ -321,6 +321,7 @@ struct Lane {
     int t, lane, warp, nw, s;
     int q7, qx, qx1, ch0;  // swizzled row-staging geometry (L = 32: two 128-B rows)
     int pad0;            // first padding element of the chunk, L if none
+    bool pad_last;       // pad0 == L - 1: only the chunk's last element is padding
     int par;             // parity of the warp-total slots (one barrier per Phi)
     bool corr, inside;   // carries the boundary correction; chunk inside the row
     double Mf[5], Pfex, Mb[5], Pbex, SB, q0;
@@ -342,6 +343,7 @@ __device__ __forceinline__ void lane_init(Lane<L>& ln, const HeatCoefDev& co) {
     ln.ch0 = (ln.s & 15) >> 1;
     ln.qx1 = (ln.qx + 1) & 7;
     ln.pad0 = (ln.s + L > co.n) ? max(0, co.n - ln.s) : L;
+    ln.pad_last = ln.pad0 == L - 1;
     ln.par = 0;
     const double* sc = co.scan + ln.t * kScanPerThread;
 #pragma unroll
@@ -394,11 +396,14 @@ __device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev
 }
 
 // x[pad0 .. L) = 0 for the thread holding element n-1 (and fully padded
-// threads).  A fall-through switch: one jump and L - pad0 moves for that
-// thread instead of L predicated selects in its whole warp.
+// threads).  A single padded element at the chunk end (n = 4095 and every
+// n = k L - 1) is a select with no branch; otherwise a fall-through switch:
+// one jump and L - pad0 moves for that thread instead of L predicated
+// selects in its whole warp.
 template <int L>
 __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L>& ln) {
-    if (ln.pad0 < L) {
+    x[L - 1] = ln.pad_last ? 0.0 : x[L - 1];
+    if (ln.pad0 < L - 1) {
         switch (ln.pad0) {
         case 0: if constexpr (L > 0) x[0] = 0.0; [[fallthrough]];
         case 1: if constexpr (L > 1) x[1] = 0.0; [[fallthrough]];
@@ -850,6 +855,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     const bool cpu = a.u_div > 1;
     const int ub = cpu ? a.u_base / a.u_div : a.u_base;
     bool seed_ready = false;
+    const bool plain = (P == 0) && !a.add_g && !a.forced && a.co.substeps == 1;
     double x[L];
 
     // stage x into an output buffer and TMA-store it.  Per-warp stores: the
@@ -939,7 +945,19 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         }
 
         // ---- chain steps u_i = Phi_i(u_{i-1}) (+ g_i)
-        for (int i = start + 1; i <= end; ++i) {
+        // Plain heat steps (one sub-step, no forcing, no stored g) with none
+        // or all of the rows stored run loops without the per-step checks:
+        // the Phi is latency-bound, and each uniform branch costs its issue
+        // slot plus a reconvergence on the critical path.
+        if (plain && !(store_from <= end && a.store != STORE_NONE)) {
+            for (int i = start + 1; i <= end; ++i) tri_solve<L>(x, a.co, ln, tb, sl);
+        } else if (plain && a.store == STORE_ALL && store_from == start + 1) {
+            for (int i = start + 1; i <= end; ++i) {
+                release_staging();
+                tri_solve<L>(x, a.co, ln, tb, sl);
+                stage_out(i - a.u_base, &tm_u, &tm_uw);
+            }
+        } else for (int i = start + 1; i <= end; ++i) {
             if (a.add_g && t == 0) {
                 mbar_expect_tx(barA, bytes);
                 tma_load_2d(bufA, &tm_g, 0, (i - a.g_base) * R, barA);
@@ -967,7 +985,8 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 tma_load_2d(bufA, &tm_g, 0, (tail_i - a.g_base) * R, barA);
             }
             release_staging();
-            phi_p<P, L>(x, a.co, ln, tb, sl, ends, tail_i, a.forced);
+            if (plain) tri_solve<L>(x, a.co, ln, tb, sl);
+            else phi_p<P, L>(x, a.co, ln, tb, sl, ends, tail_i, a.forced);
             if (a.add_g) {
                 mbar_wait(barA, phA);
                 phA ^= 1;
@@ -1074,6 +1093,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (NB == 2) issue_next(1);
     }
     int cb = 0;  // buffer of the next row to consume
+    const bool plain = (P == 0) && !a.forced && a.co.substeps == 1;
     double x[L];
     auto consume = [&](bool add) {
         if (cb) {
@@ -1103,7 +1123,8 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         }
         for (int s = lo; s <= e1; ++s) {
             if (s > lo) {
-                phi_p<P, L>(x, a.co, ln, tb, sl, ends, s, a.forced);
+                if (plain) tri_solve<L>(x, a.co, ln, tb, sl);
+                else phi_p<P, L>(x, a.co, ln, tb, sl, ends, s, a.forced);
                 consume(true);  // e = Psi(e) + r_s
             }
             if (s >= e0) {
