@@ -5,8 +5,8 @@
 set -u
 mkdir -p gpurun_out
 for r in 1 2; do
-  ATM_LIB=$PWD/tools/ab/libatmgrit_base.so python tools/ab_iter.py
-  python tools/ab_iter.py
+  ATM_LIB=$PWD/tools/ab/libatmgrit_base.so timeout 300 python tools/ab_iter.py
+  timeout 300 python tools/ab_iter.py
 done
 ATM_LIB=$PWD/tools/ab/libatmgrit_base.so python tools/seqphi_probe.py 16385
 python tools/seqphi_probe.py 16385
