@@ -12,9 +12,12 @@ Per (m, k):
     default cycle -- tests/test_gpu_cpoints.py, test_relax_reuse_*);
   * device ms per iteration of the default cycle (CUDA events, 5 iterations
     after 2 warm-up) and of the opt-in cycle;
-  * the final state at a few time points, compared across k (every converged
-    run solves the same space-time system, so the states agree to the
-    tolerance -- a size-independent check where the CPU reference cannot run).
+  * the final state at three time points against sequential time stepping
+    (u_i = Phi(u_{i-1}) from u0: every converged run solves that space-time
+    system, so the states agree to what the tolerance allows -- the
+    size-independent check where the CPU reference cannot run in minutes).
+  * with --cpu-rate R (the reference's DOF*steps/s from bench.py's
+    cpu_baseline): its estimated time to tolerance, iterations x 2 n F_0 / R.
 
 usage: python tools/config5_sweep.py [out.json] [--ms 16,64] [--ks 1,2,4,8,global]
 """
@@ -68,15 +71,31 @@ def run(m, k, probe_rows):
     return out, rows
 
 
+def sequential(probe_rows):
+    """u_i = Phi(u_{i-1}) from u0 for all N_t steps: one interval (m = N_t),
+    so one cycle's F-relaxation is exactly sequential time stepping."""
+    app = T.Heat1D(N, manufactured_forcing=False, initial_condition=T.random_state(7, N))
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, NPTS), [NPTS - 1], 2)
+    cfg = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=1e-300, max_iters=1,
+                         initial_guess=T.InitialGuess.Random, seed=20)
+    drv = T.CycleDriver(app, hier, cfg)
+    drv.setup()
+    drv.iterate(1)
+    rows = {p: drv.get_level(0, first=p, count=1)[0] for p in probe_rows}
+    drv.close()
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("out", nargs="?", default="gpurun_out/config5_sweep.json")
     ap.add_argument("--ms", default="16,64")
     ap.add_argument("--ks", default="1,2,4,8,global")
-    ap.add_argument("--cpu-s-per-iter", type=float, default=None,
-                    help="reference seconds per full-size iteration (scaled from bench's cpu sample)")
+    ap.add_argument("--cpu-rate", type=float, default=None,
+                    help="reference DOF*steps/s (bench.py cpu_baseline value)")
     args = ap.parse_args()
     probe_rows = [NPTS // 4, NPTS // 2, NPTS - 1]
+    seq = sequential(probe_rows)
     res, states = [], {}
     for m in [int(x) for x in args.ms.split(",")]:
         for k in [x if x == "global" else int(x) for x in args.ks.split(",")]:
@@ -84,14 +103,18 @@ def main():
             states[(m, str(k))] = rows
             res.append(r)
             print(json.dumps(r), flush=True)
-    # every converged run solves the same space-time system: compare states
-    conv = [key for key, r in zip(states, res) if r["converged"]]
-    if conv:
-        base = states[conv[-1]]
-        for key, r in zip(states, res):
-            if r["converged"]:
-                r["max_rel_diff_vs_" + "m%d_k%s" % conv[-1]] = max(
-                    float(np.linalg.norm(states[key][p] - base[p]) / np.linalg.norm(base[p])) for p in base)
+    # every converged run solves the same space-time system as sequential
+    # time stepping: compare the probe rows with it
+    for key, r in zip(states, res):
+        r["max_rel_err_vs_sequential"] = max(
+            float(np.linalg.norm(states[key][str(p)] - seq[p]) / np.linalg.norm(seq[p])) for p in probe_rows)
+        r["max_err_vs_sequential_over_u0"] = max(
+            float(np.linalg.norm(states[key][str(p)] - seq[p]) / np.linalg.norm(T.random_state(7, N)))
+            for p in probe_rows)
+    if args.cpu_rate:
+        for r in res:
+            f0 = (NPTS - 1) - (NPTS - 1) // r["m"]
+            r["reference_seconds_estimate"] = r["iterations"] * 2.0 * N * f0 / args.cpu_rate
     summary = dict(what=__doc__.split("\n\n")[0], n=N, n_points=NPTS, tol=TOL,
                    probe_rows=probe_rows, runs=res)
     os.makedirs(os.path.dirname(os.path.abspath(args.out)), exist_ok=True)

@@ -12,3 +12,5 @@ ncu --set full --clock-control none --import-source on -k regex:heat_sweep -s 2 
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_sweep.log 2>&1; echo "sweep rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:heat_window_linear -s 1 -c 1 -o gpurun_out/prof_win \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_win.log 2>&1; echo "win rc=$?"
+python tools/config5_sweep.py gpurun_out/config5_sweep.json > gpurun_out/config5_sweep.log 2>&1; echo "config5 sweep rc=$?"
+python tools/seqphi_probe.py > gpurun_out/seqphi.txt 2>&1; echo "seqphi rc=$?"
