@@ -894,6 +894,12 @@ void Engine::window_launch(Shard& s, int level, int kind, int pre_lo, int pre_e0
         a.seed_zero = seed_zero;
         a.idx0 = idx0;
         a.seed_off = seed_off;
+        // a long prefix chain alone in the launch (classical coarse grid,
+        // k >= N_T + 1): its emits are sequential, so the next C row is
+        // fetched two emits ahead (two more staging rows; the occupancy it
+        // costs does not matter to a single chain)
+        a.two_s = kind == WK_LINEAR && has_pre && pre_e1 - pre_e0 >= 64 && p1 < p0 &&
+                  Lv.hco.L != 32 && !std::getenv("ATM_WIN_ONE_S");
         const CUtensorMap& t1 = x1.has_tm ? x1.tm : out.tm;
         const CUtensorMap& t2 = x2.has_tm ? x2.tm : t1;
         const CUtensorMap& t3 = x3.has_tm ? x3.tm : t1;

@@ -116,6 +116,7 @@ struct WindowArgs {
     int seed_zero;     // WK_APPLY: seed is the zero vector (forcing computation)
     int idx0;          // WK_APPLY: step index offset (job p applies Phi_{idx0+p})
     int seed_off;      // WK_APPLY: seed row is p + seed_off
+    int two_s;         // WK_LINEAR: double-buffered fine C rows (long prefix chain)
 };
 
 // Launchers (stream-ordered).  Return cudaError_t as int.

@@ -376,7 +376,7 @@ struct Slots {                // small shared scratch
     double z0[2], ra0[2];     // thread 0's z_loc[0] and RA_next (ncw > 1)
     double zl[2], el[2], ral[2];  // cyclic: thread tl's z_loc[pl-1], E, RA_next
     double nrm[2][kMaxWarps][2];  // Newton: per-warp residual square sums, max u^2
-    uint64_t bar[4];
+    uint64_t bar[5];
 };
 
 __device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev& co) {
@@ -1031,13 +1031,18 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     constexpr int NB = (L == 32) ? 1 : 2;
     char* bufA0 = base;
     char* bufA1 = base + (NB - 1) * rb;
+    // fine C rows: one buffer, or three (a.two_s: long prefix chains, whose
+    // emits are back to back: row s + 2 is fetched at emit s into the buffer
+    // of emit s - 1, whose store has had a whole step to drain, so neither
+    // the store's smem read nor the load sits on the chain)
+    const int NS = a.two_s ? 3 : 1;
     char* bufS = base + NB * rb;
-    Tabs& tb = *reinterpret_cast<Tabs*>(base + (NB + 1) * rb);
-    Slots& sl = *reinterpret_cast<Slots*>(base + (NB + 1) * rb + sizeof(Tabs));
-    double* ends = reinterpret_cast<double*>(base + (NB + 1) * rb + sizeof(Tabs) + sizeof(Slots));
+    Tabs& tb = *reinterpret_cast<Tabs*>(base + (NB + NS) * rb);
+    Slots& sl = *reinterpret_cast<Slots*>(base + (NB + NS) * rb + sizeof(Tabs));
+    double* ends = reinterpret_cast<double*>(base + (NB + NS) * rb + sizeof(Tabs) + sizeof(Slots));
     uint64_t* barA0 = &sl.bar[0];
     uint64_t* barA1 = &sl.bar[1];
-    uint64_t* barS = &sl.bar[2];
+    uint64_t* barS = &sl.bar[2];  // S_b uses sl.bar[2 + b] (Slots.bar has 5)
     const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
     const int R = pitch >> 4;
 
@@ -1048,11 +1053,11 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     if (t == 0) {
         mbar_init(barA0, 1);
         mbar_init(barA1, 1);
-        mbar_init(barS, 1);
+        for (int b = 0; b < NS; ++b) mbar_init(barS + b, 1);
         mbar_fence_init();
     }
     __syncthreads();
-    uint32_t ph0 = 0, ph1 = 0, phS = 0;
+    uint32_t ph0 = 0, ph1 = 0, phS = 0;  // phS: bit b = phase of S_b
 
     const bool has_pre = a.pre_e1 >= a.pre_e0;
     const int n_ind = max(0, a.p1 - a.p0 + 1);
@@ -1116,10 +1121,14 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         int lo, e0, e1;
         job_range(q, lo, e0, e1);
         consume(false);  // e = r_lo
+        const int f0 = max(e0, lo);  // first emitted C row of the job
         if (t == 0) {
             bulk_wait_read<0>();  // S free again
-            mbar_expect_tx(barS, bytes);
-            tma_load_2d(bufS, &tm_fine, 0, (max(e0, lo) * a.out_stride - a.out_base) * R, barS);
+            for (int b = 0; b < (NS == 1 ? 1 : NS - 1) && f0 + b <= e1; ++b) {
+                mbar_expect_tx(barS + b, bytes);
+                tma_load_2d(bufS + b * rb, &tm_fine, 0, ((f0 + b) * a.out_stride - a.out_base) * R,
+                            barS + b);
+            }
         }
         for (int s = lo; s <= e1; ++s) {
             if (s > lo) {
@@ -1128,24 +1137,37 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 consume(true);  // e = Psi(e) + r_s
             }
             if (s >= e0) {
-                // fine.u[c_s] += e
-                mbar_wait(barS, phS);
-                phS ^= 1;
+                // fine.u[c_s] += e (emits rotate over the NS buffers)
+                const int sb = (NS == 1) ? 0 : (s - f0) % NS;
+                char* bs = bufS + sb * rb;
+                mbar_wait(barS + sb, (phS >> sb) & 1);
+                phS ^= 1u << sb;
                 double y[L];
-                row_load<L>(bufS, y, ln);
+                row_load<L>(bs, y, ln);
 #pragma unroll
                 for (int e = 0; e < L; ++e) y[e] += x[e];
-                row_store<L>(bufS, y, ln);
+                row_store<L>(bs, y, ln);
                 fence_proxy_async();
                 __syncthreads();
                 if (t == 0) {
-                    tma_store_2d(&tm_fine, 0, (s * a.out_stride - a.out_base) * R, bufS);
+                    tma_store_2d(&tm_fine, 0, (s * a.out_stride - a.out_base) * R, bs);
                     bulk_commit();
-                    if (s + 1 <= e1) {
-                        bulk_wait_read<0>();
-                        mbar_expect_tx(barS, bytes);
-                        tma_load_2d(bufS, &tm_fine, 0, ((s + 1) * a.out_stride - a.out_base) * R,
-                                    barS);
+                    if (NS == 1) {
+                        if (s + 1 <= e1) {
+                            bulk_wait_read<0>();
+                            mbar_expect_tx(barS, bytes);
+                            tma_load_2d(bufS, &tm_fine, 0, ((s + 1) * a.out_stride - a.out_base) * R,
+                                        barS);
+                        }
+                    } else if (s + NS - 1 <= e1) {
+                        // row s + NS - 1 goes to the buffer of emit s - 1 (for
+                        // s = f0 the never-used last buffer): all stores but
+                        // this emit's have finished reading
+                        const int nb = (s - f0 + NS - 1) % NS;
+                        bulk_wait_read<1>();
+                        mbar_expect_tx(barS + nb, bytes);
+                        tma_load_2d(bufS + nb * rb, &tm_fine, 0,
+                                    ((s + NS - 1) * a.out_stride - a.out_base) * R, barS + nb);
                     }
                 }
             }
@@ -1326,7 +1348,7 @@ size_t heat_sweep_smem(const SweepArgs& a) {
 
 size_t heat_window_smem(const WindowArgs& a) {
     int rows;
-    if (a.kind == WK_LINEAR) rows = a.co.L == 32 ? 2 : 3;
+    if (a.kind == WK_LINEAR) rows = (a.co.L == 32 ? 2 : 3) + (a.two_s ? 2 : 0);
     else rows = (a.kind == WK_FAS || a.kind == WK_FAS_RHS) ? 5 : 3;
     return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) +
            sizeof(Slots) + ends_bytes(a.co);

@@ -370,3 +370,37 @@ def test_relax_reuse_invalidated_by_set_level():
     na, nb = drv_a.iterate(3), drv_b.iterate(3)
     assert np.array_equal(na, nb)
     assert np.array_equal(drv_a.get_level(0), drv_b.get_level(0))
+
+
+@pytest.mark.parametrize("m,k", [(16, 8), (64, 4)])
+def test_config5_shape_large_front_bound_and_sequential_state(m, k):
+    """Config-5 shape at N_t = 2^16 (beyond what the CPU oracle finishes in
+    seconds), size-independent properties: with a random guess the solve
+    converges once the exact-C-point front has crossed the grid, i.e. in
+    N_T/k (+1) iterations (test_solver.cpp:428-465), and the converged state
+    equals sequential time stepping (a single interval, m = N_t, whose one
+    F-relaxation IS u_i = Phi(u_{i-1})) to what the 1e-10 residual allows."""
+    n, npts = 4095, 2 ** 16 + 1
+    app = T.Heat1D(n, manufactured_forcing=False, initial_condition=T.random_state(7, n))
+    rows = [npts // 4, npts // 2, npts - 1]
+    seq_h = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, npts), [npts - 1], 2)
+    seq = T.CycleDriver(app, seq_h, T.SolverConfig(relaxation=T.Relaxation.F, tol=1e-300, max_iters=1,
+                                                   initial_guess=T.InitialGuess.Random, seed=20))
+    seq.setup()
+    seq.iterate(1)
+    ref = {p: seq.get_level(0, first=p, count=1)[0] for p in rows}
+    seq.close()
+    n_t = (npts - 1) // m
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, npts), [m], k)
+    cfg = T.SolverConfig(relaxation=T.Relaxation.F, tol=1e-10, max_iters=2 * n_t // k + 50,
+                         initial_guess=T.InitialGuess.Random, seed=20)
+    drv = T.CycleDriver(app, hier, cfg, reuse_relax=True, cpoint_storage=True)
+    drv.setup()
+    rep = drv.drive()
+    assert rep.converged
+    assert n_t // k <= rep.iterations <= n_t // k + 2, rep.iterations
+    u0 = np.linalg.norm(T.random_state(7, n))
+    for p in rows:
+        err = np.linalg.norm(drv.get_level(0, first=p, count=1)[0] - ref[p]) / u0
+        assert err < 1e-11, (p, err)
+    drv.close()
