@@ -208,6 +208,39 @@ def time_to_tolerance(T):
                     "iterations alone, without and with the opt-ins (relax reuse; relax reuse + C-point storage)"}
 
 
+def time_to_tolerance_full(T, W, name, app, hier, dev, world, rank, nccl_id, pg):
+    """Setup + solve to 1e-10 on the bench workload itself (full N_t), on
+    every rank of the job: atm_setup to the converged iteration, wall clock
+    between barriers, max over ranks.  Runs the bitwise-neutral opt-ins
+    (relax reuse + C-point storage: the default cycle's iterations and
+    norms, tests/test_gpu_cpoints.py).  With a random guess the heat problem
+    converges at the N_T/k front bound (test_solver.cpp:428-465)."""
+    n_t = (W["n_points"] - 1) // W["m"]
+    cfg = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=W["tol"],
+                         max_iters=2 * n_t // W["k"] + 100, initial_guess=T.InitialGuess.Random,
+                         seed=W["guess_seed"])
+    drv = T.CycleDriver(app, hier, cfg, device=dev, world_size=world, rank=rank, nccl_id=nccl_id,
+                        reuse_relax=True, cpoint_storage=True)
+    if pg:
+        pg.barrier()
+    t0 = time.perf_counter()
+    drv.setup()
+    rep = drv.drive()
+    secs = time.perf_counter() - t0
+    drv.close()
+    if pg:
+        import torch
+        t = torch.tensor([secs], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        secs = float(t.item())
+    return {"config": f"bench workload ({name}), tol {W['tol']:g}", "n_gpus": world,
+            "iterations": rep.iterations, "front_bound": -(-n_t // W["k"]),
+            "converged": bool(rep.converged), "setup_to_tol_seconds": secs,
+            "last_norm": float(rep.residual_norms[-1]) if rep.residual_norms else None,
+            "what": "atm_setup + drive to tol (one norm readback per iteration), wall clock, max over "
+                    "ranks; relax reuse + C-point storage (bitwise the default cycle's iterations)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -216,6 +249,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ttt-full", action="store_true")
     ap.add_argument("--n-points", type=int, default=WORKLOAD["n_points"])
     ap.add_argument("--k", type=int, default=WORKLOAD["k"])
     ap.add_argument("--m", type=int, default=WORKLOAD["m"])
@@ -383,6 +417,15 @@ def main():
             T.lib().atm_host_unregister(gsl.ctypes.data)
             T.lib().atm_host_unregister(osl.ctypes.data)
 
+    # ---- time-to-tolerance on the full bench workload, every rank
+    ttf = None
+    if not args.no_ttt_full:
+        try:
+            ttf = time_to_tolerance_full(T, W, config["workload"], app, hier, dev, world, rank, nccl_id, pg)
+            line["time_to_tolerance_full"] = ttf
+        except Exception as e:  # reported, not fatal
+            line["time_to_tolerance_full"] = {"unavailable": str(e)}
+
     # ---- time-to-tolerance (BASELINE metric, second half) on the config-5
     # shape at N_t = 2^14 (t in [0,1], k = 8), where the compiled reference's
     # iteration count is pinned (tests/golden/cases.json config5r_k8)
@@ -401,6 +444,10 @@ def main():
             if ttt and "iterations" in ttt:
                 # same N_t = 2^14 sizes: reference seconds per iteration x its iteration count
                 ttt["reference_seconds_estimate"] = cb["seconds_per_iteration"] * ttt["reference_iterations"]
+            if ttf and "iterations" in ttf:
+                # full size: the sample's rate over the workload's DOF*steps per iteration
+                ttf["reference_seconds_estimate"] = (dof_steps_per_iter(n, W["n_points"], W["m"]) /
+                                                     cb["value"] * ttf["iterations"])
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "unit": unit, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}

@@ -4,13 +4,13 @@
 set -u
 mkdir -p gpurun_out
 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo "bench rc=$?"
-python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain.log 2>&1 && \
+python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-ttt-full > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_list.log 2>&1; echo "list rc=$?"
-python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/plain2.log 2>&1 && \
+    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-ttt-full > gpurun_out/ncu_list.log 2>&1; echo "list rc=$?"
+python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-ttt-full > gpurun_out/plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:heat_sweep -s 2 -c 2 -o gpurun_out/prof_sweep \
-    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_sweep.log 2>&1; echo "sweep rc=$?"
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-ttt-full > gpurun_out/ncu_sweep.log 2>&1; echo "sweep rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:heat_window_linear -s 1 -c 1 -o gpurun_out/prof_win \
-    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_win.log 2>&1; echo "win rc=$?"
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-ttt-full > gpurun_out/ncu_win.log 2>&1; echo "win rc=$?"
 python tools/config5_sweep.py gpurun_out/config5_sweep.json > gpurun_out/config5_sweep.log 2>&1; echo "config5 sweep rc=$?"
 python tools/seqphi_probe.py > gpurun_out/seqphi.txt 2>&1; echo "seqphi rc=$?"
