@@ -401,17 +401,23 @@ def main():
         o0, o1 = rr["lo"][0], rr["hi"][0] + 1
         drv2.get_level(0, first=o0, count=o1 - o0, out=out[o0:o1])
         wall = time.perf_counter() - t0
+        # bytes the engine actually moved (setup sends the guess's C rows:
+        # its F rows are dead under cycling, see atm_host_traffic)
+        h2d, d2h = drv2.host_traffic()
         if pg:
             import torch
             t = torch.tensor([wall], dtype=torch.float64)
             pg.all_reduce(t, op=pg.ReduceOp.MAX)
             wall = float(t.item())
-        h2d = gsl.nbytes * world  # every rank moves its own block
+            tb = torch.tensor([h2d, d2h], dtype=torch.float64)
+            pg.all_reduce(tb, op=pg.ReduceOp.SUM)
+            h2d, d2h = int(tb[0].item()), int(tb[1].item())
         line["e2e"] = {"value": per_iter * rep.iterations / wall, "unit": unit,
                        "h2d_bytes_per_step": int(h2d / args.steps),
-                       "d2h_bytes_per_step": int(osl.nbytes * world / args.steps + 8),
+                       "d2h_bytes_per_step": int(d2h / args.steps + 8),
+                       "guess_bytes_offered": int(gsl.nbytes * world),
                        "wall_s": wall, "pinned": bool(reg),
-                       "what": "atm_setup(provided guess from pinned host) + atm_solve(K iterations) + atm_get_level(level 0) into pinned host"}
+                       "what": "atm_setup(provided guess from pinned host: its C rows are sent, its F rows are dead under cycling) + atm_solve(K iterations) + atm_get_level(level 0) into pinned host"}
         drv2.close()
         if reg:
             T.lib().atm_host_unregister(gsl.ctypes.data)

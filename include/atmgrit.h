@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define ATM_ABI_VERSION 4
+#define ATM_ABI_VERSION 5
 #define ATM_MAX_LEVELS 8
 
 typedef enum {
@@ -97,7 +97,11 @@ typedef struct atm_solver {
     int initial_guess;
     uint64_t seed;
     const double* constant_value; /* n values or NULL (=> initial condition)       */
-    const double* provided;       /* n_points*n values (InitialGuess::Provided)    */
+    const double* provided;       /* n_points*n values (InitialGuess::Provided);   *
+                                   * caller-owned, must stay valid until the first  *
+                                   * cycle (atm_cycle / atm_solve / atm_iterate)    *
+                                   * returns: setup sends the C rows, the F rows    *
+                                   * are read only if needed before that cycle      */
     int coarse_substeps;
 } atm_solver;
 
@@ -194,6 +198,12 @@ atm_status atm_last_iteration_stats(const atm_ctx* ctx, int* launches, double* s
  * BiCGSTAB; 0 for the other families) -- the SURVEY 8(d) DOF*CG-iterations
  * unit of the inner-solver configs. */
 atm_status atm_inner_iterations(atm_ctx* ctx, unsigned long long* out);
+
+/* Level-0 state bytes moved so far between host and device: the provided
+ * guess (atm_setup sends its C rows; its F rows only if something reads them
+ * before the first cycle, which rewrites them) and atm_get_level /
+ * atm_set_level.  The e2e bench reports these. */
+atm_status atm_host_traffic(const atm_ctx* ctx, unsigned long long* h2d, unsigned long long* d2h);
 
 /* `count` cycles + stopping norms, timed on the context's stream with CUDA
  * events (device milliseconds into *device_ms). */

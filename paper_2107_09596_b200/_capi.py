@@ -84,6 +84,7 @@ SIGNATURES = {
     "atm_phase_times": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, _DP, C.c_int]),
     "atm_last_iteration_stats": (C.c_int, [C.c_void_p, _IP, _DP]),
     "atm_inner_iterations": (C.c_int, [C.c_void_p, C.POINTER(C.c_ulonglong)]),
+    "atm_host_traffic": (C.c_int, [C.c_void_p, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     "atm_phase_counts": (C.c_int, [C.c_void_p, _IP, C.c_int]),
     "atm_iterate_timed": (C.c_int, [C.c_void_p, C.c_int, _DP, _DP]),
     "atm_host_register": (C.c_int, [C.c_void_p, C.c_size_t]),

@@ -629,6 +629,12 @@ class CycleDriver:
         self._check(lib().atm_inner_iterations(self._h, C.byref(v)))
         return int(v.value)
 
+    def host_traffic(self):
+        """(host-to-device, device-to-host) level-0 state bytes moved so far."""
+        h, d = C.c_ulonglong(0), C.c_ulonglong(0)
+        self._check(lib().atm_host_traffic(self._h, C.byref(h), C.byref(d)))
+        return int(h.value), int(d.value)
+
     def f_relax(self, level, first_interval, count):
         self._check(lib().atm_kernel_f_relax(self._h, level, first_interval, count))
 

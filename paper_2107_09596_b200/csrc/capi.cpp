@@ -175,6 +175,12 @@ atm_status atm_inner_iterations(atm_ctx* c, unsigned long long* out) {
     return guard(c, [&] { *out = c->eng->inner_iterations(); return 0; });
 }
 
+atm_status atm_host_traffic(const atm_ctx* c, unsigned long long* h2d, unsigned long long* d2h) {
+    if (!c || !c->eng) return ATM_CONFIG_ERROR;
+    c->eng->host_traffic(h2d, d2h);
+    return ATM_OK;
+}
+
 // ---- host-only helpers ------------------------------------------------------
 
 void atm_random_state(uint64_t seed, int n, double* out) {

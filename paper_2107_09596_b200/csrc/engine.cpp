@@ -393,8 +393,8 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
         ff_.assign(p.fine_forcing, p.fine_forcing + p.n_ff);
     if (s.functional_w) fw_.assign(s.functional_w, s.functional_w + n_);
     if (s.constant_value) cval_.assign(s.constant_value, s.constant_value + n_);
-    // the provided guess stays caller-owned until setup (no host copy: it can
-    // be the full level-0 array)
+    // the provided guess stays caller-owned until the first cycle (no host copy:
+    // it can be the full level-0 array)
     prov_ptr_ = s.provided;
     prob_.ic = nullptr;
     prob_.fine_forcing = nullptr;
@@ -1095,14 +1095,51 @@ void Engine::fill_initial_guess() {
                              "fill random");
                 break;
             case ATM_GUESS_PROVIDED:
-                if (nrows > 0)
+                if (nrows > 0 && dv == 1 && H_.L >= 2 && H_.m[0] > 1 && !std::getenv("ATM_EAGER_GUESS")) {
+                    // Only the C rows go now. Every cycle opens with an
+                    // F-relaxation from the C points (kernels.cpp:7-17) and
+                    // its correction F-sweep rewrites every F row before
+                    // anything reads one, so the guess's F values are dead
+                    // under cycling; an access that could see them first
+                    // (residual_norm, level-0 reads/writes, kernel-level
+                    // entry points, nested init) copies them (flush_guess).
+                    const int m = H_.m[0];
+                    const int c0 = (i0 + m - 1) / m * m;
+                    const int nc = c0 < i1 ? (i1 - 1 - c0) / m + 1 : 0;
+                    if (nc > 0)
+                        CK(cudaMemcpy2DAsync(Lv.u.p + Lv.u.off(c0, pitch_), sizeof(double) * pitch_ * m,
+                                             prov_ptr_ + static_cast<size_t>(c0) * n_,
+                                             sizeof(double) * n_ * m, sizeof(double) * n_, nc,
+                                             cudaMemcpyHostToDevice, st_));
+                    h2d_bytes_ += sizeof(double) * n_ * static_cast<size_t>(nc);
+                    guess_pending_ = true;
+                } else if (nrows > 0) {
                     CK(cudaMemcpy2DAsync(Lv.u.p + Lv.u.off(i0, pitch_),
                                          sizeof(double) * pitch_, prov_ptr_ + static_cast<size_t>(i0) * n_,
                                          sizeof(double) * n_ * dv, sizeof(double) * n_, nrows,
                                          cudaMemcpyHostToDevice, st_));
+                    h2d_bytes_ += sizeof(double) * n_ * static_cast<size_t>(nrows);
+                }
                 break;
         }
     }
+}
+
+// the deferred F rows of a provided guess (full level-0 storage only)
+void Engine::flush_guess() {
+    if (!guess_pending_) return;
+    guess_pending_ = false;
+    for (Shard& s : sh_) {
+        LevelDev& Lv = s.lv[0];
+        if (Lv.hi < Lv.lo) continue;
+        const int i0 = std::max(1, Lv.lo), i1 = Lv.hi + 1;
+        if (i1 <= i0) continue;
+        CK(cudaMemcpy2DAsync(Lv.u.p + Lv.u.off(i0, pitch_), sizeof(double) * pitch_,
+                             prov_ptr_ + static_cast<size_t>(i0) * n_, sizeof(double) * n_,
+                             sizeof(double) * n_, i1 - i0, cudaMemcpyHostToDevice, st_));
+        h2d_bytes_ += sizeof(double) * n_ * static_cast<size_t>(i1 - i0);
+    }
+    CK(cudaStreamSynchronize(st_));
 }
 
 void Engine::fill_level_rhs(int level) {
@@ -1410,6 +1447,7 @@ bool Engine::use_graphs() const {
 
 void Engine::cycle() {
     setup();
+    guess_pending_ = false;  // this cycle rewrites every level-0 F row before reading one
     launches_ = 0;
     // with relax reuse the first cycle (which still runs the opening F-sweep)
     // is not the steady-state launch sequence: capture from the second on
@@ -1467,6 +1505,7 @@ void Engine::check_newton() {
 void Engine::nested_init() {
     // solver.cpp:331-368
     setup();
+    flush_guess();
     relax_valid_ = false;
     const int lc = H_.coarsest();
     for (int l = 0; l < lc; ++l) {
@@ -1539,6 +1578,7 @@ void Engine::nested_init() {
 double Engine::residual_norm() {
     // full residual over all level-0 points (solver.cpp:370-378), m = 1 jobs
     setup();
+    flush_guess();
     phase_begin("norm");
     halo(0, &LevelDev::u);
     for (Shard& s : sh_) {
@@ -1678,6 +1718,7 @@ void Engine::xfer_level(int level, int which, int first, int count, double* host
         setup();
         relax_valid_ = false;
     }
+    if (level == 0) flush_guess();
     CK(cudaStreamSynchronize(st_));
     if (to_host && level == 0 && which == 0 && cpts_) {
         get_level0_cpts(first, count, host);
@@ -1704,6 +1745,7 @@ void Engine::xfer_level(int level, int which, int first, int count, double* host
         const int nrow = (hi - lo) / dv + 1;
         double* h = host + static_cast<size_t>(lo - first) * n_;
         double* d = a->p + a->off(lo, pitch_);
+        (to_host ? d2h_bytes_ : h2d_bytes_) += sizeof(double) * n_ * static_cast<size_t>(nrow);
         if (to_host)
             CK(cudaMemcpy2DAsync(h, sizeof(double) * n_ * dv, d, sizeof(double) * pitch_,
                                  sizeof(double) * n_, nrow, cudaMemcpyDeviceToHost, st_));
@@ -1745,6 +1787,7 @@ void Engine::get_level0_cpts(int first, int count, double* out) {
             }
             std::swap(Lv.u, T);
             const int r0 = std::max(lo, cb), r1 = std::min(hi, ce);
+            d2h_bytes_ += sizeof(double) * n_ * static_cast<size_t>(r1 - r0 + 1);
             CK(cudaMemcpy2DAsync(out + static_cast<size_t>(r0 - first) * n_, sizeof(double) * n_,
                                  T.p + T.off(r0, pitch_), rowb, sizeof(double) * n_, r1 - r0 + 1,
                                  cudaMemcpyDeviceToHost, st_));
@@ -1803,6 +1846,7 @@ void Engine::kernel_f_relax(int level, int first_iv, int count) {
     relax_valid_ = false;
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
+    flush_guess();
     sweep_jobs(sh_[0], level, SW_F, first_iv, first_iv + count, TAIL_NONE, 0, nullptr, 0);
     CK(cudaStreamSynchronize(st_));
     check_newton();
@@ -1814,6 +1858,7 @@ void Engine::kernel_c_relax(int level, int first_c, int count) {
     relax_valid_ = false;
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
+    flush_guess();
     sweep_jobs(sh_[0], level, SW_CRELAX, std::max(1, first_c), first_c + count, TAIL_NONE, 0,
                nullptr, 0);
     CK(cudaStreamSynchronize(st_));
@@ -1825,6 +1870,7 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
         config_error("kernel-level entry points need full level-0 storage");
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
+    flush_guess();
     Shard& s = sh_[0];
     LevelDev tmp;
     DArr r = alloc_arr(tmp, first, count, true, Lvl_.empty() ? 0 : Lvl_[level]);

@@ -141,6 +141,11 @@ public:
     int last_launches() const { return last_launches_; }
     double last_sweep_ms() const { return last_sweep_ms_; }
     unsigned long long inner_iterations();
+    // state bytes moved between host and device (guess, get/set_level)
+    void host_traffic(unsigned long long* h2d, unsigned long long* d2h) const {
+        if (h2d) *h2d = h2d_bytes_;
+        if (d2h) *d2h = d2h_bytes_;
+    }
 
 private:
     // setup helpers
@@ -150,6 +155,7 @@ private:
     // by per-warp slices (its slice-map box is 2 slice_L rows)
     DArr alloc_arr(LevelDev& L, int base, int rows, bool tmap, int slice_L = 0);
     void fill_initial_guess();
+    void flush_guess();
     void fill_level_rhs(int level);
     // cycle pieces
     // f_dead: the cycle's correction F-sweep rewrites every F row of the
@@ -235,6 +241,10 @@ private:
     std::vector<Pending> pending_;
     std::map<std::string, int> phase_cnt_;
     const double* prov_ptr_ = nullptr;
+    // level-0 F rows of a provided guess not yet copied (setup sent the C
+    // rows only; the first cycle overwrites every F row before reading it)
+    bool guess_pending_ = false;
+    unsigned long long h2d_bytes_ = 0, d2h_bytes_ = 0;
     const char* cur_phase_ = nullptr;
     cudaEvent_t cur_ev_ = nullptr;
     std::vector<cudaEvent_t> ev_pool_;

@@ -1,0 +1,142 @@
+"""Provided initial guess: atm_setup sends only the level-0 C rows.
+
+Every cycle opens with an F-relaxation from the C points (kernels.cpp:7-17)
+and its correction F-sweep rewrites every level-0 F row before anything reads
+one, so the F values of a provided guess (solver.cpp:129-131) cannot reach
+the result.  The engine therefore defers them: they are copied only if
+something could read them before the first cycle (the full residual norm,
+level-0 reads and writes, the kernel-level entry points, nested init).
+
+Checks: a guess whose F rows are NaN solves BITWISE like the same guess with
+finite F rows copied eagerly (ATM_EAGER_GUESS=1), across cycle modes,
+relaxations, families and shard counts; every pre-cycle access sees the full
+guess; the traffic counters report what moved."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2107_09596_b200 as T
+from helpers import device_objects
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # two-level F, short trailing interval (n_points - 1 not a multiple of m)
+    dict(problem="heat1d", n=255, tf=1.0, n_points=1000, m=8, k=3, folded=0, manufactured=0,
+         max_iters=40, tol=1e-10),
+    # two-level FCF, L = 16 rows
+    dict(problem="heat1d", n=4095, tf=1.0 / 64, n_points=1025, m=16, k=8, folded=0, manufactured=0,
+         relax="FCF", max_iters=30, tol=1e-10),
+    # FAS V-cycle on three levels, manufactured forcing
+    dict(problem="heat1d", n=127, tf=1.0, n_points=1025, m="4,4", k=3, folded=1, manufactured=1,
+         mode="v-cycle", max_iters=40, tol=1e-10),
+    # scalar backend
+    dict(problem="dahlquist", tf=2.0, n_points=4097, m="4,4", k=2, folded=1, mode="v-cycle",
+         max_iters=40, tol=1e-12),
+]
+
+
+def _guess(args, n, seed=0):
+    npts = int(args["n_points"])
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, (npts, n))
+
+
+def _f_rows_nan(args, g):
+    m = int(str(args["m"]).split(",")[0])
+    h = g.copy()
+    f = np.ones(len(h), bool)
+    f[::m] = False
+    h[f] = np.nan
+    return h
+
+
+def _solve(args, guess, workers, eager, monkeypatch):
+    if eager:
+        monkeypatch.setenv("ATM_EAGER_GUESS", "1")
+    else:
+        monkeypatch.delenv("ATM_EAGER_GUESS", raising=False)
+    app, hier, cfg = device_objects(dict(args, guess="provided"))
+    cfg.provided = guess
+    return T.solve(app, hier, cfg, workers=workers)
+
+
+@pytest.mark.parametrize("args", CASES)
+@pytest.mark.parametrize("workers", [1, 3])
+def test_nan_f_rows_solve_bitwise_like_eager_copy(args, workers, monkeypatch):
+    n = 1 if args["problem"] != "heat1d" else int(args["n"])
+    g = _guess(args, n)
+    a = _solve(args, g, workers, True, monkeypatch)
+    b = _solve(args, _f_rows_nan(args, g), workers, False, monkeypatch)
+    assert a.report.iterations == b.report.iterations
+    assert np.array_equal(np.array(a.report.residual_norms), np.array(b.report.residual_norms))
+    assert np.array_equal(a.state, b.state)
+    assert np.isfinite(b.state).all()
+
+
+def _driver(args, guess, monkeypatch, eager=False, **kw):
+    if eager:
+        monkeypatch.setenv("ATM_EAGER_GUESS", "1")
+    else:
+        monkeypatch.delenv("ATM_EAGER_GUESS", raising=False)
+    app, hier, cfg = device_objects(dict(args, guess="provided"))
+    cfg.provided = guess
+    d = T.CycleDriver(app, hier, cfg, **kw)
+    d.setup()
+    return d
+
+
+def test_pre_cycle_accesses_see_the_full_guess(monkeypatch):
+    args = CASES[0]
+    g = _guess(args, 255, seed=3)
+    # full residual norm before any cycle reads every F row
+    e = _driver(args, g, monkeypatch, eager=True)
+    ref_norm = e.residual_norm()
+    ref_state = e.get_level(0)
+    lz = _driver(args, g, monkeypatch)
+    assert lz.residual_norm() == ref_norm
+    # level-0 read before any cycle: the provided guess (point 0 = IC)
+    lz2 = _driver(args, g, monkeypatch)
+    s = lz2.get_level(0)
+    assert np.array_equal(s, ref_state)
+    assert np.array_equal(s[1:], g[1:])
+    # kernel-level F-relaxation of one interval reads no F row, but the
+    # residual of an F point does
+    k1 = _driver(args, g, monkeypatch)
+    k2 = _driver(args, g, monkeypatch, eager=True)
+    r1 = k1.residual(0, 0, 40)
+    r2 = k2.residual(0, 0, 40)
+    assert np.array_equal(r1, r2)
+    # a partial level-0 write before the first cycle keeps the other F rows
+    w = _driver(args, g, monkeypatch)
+    w.set_level(0, np.full((2, 255), 0.5), first=9)
+    s = w.get_level(0)
+    assert np.array_equal(s[9:11], np.full((2, 255), 0.5))
+    assert np.array_equal(s[11:], g[11:])
+    assert np.array_equal(s[1:9], g[1:9])
+
+
+def test_nested_v_with_provided_guess(monkeypatch):
+    args = dict(problem="heat1d", n=255, tf=1.0, n_points=1025, m="8,4", k=2, folded=1, manufactured=1,
+                mode="nested-v", max_iters=30, tol=1e-10)
+    g = _guess(args, 255, seed=4)
+    a = _solve(args, g, 1, True, monkeypatch)
+    b = _solve(args, g, 1, False, monkeypatch)
+    assert a.report.iterations == b.report.iterations
+    assert np.array_equal(a.state, b.state)
+
+
+def test_host_traffic_counts_c_rows_then_readback(monkeypatch):
+    args = CASES[0]
+    n, npts, m = 255, 1000, 8
+    g = _guess(args, n, seed=5)
+    d = _driver(args, g, monkeypatch)
+    h2d, d2h = d.host_traffic()
+    c_rows = len(range(m, npts, m))  # C points after point 0 (the IC)
+    assert (h2d, d2h) == (8 * n * c_rows, 0)
+    d.iterate(2)
+    assert d.host_traffic() == (8 * n * c_rows, 0)  # the cycles never needed the F rows
+    d.get_level(0)
+    assert d.host_traffic() == (8 * n * c_rows, 8 * n * npts)
+    e = _driver(args, g, monkeypatch, eager=True)
+    assert e.host_traffic() == (8 * n * (npts - 1), 0)
