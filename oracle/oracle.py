@@ -213,7 +213,10 @@ class Driver:
         it, conv = C.c_int(), C.c_int()
         st = lib().orc_drive(self.h, _ptr(hist), C.byref(it), C.byref(conv))
         if st not in (0, 1):
-            raise OracleError(st, lib().orc_error(self.h).decode())
+            err = OracleError(st, lib().orc_error(self.h).decode())
+            # completed iterations and their norms before the failing cycle
+            err.iterations, err.history = it.value, hist[: it.value].copy()
+            raise err
         return dict(iterations=it.value, converged=bool(conv.value),
                     history=hist[: it.value].copy())
 

@@ -1,0 +1,56 @@
+"""Device time to tolerance (1e-10) of BASELINE configs 1-3 at full size, one
+B200: iterations, setup-to-converged wall seconds, device ms per iteration.
+The oracle's iteration counts for configs 2 and 3 are in
+tests/golden/fullsize_config{2,3}.json (tests/test_gpu_fullsize.py checks).
+
+  python tools/fullsize_ttt.py [out.json]"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2107_09596_b200 as T  # noqa: E402
+
+
+def cases():
+    ic1 = np.sin(np.pi * np.arange(1, 64) / 64) + 0.1 * T.random_state(1, 63)
+    yield ("config1", T.Heat1D(63, folded=False, manufactured_forcing=False, initial_condition=ic1),
+           (0.0, 1.0, 1025, [16], 2), T.CycleMode.TwoLevel, T.Relaxation.FCF)
+    yield ("config2", T.Heat2D(127, folded=False, source=T.gaussian_source(127), cg_rtol=1e-12, cg_max=10000),
+           (0.0, 1.0, 4097, [16], 4), T.CycleMode.TwoLevel, T.Relaxation.F)
+    yield ("config3", T.AllenCahn(4096, 0.02, 1.0, 1e-12, 30, initial_condition=0.05 * T.random_state(3, 4096)),
+           (0.0, 8.0, 16385, [8, 8], 4), T.CycleMode.VCycle, T.Relaxation.F)
+
+
+def main():
+    out = []
+    for name, app, (t0, tf, npts, ms, k), mode, relax in cases():
+        hier = T.build_hierarchy(T.TimeGrid.make(t0, tf, npts), ms, k)
+        cfg = T.SolverConfig(mode=mode, relaxation=relax, max_iters=200, tol=1e-10,
+                             initial_guess=T.InitialGuess.Random, seed=20)
+        T.solve(app, hier, cfg)  # warm (module load, graphs)
+        drv = T.CycleDriver(app, hier, cfg)
+        w0 = time.perf_counter()
+        drv.setup()
+        rep = drv.drive()
+        wall = time.perf_counter() - w0
+        drv.close()
+        d2 = T.CycleDriver(app, hier, cfg)
+        d2.setup()
+        _, ms_dev = d2.iterate_timed(min(rep.iterations, 10))
+        d2.close()
+        rec = dict(config=name, iterations=rep.iterations, converged=rep.converged,
+                   setup_to_tol_seconds=wall, device_ms_per_iteration=ms_dev / min(rep.iterations, 10),
+                   last_norm=rep.residual_norms[-1])
+        print(json.dumps(rec), flush=True)
+        out.append(rec)
+    if len(sys.argv) > 1:
+        json.dump(out, open(sys.argv[1], "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
