@@ -5,7 +5,7 @@ count and residual history to tol 1e-10 and every SAMPLE-th level-0 row of
 its final state (the full state is 0.5 GB): tests/test_gpu_fullsize.py
 compares the device solve against them.
 
-  python tests/golden/make_fullsize.py {2,3} [random|constant]
+  python tests/golden/make_fullsize.py {2,3} [random|constant] [newton_tol (config 3, default 1e-12)]
 
 Config definitions follow DESIGN.md section 9 (pinned choices)."""
 from __future__ import annotations
@@ -33,7 +33,7 @@ def gaussian_source(nx):
     return T.gaussian_source(nx)
 
 
-def config(c, guess="random"):
+def config(c, guess="random", newton_tol=1e-12):
     if c == 2:
         nx = 127
         return (dict(kind=O.HEAT2D, n=nx * nx, nx=nx, folded=0, source=gaussian_source(nx), ic=None,
@@ -43,7 +43,7 @@ def config(c, guess="random"):
                      initial_guess=O.GUESS_RANDOM, seed=20))
     if c == 3:
         n = 4096
-        return (dict(kind=O.ALLEN_CAHN, n=n, eps=0.02, length=1.0, newton_tol=1e-12, newton_max=30,
+        return (dict(kind=O.ALLEN_CAHN, n=n, eps=0.02, length=1.0, newton_tol=newton_tol, newton_max=30,
                      folded=1, ic=0.05 * O.random_state(3, n)),
                 dict(tf=8.0, n_points=16385, m=[8, 8], k=4),
                 dict(mode=O.VCYCLE, relaxation=O.RELAX_F, max_iters=200, tol=TOL,
@@ -55,11 +55,12 @@ def config(c, guess="random"):
 def main():
     c = int(sys.argv[1])
     guess = sys.argv[2] if len(sys.argv) > 2 else "random"
-    tag = f"config{c}" + ("" if guess == "random" else f"_{guess}")
-    p, g, s = config(c, guess)
+    ntol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-12
+    tag = f"config{c}" + ("" if guess == "random" else f"_{guess}") + ("" if ntol == 1e-12 else f"_newton{ntol:g}")
+    p, g, s = config(c, guess, ntol)
     t0 = time.time()
     d = O.Driver(p, g, s)
-    meta = dict(config=c, guess=guess, tol=TOL, sample_every=SAMPLE[c])
+    meta = dict(config=c, guess=guess, tol=TOL, newton_tol=ntol, sample_every=SAMPLE[c])
     try:
         res = d.drive()
     except O.OracleError as e:

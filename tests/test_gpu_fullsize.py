@@ -30,13 +30,13 @@ def _fixture(tag):
     return meta, (np.load(rows) if os.path.exists(rows) else None)
 
 
-def _objects(c, tol, guess="random"):
+def _objects(c, tol, guess="random", newton_tol=1e-12):
     if c == 2:
         app = T.Heat2D(127, folded=False, source=T.gaussian_source(127), cg_rtol=1e-12, cg_max=10000)
         hier = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, 4097), [16], 4)
         mode = T.CycleMode.TwoLevel
     else:
-        app = T.AllenCahn(4096, 0.02, 1.0, 1e-12, 30,
+        app = T.AllenCahn(4096, 0.02, 1.0, newton_tol, 30,
                           initial_condition=0.05 * T.random_state(3, 4096))
         hier = T.build_hierarchy(T.TimeGrid.make(0.0, 8.0, 16385), [8, 8], 4)
         mode = T.CycleMode.VCycle
@@ -53,7 +53,8 @@ TAGS = sorted(f[len("fullsize_"):-len(".json")] for f in os.listdir(GOLDEN)
 @pytest.mark.parametrize("tag", TAGS)
 def test_full_size_config_matches_oracle(tag):
     meta, rows = _fixture(tag)
-    app, hier, cfg = _objects(meta["config"], meta["tol"], meta.get("guess", "random"))
+    app, hier, cfg = _objects(meta["config"], meta["tol"], meta.get("guess", "random"),
+                              meta.get("newton_tol", 1e-12))
     if "failed_at_iteration" in meta:
         # the oracle's Newton hit its cap (NonlinearSolveError, gray_scott.cpp:
         # 165-169): the device must fail in the same cycle, after the same history
