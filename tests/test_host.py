@@ -211,3 +211,26 @@ def test_direct_window_schedule_delivers_the_two_round_set(n_points, m, k, worke
         assert want[r] <= have
         # nothing beyond the windows is moved
         assert have - set(range(lay.coarse_lo[r], lay.coarse_hi[r] + 1)) <= want[r]
+
+
+def test_fullsize_fixtures_are_consistent():
+    """tests/golden/fullsize_*.json (oracle runs at BASELINE sizes): histories,
+    iteration counts, failure cycles and sampled-row shapes agree."""
+    import glob
+    import json
+    import os
+
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    metas = sorted(glob.glob(os.path.join(gold, "fullsize_*.json")))
+    assert metas
+    for p in metas:
+        meta = json.load(open(p))
+        hist = meta["history"]
+        if "failed_at_iteration" in meta:
+            assert meta["code"] == 5 and len(hist) == meta["failed_at_iteration"] - 1
+            continue
+        assert meta["converged"] and meta["iterations"] == len(hist)
+        assert hist[-1] <= meta["tol"] < min(hist[:-1])
+        rows = np.load(p[:-5] + "_rows.npy")
+        npts, n = {2: (4097, 127 * 127), 3: (16385, 4096)}[meta["config"]]
+        assert rows.shape == (len(range(0, npts, meta["sample_every"])), n)
