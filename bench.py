@@ -13,9 +13,17 @@ n x 2 x F_0 per iteration (F_0 = 245760 fine F-points).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Multi-GPU: launched by torchrun, one process per GPU, time shards of the
-reference rank layout; NCCL (from the C++ runtime) moves halo rows, window
-payloads and the norm squares; gloo only broadcasts the NCCL id.
+Multi-GPU: one process per GPU, time shards of the reference rank layout;
+NCCL (from the C++ runtime) moves halo rows, window payloads and the norm
+squares; gloo only broadcasts the NCCL id.  Under torchrun WORLD_SIZE must
+equal --gpus; without a launcher, --gpus N > 1 re-launches itself through
+torch.distributed.run with N local ranks.
+
+CPU reference arm (--impl reference, and the cpu_baseline leg): the
+reference's own CPU solver compiled from its sources (oracle/_ref/tempo_ref,
+runtime::run_parallel over the host's threads) on the SAME workload (N_t =
+2^18), W untimed + K timed iterations, seconds per iteration from the
+reference's own ConvergenceReport::iteration_seconds (solver.cpp:414-416).
 """
 from __future__ import annotations
 
@@ -36,9 +44,6 @@ sys.path.insert(0, ROOT)
 
 WORKLOAD = dict(name="config5_heat1d_n4095_Nt2^18_m16_k8", n=4095, n_points=2 ** 18 + 1, m=16, k=8,
                 tf=1.0, u0_seed=7, guess_seed=20, tol=1e-10)
-# bounded CPU sample of the same workload (same n, m, k, dt-per-level shape at
-# reduced N_t): the reference's own CPU implementation on the host cores
-CPU_SAMPLE = dict(n=4095, n_points=2 ** 14 + 1, m=16, k=8, tf=1.0 / 16)
 
 
 def level0_counts(n_points, m):
@@ -113,26 +118,45 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_run(iters, workers=None, sample=CPU_SAMPLE):
-    """Time the compiled reference (oracle/_ref/tempo_ref) on the bounded sample."""
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_reference_run(warmup, steps, W, workers=None):
+    """The compiled reference (oracle/_ref/tempo_ref: the reference's own
+    solver sources, run_parallel) on the bench workload itself: `warmup`
+    untimed + `steps` timed iterations; seconds per iteration from the
+    reference's ConvergenceReport::iteration_seconds.  The C restatement
+    (oracle/) stands in, single-threaded, only if the binary is missing."""
     from oracle import oracle as O
-    n = sample["n"]
+    n, npts = W["n"], W["n_points"]
     nproc = os.cpu_count() or 1
-    nc = (sample["n_points"] - 1) // sample["m"] + 1
-    workers = workers or min(nproc, nc)
-    args = dict(problem="heat1d", n=n, tf=sample["tf"], n_points=sample["n_points"], m=sample["m"],
-                k=sample["k"], manufactured=0, guess="random", seed=20, timing_iters=iters,
-                workers=workers, driver="parallel")
-    ic = O.random_state(7, n)
+    nc = (npts - 1) // W["m"] + 1
+    workers = min(workers or nproc, nc)
+    iters = warmup + steps
+    ic = O.random_state(W["u0_seed"], n)
+    t0 = time.perf_counter()
     if O.ref_available():
-        res, _ = O.run_ref(args, files={"ic_file": ic}, timeout=3600)
-        kind = "reference"
-        secs = res["iteration_seconds"]
+        args = dict(problem="heat1d", n=n, tf=W["tf"], n_points=npts, m=W["m"], k=W["k"], manufactured=0,
+                    guess="random", seed=W["guess_seed"], timing_iters=iters, workers=workers,
+                    driver="parallel")
+        res, _ = O.run_ref(args, files={"ic_file": ic}, timeout=7200)
+        if "error" in res:
+            raise RuntimeError(f"reference run failed: {res}")
+        kind, secs, setup = "reference", res["iteration_seconds"], res["timings"].get("setup")
     else:  # the C restatement, single thread
         drv = O.Driver(dict(kind=O.HEAT1D, n=n, manufactured=0, ic=ic),
-                       dict(tf=sample["tf"], n_points=sample["n_points"], m=sample["m"], k=sample["k"]),
-                       dict(tol=1e-300, max_iters=iters, initial_guess=O.GUESS_RANDOM, seed=20))
+                       dict(tf=W["tf"], n_points=npts, m=W["m"], k=W["k"]),
+                       dict(tol=1e-300, max_iters=iters, initial_guess=O.GUESS_RANDOM, seed=W["guess_seed"]))
+        t = time.perf_counter()
         drv.setup()
+        setup = time.perf_counter() - t
         secs = []
         for _ in range(iters):
             t = time.perf_counter()
@@ -140,12 +164,15 @@ def cpu_reference_run(iters, workers=None, sample=CPU_SAMPLE):
             drv.residual_norm()
             secs.append(time.perf_counter() - t)
         kind, workers = "port", 1
-    per_iter = float(np.mean(secs))
-    value = dof_steps_per_iter(n, sample["n_points"], sample["m"]) / per_iter
-    desc = (f"config-5 shape (n={n}, m={sample['m']}, k={sample['k']}) at N_t={sample['n_points'] - 1}, "
-            f"{iters} iterations, reference run_parallel with {workers} threads")
+    timed = secs[warmup:] or secs
+    per_iter = float(np.mean(timed))
+    value = dof_steps_per_iter(n, npts, W["m"]) / per_iter
+    desc = (f"the bench workload itself (heat1d n={n}, N_t={npts - 1}, m={W['m']}, k={W['k']}): "
+            f"{warmup} untimed + {len(timed)} timed iterations of the reference's run_parallel "
+            f"with {workers} threads")
     return dict(value=value, unit="DOF*steps/s", cores=workers, kind=kind, sample=desc,
-                seconds_per_iteration=per_iter, seconds=secs)
+                seconds_per_iteration=per_iter, seconds=secs, setup_seconds=setup,
+                wall_seconds=time.perf_counter() - t0, cpu_model=cpu_model(), host_threads=nproc)
 
 
 def dist_env():
@@ -160,9 +187,10 @@ def time_to_tolerance(T):
     m=16, k=8, u0 = random_state(7, n), guess seed 20), wall clock with the
     device synchronised (atm_solve reads each iteration's norm back)."""
     n, npts = 4095, 2 ** 14 + 1
-    ref_it = None
+    ref_it = ref_s = None
     try:
-        ref_it = json.load(open(os.path.join(ROOT, "tests", "golden", "cases.json")))["config5r_k8"]["iterations"]
+        case = json.load(open(os.path.join(ROOT, "tests", "golden", "cases.json")))["config5r_k8"]
+        ref_it, ref_s = case["iterations"], case["ref_seconds"]
     except Exception:
         pass
     app = T.Heat1D(n, manufactured_forcing=False, initial_condition=T.random_state(7, n))
@@ -197,6 +225,7 @@ def time_to_tolerance(T):
                for r in (rep2, rep3))
     return {"config": "config5r: heat1d n=4095, N_t=2^14, t in [0,1], m=16, k=8, tol 1e-10",
             "iterations": res.report.iterations, "reference_iterations": ref_it,
+            "reference_seconds_fixture": ref_s,
             "converged": bool(res.report.converged), "seconds": wall,
             "setup_to_tol_seconds": s2t,
             "drive_seconds": d1, "drive_seconds_reuse_relax": d2,
@@ -205,7 +234,9 @@ def time_to_tolerance(T):
             "what": "seconds: wall clock of solve() (context + device arrays, setup, drive to tol with "
                     "one norm readback per iteration, level-0 state read back); setup_to_tol_seconds: "
                     "atm_setup to the converged iteration (SURVEY 8(d)); drive_seconds: the "
-                    "iterations alone, without and with the opt-ins (relax reuse; relax reuse + C-point storage)"}
+                    "iterations alone, without and with the opt-ins (relax reuse; relax reuse + C-point storage); "
+                    "reference_seconds_fixture: the compiled reference's solve of the same case when its "
+                    "fixture was written (tests/golden/cases.json; dev container, 8 threads)"}
 
 
 def time_to_tolerance_full(T, W, name, app, hier, dev, world, rank, nccl_id, pg):
@@ -255,6 +286,18 @@ def main():
     ap.add_argument("--m", type=int, default=WORKLOAD["m"])
     args = ap.parse_args()
     world, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # no launcher: one process per GPU through torch.distributed.run
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+               os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
     W = dict(WORKLOAD, n_points=args.n_points, k=args.k, m=args.m)
     n = W["n"]
     unit = "DOF*steps/s"
@@ -269,22 +312,20 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        r = cpu_reference_run(args.warmup + args.steps)
-        secs = r["seconds"][args.warmup:] or r["seconds"]
-        per = float(np.mean(secs))
-        value = dof_steps_per_iter(n, CPU_SAMPLE["n_points"], CPU_SAMPLE["m"]) / per
+        r = cpu_reference_run(args.warmup, args.steps, W)
+        value, per = r["value"], r["seconds_per_iteration"]
         line = {"impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": dict(config, sample=r["sample"]),
+                "data": "synthetic (seeded splitmix64 u0 and initial guess)", "config": config,
                 "cpu_baseline": {"value": value, "unit": unit, "cores": r["cores"], "kind": r["kind"],
-                                 "sample": r["sample"]},
+                                 "sample": r["sample"], "cpu_model": r["cpu_model"],
+                                 "host_threads": r["host_threads"], "setup_seconds": r["setup_seconds"]},
                 "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
 
     import paper_2107_09596_b200 as T
-    from oracle import oracle as O  # noqa: F401  (input generation only: random_state)
 
     nccl_id = None
     pg = None
@@ -390,7 +431,9 @@ def main():
         cfg2 = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=1e-300,
                               max_iters=args.steps, initial_guess=T.InitialGuess.Provided,
                               provided=guess)
-        drv2 = T.CycleDriver(app, hier, cfg2, device=dev,
+        # defer_guess: atm_setup sends the guess's C rows; its F rows are dead
+        # under cycling (rewritten before any read), so they never move
+        drv2 = T.CycleDriver(app, hier, cfg2, device=dev, defer_guess=True,
                              world_size=world, rank=rank, nccl_id=nccl_id)
         if pg:
             pg.barrier()
@@ -445,15 +488,24 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cb = cpu_reference_run(3)
+            # the same workload and warm-up rule as --impl reference (1 + 2
+            # iterations on all host threads), and one single-thread iteration
+            cb = cpu_reference_run(1, 2, W)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-            if ttt and "iterations" in ttt:
-                # same N_t = 2^14 sizes: reference seconds per iteration x its iteration count
-                ttt["reference_seconds_estimate"] = cb["seconds_per_iteration"] * ttt["reference_iterations"]
+            line["cpu_baseline"].update(cpu_model=cb["cpu_model"], host_threads=cb["host_threads"],
+                                        seconds_per_iteration=cb["seconds_per_iteration"],
+                                        setup_seconds=cb["setup_seconds"])
+            try:
+                c1 = cpu_reference_run(0, 1, W, workers=1)
+                line["cpu_baseline"]["single_thread"] = {
+                    "value": c1["value"], "seconds_per_iteration": c1["seconds_per_iteration"],
+                    "setup_seconds": c1["setup_seconds"], "sample": c1["sample"]}
+            except Exception as e:  # reported, not fatal
+                line["cpu_baseline"]["single_thread"] = {"unavailable": str(e)}
             if ttf and "iterations" in ttf:
-                # full size: the sample's rate over the workload's DOF*steps per iteration
-                ttf["reference_seconds_estimate"] = (dof_steps_per_iter(n, W["n_points"], W["m"]) /
-                                                     cb["value"] * ttf["iterations"])
+                # measured reference seconds per iteration (this workload, all
+                # host threads) x the iterations the solve needs
+                ttf["reference_seconds_estimate"] = cb["seconds_per_iteration"] * ttf["iterations"]
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "unit": unit, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define ATM_ABI_VERSION 5
+#define ATM_ABI_VERSION 6
 #define ATM_MAX_LEVELS 8
 
 typedef enum {
@@ -50,6 +50,10 @@ typedef enum { ATM_RELAX_F = 0, ATM_RELAX_FCF = 1 } atm_relaxation;             
 typedef enum { ATM_NORM_L2 = 0, ATM_NORM_FUNCTIONAL = 1 } atm_norm;              /* NormKind    */
 typedef enum { ATM_GUESS_CONSTANT = 0, ATM_GUESS_RANDOM = 1, ATM_GUESS_PROVIDED = 2 } atm_guess;
 typedef enum { ATM_STORE_FULL = 0, ATM_STORE_CPOINTS = 1 } atm_storage;
+/* FunctionalChange functional f(u) (SolverConfig::functional, solver_config.hpp:43):
+ * LINEAR = w.u with functional_w; NORM2 = u.norm2() (state_vector.hpp:61-67),
+ * the reference CLI's functional (run_config.cpp:241-243). */
+typedef enum { ATM_FUNCTIONAL_LINEAR = 0, ATM_FUNCTIONAL_NORM2 = 1 } atm_functional;
 
 /* Problem descriptor: replaces the Application subclass (application.hpp:33). */
 typedef struct atm_problem {
@@ -93,16 +97,15 @@ typedef struct atm_solver {
     int mode, relaxation, nu, max_iters;
     double tol;
     int norm;
-    const double* functional_w; /* FunctionalChange: linear functional w.u        */
+    const double* functional_w; /* FunctionalChange, LINEAR: weights w (n values)  */
     int initial_guess;
     uint64_t seed;
     const double* constant_value; /* n values or NULL (=> initial condition)       */
     const double* provided;       /* n_points*n values (InitialGuess::Provided);   *
-                                   * caller-owned, must stay valid until the first  *
-                                   * cycle (atm_cycle / atm_solve / atm_iterate)    *
-                                   * returns: setup sends the C rows, the F rows    *
-                                   * are read only if needed before that cycle      */
+                                   * copied by atm_setup, unless                    *
+                                   * atm_runtime.defer_guess (see there)            */
     int coarse_substeps;
+    int functional_kind;          /* atm_functional (FunctionalChange norm only)   */
 } atm_solver;
 
 /* Execution / runtime options (replaces SequentialExecution and
@@ -118,6 +121,17 @@ typedef struct atm_runtime {
     int reuse_relax;   /* two-level F-relaxation: skip a cycle's opening F-sweep,
                           whose results the previous correction F-sweep already
                           produced (bitwise the same cycle; opt-in)                */
+    int defer_guess;   /* 1: atm_setup sends only the C rows of a provided guess;
+                          its F rows are dead under cycling (every cycle rewrites
+                          them before reading one) and are copied only if read
+                          first (residual norm, level-0 access, kernel entry
+                          points, nested init).  The caller's `provided` buffer
+                          must then stay valid until the first cycle returns.
+                          0 (default): atm_setup copies the whole guess.        */
+    int timeout_ms;    /* world_size > 1: an exchange or collective that has not
+                          completed after this long aborts the communicator and
+                          fails with ATM_RUNTIME_FAULT (ParallelOptions::timeout,
+                          parallel.hpp:15; transport.cpp:29-48).  0 = 30000.    */
 } atm_runtime;
 
 /* ConvergenceReport (solver_config.hpp:57-64). */
@@ -125,8 +139,9 @@ typedef struct atm_report {
     int iterations;
     int converged;
     int stop_reason;   /* 0 converged, 1 max iterations, 2 diverged                */
-    double total_seconds;
+    double total_seconds;  /* timings["total"]: setup + nested init + iterations   */
     double dof_steps;  /* n x relaxation Phi applications performed (all levels)   */
+    double setup_seconds;  /* timings["setup"] (solver.cpp:403-407)                */
 } atm_report;
 
 typedef struct atm_ctx atm_ctx;
@@ -151,9 +166,12 @@ atm_status atm_nested_init(atm_ctx* ctx);
 atm_status atm_cycle(atm_ctx* ctx);
 /* CycleDriver::residual_norm (solver.cpp:370-378) */
 atm_status atm_residual_norm(atm_ctx* ctx, double* out);
-/* CycleDriver::drive / solve() (solver.cpp:398-435, :485-492); norms[] gets
- * one entry per iteration (capacity max_iters), may be NULL. */
-atm_status atm_solve(atm_ctx* ctx, atm_report* report, double* norms);
+/* CycleDriver::drive / solve() (solver.cpp:398-435, :485-492): the
+ * ConvergenceReport (solver_config.hpp:57-64).  norms[] (residual_norms) and
+ * iteration_seconds[] (wall time of each cycle + stopping norm) get one entry
+ * per iteration (capacity max_iters); either may be NULL.  Per-phase times
+ * (ConvergenceReport::timings) come from atm_phase_times. */
+atm_status atm_solve(atm_ctx* ctx, atm_report* report, double* norms, double* iteration_seconds);
 /* Fixed-count cycles with one stopping norm each, no host sync in between
  * except the norm readback (bench helper; same arithmetic as atm_solve). */
 atm_status atm_iterate(atm_ctx* ctx, int count, double* norms);
@@ -181,9 +199,11 @@ atm_status atm_kernel_c_relax(atm_ctx* ctx, int level, int first_c, int count);
 atm_status atm_kernel_residual(atm_ctx* ctx, int level, int first, int count,
                                double* host_out);
 
-/* Per-phase device timings accumulated since setup (PhaseTimer,
- * solver.cpp:11-28): names "relax","restrict","coarse","correct","norm".
- * Returns the number of phases written (<= cap). */
+/* Per-phase timings accumulated since creation (PhaseTimer, solver.cpp:11-28;
+ * ConvergenceReport::timings): always "setup" and "iterations" (host wall
+ * clock); with atm_runtime.trace also the device-event phases "relax",
+ * "restrict", "exchange", "coarse", "correct", "norm" (and the level-0 sweep
+ * kernels "sweep_relax", "sweep_correct").  Returns the number written (<= cap). */
 int atm_phase_times(const atm_ctx* ctx, char* names_csv, int names_cap, double* seconds,
                     int cap);
 
@@ -231,8 +251,9 @@ atm_status atm_rank_ranges(const atm_grid* grid, int workers, int rank, int* lo,
 
 /* Window payload schedule that replaces the two-round group exchange
  * (parallel.cpp:134-194): rank `rank` needs coarsest indices
- * [need_lo, c_lo-1] from its left; returns the count of (src_rank, first,
- * count) triples written to `sends` (capacity cap triples). */
+ * [need_lo, c_lo-1] from its left; returns the total count of (src_rank,
+ * first, count) triples (at most `workers`); min(total, cap) are written to
+ * `sends` (capacity cap triples). */
 int atm_window_recvs(const atm_grid* grid, int workers, int rank, int* sends, int cap);
 
 /* NCCL unique id for multi-process runs (128 bytes); ATM_RUNTIME_FAULT if

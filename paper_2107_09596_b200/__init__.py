@@ -7,7 +7,7 @@ reference-shaped Python binding used by tests and the benchmark.
 from .api import (  # noqa: F401
     AllenCahn, Application, ConfigError, ConvergenceReport, CycleDriver, CycleMode, Dahlquist,
     DivergenceError, GrayScott, Heat1D, Heat2D, Hierarchy, InitialGuess, NonlinearSolveError, NormKind,
-    Relaxation, RuntimeFault, ScalarLinear, SolveResult, SolverConfig, StopReason, TimeGrid,
+    Relaxation, RuntimeFault, ScalarLinear, SolveResult, SolverConfig, StopReason, TempoError, TimeGrid,
     allen_cahn_ic, build_comm_groups, build_hierarchy, build_layout, fourier_ic, gaussian_source,
     make_cf_split, random_state,
     rank_ranges, run_parallel, solve, window_recvs,

@@ -11,6 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ATM_LIB") or os.path.join(HERE, "libatmgrit.so")
 MAXL = 8
+ABI_VERSION = 6  # include/atmgrit.h ATM_ABI_VERSION: the structs below are its layout
 _DP = C.POINTER(C.c_double)
 _IP = C.POINTER(C.c_int)
 
@@ -42,18 +43,21 @@ class atm_solver(C.Structure):
     _fields_ = [("mode", C.c_int), ("relaxation", C.c_int), ("nu", C.c_int),
                 ("max_iters", C.c_int), ("tol", C.c_double), ("norm", C.c_int),
                 ("functional_w", _DP), ("initial_guess", C.c_int), ("seed", C.c_uint64),
-                ("constant_value", _DP), ("provided", _DP), ("coarse_substeps", C.c_int)]
+                ("constant_value", _DP), ("provided", _DP), ("coarse_substeps", C.c_int),
+                ("functional_kind", C.c_int)]
 
 
 class atm_runtime(C.Structure):
     _fields_ = [("device", C.c_int), ("n_shards", C.c_int), ("world_size", C.c_int),
                 ("rank", C.c_int), ("nccl_id", C.c_void_p), ("storage", C.c_int),
-                ("trace", C.c_int), ("reuse_relax", C.c_int)]
+                ("trace", C.c_int), ("reuse_relax", C.c_int), ("defer_guess", C.c_int),
+                ("timeout_ms", C.c_int)]
 
 
 class atm_report(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("stop_reason", C.c_int),
-                ("total_seconds", C.c_double), ("dof_steps", C.c_double)]
+                ("total_seconds", C.c_double), ("dof_steps", C.c_double),
+                ("setup_seconds", C.c_double)]
 
 
 # exported symbol -> (restype, argtypes); the authoritative list is atmgrit.h
@@ -69,7 +73,7 @@ SIGNATURES = {
     "atm_nested_init": (C.c_int, [C.c_void_p]),
     "atm_cycle": (C.c_int, [C.c_void_p]),
     "atm_residual_norm": (C.c_int, [C.c_void_p, _DP]),
-    "atm_solve": (C.c_int, [C.c_void_p, C.POINTER(atm_report), _DP]),
+    "atm_solve": (C.c_int, [C.c_void_p, C.POINTER(atm_report), _DP, _DP]),
     "atm_iterate": (C.c_int, [C.c_void_p, C.c_int, _DP]),
     "atm_get_level": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _DP]),
     "atm_set_level": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _DP]),
@@ -116,6 +120,9 @@ def lib():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if L.atm_abi_version() != ABI_VERSION:
+            raise LibraryMissing(f"{LIB_PATH} has ABI {L.atm_abi_version()}, these bindings expect "
+                                 f"{ABI_VERSION}: rebuild it")
         _lib = L
     return _lib
 

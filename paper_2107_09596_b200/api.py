@@ -211,7 +211,9 @@ class SolverConfig:
     max_iters: int = 100
     tol: float = 1e-7
     norm: NormKind = NormKind.ResidualL2
-    functional: Optional[np.ndarray] = None  # linear functional weights w (w . u)
+    # FunctionalChange functional f(u): weights w of a linear functional w . u,
+    # or the string "norm2" for u.norm2() (the reference CLI's, run_config.cpp:241-243)
+    functional: Optional[object] = None
     initial_guess: InitialGuess = InitialGuess.Constant
     seed: int = 0
     constant_value: Optional[np.ndarray] = None
@@ -228,6 +230,7 @@ class ConvergenceReport:
     total_seconds: float = 0.0
     dof_steps: float = 0.0
     timings: dict = dataclasses.field(default_factory=dict)
+    iteration_seconds: list = dataclasses.field(default_factory=list)
 
 
 # ---------------------------------------------------------------------------
@@ -488,7 +491,7 @@ class CycleDriver:
     def __init__(self, app: Application, hier: Hierarchy, cfg: SolverConfig, workers: int = 1,
                  device: int = 0, trace: bool = False, world_size: int = 1, rank: int = 0,
                  nccl_id: Optional[bytes] = None, reuse_relax: bool = False,
-                 cpoint_storage: bool = False):
+                 cpoint_storage: bool = False, defer_guess: bool = False, timeout_ms: int = 0):
         self.app, self.hier, self.cfg = app, hier, cfg
         self._keep = []
         p = app.c_problem(self._keep)
@@ -498,7 +501,12 @@ class CycleDriver:
         s.max_iters, s.tol, s.norm = cfg.max_iters, cfg.tol, int(cfg.norm)
         s.initial_guess, s.seed, s.coarse_substeps = int(cfg.initial_guess), cfg.seed, cfg.coarse_substeps
         n = app.vector_size()
-        for field, val in (("functional_w", cfg.functional), ("constant_value", cfg.constant_value),
+        functional = cfg.functional
+        if isinstance(functional, str):
+            if functional != "norm2":
+                raise ConfigError(f"unknown functional {functional!r} (weights or 'norm2')")
+            s.functional_kind, functional = 1, None  # ATM_FUNCTIONAL_NORM2
+        for field, val in (("functional_w", functional), ("constant_value", cfg.constant_value),
                            ("provided", cfg.provided)):
             if val is not None:
                 a = np.ascontiguousarray(val, np.float64).reshape(-1)
@@ -511,6 +519,8 @@ class CycleDriver:
         rt.trace = int(trace)
         rt.reuse_relax = int(reuse_relax)
         rt.storage = int(bool(cpoint_storage))  # ATM_STORE_CPOINTS
+        rt.defer_guess = int(bool(defer_guess))
+        rt.timeout_ms = int(timeout_ms)
         if nccl_id is not None:
             self._nid = C.create_string_buffer(bytes(nccl_id), 128)
             rt.nccl_id = C.cast(self._nid, C.c_void_p)
@@ -552,15 +562,18 @@ class CycleDriver:
 
     def drive(self) -> ConvergenceReport:
         norms = np.zeros(self.cfg.max_iters, np.float64)
+        secs = np.zeros(self.cfg.max_iters, np.float64)
         rep = _capi.atm_report()
-        st = lib().atm_solve(self._h, C.byref(rep), ptr(norms))
+        st = lib().atm_solve(self._h, C.byref(rep), ptr(norms), ptr(secs))
         if st == 4:
             msg = lib().atm_last_error(self._h).decode()
             raise DivergenceError(rep.iterations, msg)
         self._check(st)
+        t = self.timings()
+        t["total"] = rep.total_seconds
         return ConvergenceReport(list(norms[: rep.iterations]), rep.iterations, bool(rep.converged),
-                                 StopReason(rep.stop_reason), rep.total_seconds, rep.dof_steps,
-                                 self.timings())
+                                 StopReason(rep.stop_reason), rep.total_seconds, rep.dof_steps, t,
+                                 list(secs[: rep.iterations]))
 
     def iterate(self, count: int) -> np.ndarray:
         norms = np.zeros(count, np.float64)
@@ -748,11 +761,14 @@ def rank_ranges(hier: Hierarchy, workers: int, rank: int) -> dict:
 
 def window_recvs(hier: Hierarchy, workers: int, rank: int) -> list:
     g = hier.c_grid()
-    buf = (C.c_int * (3 * 64))()
-    n = lib().atm_window_recvs(C.byref(g), workers, rank, buf, 64)
+    cap = max(1, workers)  # at most one (src, first, count) triple per other rank
+    buf = (C.c_int * (3 * cap))()
+    n = lib().atm_window_recvs(C.byref(g), workers, rank, buf, cap)
     if n < 0:
         _raise(2, lib().atm_create_error().decode())
-    return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(min(n, 64))]
+    if n > cap:
+        raise RuntimeFault(f"window schedule has {n} sends, more than the {cap} ranks")
+    return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n)]
 
 
 def build_comm_groups(n_coarse_points: int, k: int):

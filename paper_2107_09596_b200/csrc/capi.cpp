@@ -1,6 +1,7 @@
 // capi.cpp -- extern "C" boundary (include/atmgrit.h) over atm::Engine.
 // Every exception is mapped to an atm_status (errors.hpp:9-42 taxonomy).
 #include <cstring>
+#include <memory>
 #include <string>
 
 #include "atmgrit.h"
@@ -55,9 +56,11 @@ atm_status atm_create(const atm_problem* problem, const atm_grid* grid, const at
     atm_runtime rt{};
     if (runtime) rt = *runtime;
     try {
-        auto* c = new atm_ctx();
-        c->eng.reset(new atm::Engine(*problem, *grid, *solver, rt));
-        *out = c;
+        // the context is released to the caller only once the engine exists
+        // (a ConfigError or CUDA fault in the constructor frees it here)
+        auto c = std::make_unique<atm_ctx>();
+        c->eng = std::make_unique<atm::Engine>(*problem, *grid, *solver, rt);
+        *out = c.release();
         g_create_err.clear();
         return ATM_OK;
     } catch (const atm::Error& e) {
@@ -89,8 +92,8 @@ atm_status atm_residual_norm(atm_ctx* c, double* out) {
     return guard(c, [&] { *out = c->eng->residual_norm(); return 0; });
 }
 
-atm_status atm_solve(atm_ctx* c, atm_report* rep, double* norms) {
-    return guard(c, [&] { return c->eng->solve(rep, norms); });
+atm_status atm_solve(atm_ctx* c, atm_report* rep, double* norms, double* iteration_seconds) {
+    return guard(c, [&] { return c->eng->solve(rep, norms, iteration_seconds); });
 }
 
 atm_status atm_iterate(atm_ctx* c, int count, double* norms) {

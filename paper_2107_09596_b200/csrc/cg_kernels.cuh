@@ -48,7 +48,7 @@ struct CgSweepArgs {
     const double* g; int g_base; int add_g;
     int forced, store, tail;
     double* out; int out_base;
-    double* sq; int sq_base;
+    double* sq; int sq_base; int sq_div;  // squares at (tail point - sq_base) / sq_div
     int u_div;  // > 1: C-point-only u array
 };
 

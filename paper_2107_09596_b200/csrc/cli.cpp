@@ -249,10 +249,9 @@ Built build(const Config& c, const std::vector<int>& m, int k, int workers) {
     if (norm == "residual-2norm") {
         b.s.norm = ATM_NORM_L2;
     } else if (norm == "functional-change") {
-        // the reference's CLI functional is u.norm2(); the GPU path takes a
-        // linear functional w.u -- not the same quantity
-        throw ConfigErr("config: solver.norm = functional-change (u.norm2) is not available on the "
-                        "GPU path; use residual-2norm");
+        // the reference CLI's functional is u.norm2() (run_config.cpp:241-243)
+        b.s.norm = ATM_NORM_FUNCTIONAL;
+        b.s.functional_kind = ATM_FUNCTIONAL_NORM2;
     } else {
         throw ConfigErr("config: solver.norm must be residual-2norm or functional-change");
     }

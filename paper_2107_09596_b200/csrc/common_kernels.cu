@@ -1,5 +1,6 @@
 // common_kernels.cu -- seeded fills, row arithmetic, deterministic norm
 // reduction, and the scalar (n = 1) Phi backend.
+#include <algorithm>
 #include <climits>
 #include <cmath>
 
@@ -172,46 +173,46 @@ int launch_norm_from_squares(const double* sq, int count, double* out, cudaStrea
     return static_cast<int>(cudaGetLastError());
 }
 
-__device__ double dot_w(const double* w, const double* u, int n) {
-    double s = 0.0;
-    for (int q = 0; q < n; ++q) s += w[q] * u[q];
-    return s;
-}
-
 __global__ void functional_kernel(const double* u, int u_base, int m, int pitch, int n,
-                                  const double* w, double* prev, int j0, int j1, double* out_max,
-                                  int init) {
-    // one thread per C-point; sequential dot in index order (functional_w . u)
-    __shared__ double red[256];
-    double local = 0.0;
-    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-        const double val = dot_w(w, u + static_cast<size_t>(j * m - u_base) * pitch, n);
-        if (!init) {
-            const double p = prev[j];
-            const double denom = fmax(fabs(p), 1e-300);
-            local = fmax(local, fabs(val - p) / denom);
+                                  const double* w, double* prev, int j0, int j1,
+                                  unsigned long long* out_max, int init) {
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int j = j0 + blockIdx.x * wpb + (threadIdx.x >> 5); j < j1; j += gridDim.x * wpb) {
+        const double* row = u + static_cast<size_t>(j * m - u_base) * pitch;
+        // lane-strided partial sums in index order, then a fixed xor tree:
+        // deterministic, the same for any grid or shard count
+        double s = 0.0;
+        if (w) {
+            for (int q = lane; q < n; q += 32) s = __dadd_rn(s, __dmul_rn(w[q], row[q]));
+        } else {
+            for (int q = lane; q < n; q += 32) s = __dadd_rn(s, __dmul_rn(row[q], row[q]));
         }
-        prev[j] = val;
-    }
-    red[threadIdx.x] = local;
-    __syncthreads();
-    if (threadIdx.x == 0 && !init) {
-        double mx = 0.0;
-        for (int i = 0; i < static_cast<int>(blockDim.x); ++i) mx = fmax(mx, red[i]);
-        out_max[0] = mx;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+        const double val = w ? s : sqrt(s);
+        if (lane == 0) {
+            if (!init) {
+                const double p = prev[j];
+                const double rel = fabs(val - p) / fmax(fabs(p), 1e-300);
+                // rel >= 0: the bit pattern orders like the value (+inf last)
+                if (rel > 0.0) atomicMax(out_max, static_cast<unsigned long long>(__double_as_longlong(rel)));
+            }
+            prev[j] = val;
+        }
     }
 }
 
-int launch_functional_change(const double* u, int u_base, int m, int pitch, int n,
-                             const double* w, double* prev, int j0, int j1, double* out_max,
-                             cudaStream_t s) {
-    functional_kernel<<<1, 256, 0, s>>>(u, u_base, m, pitch, n, w, prev, j0, j1, out_max, 0);
-    return static_cast<int>(cudaGetLastError());
-}
-
-int launch_functional_init(const double* u, int u_base, int m, int pitch, int n,
-                           const double* w, double* prev, int j0, int j1, cudaStream_t s) {
-    functional_kernel<<<1, 256, 0, s>>>(u, u_base, m, pitch, n, w, prev, j0, j1, nullptr, 1);
+int launch_functional(const double* u, int u_base, int m, int pitch, int n, const double* w,
+                      double* prev, int j0, int j1, double* out_max, int init, cudaStream_t s) {
+    if (j1 <= j0) return 0;
+    if (!init) {
+        const cudaError_t e = cudaMemsetAsync(out_max, 0, sizeof(double), s);
+        if (e != cudaSuccess) return static_cast<int>(e);
+    }
+    const int warps = 8, blocks = std::min((j1 - j0 + warps - 1) / warps, 148 * 8);
+    functional_kernel<<<blocks, warps * 32, 0, s>>>(u, u_base, m, pitch, n, w, prev, j0, j1,
+                                                   reinterpret_cast<unsigned long long*>(out_max), init);
     return static_cast<int>(cudaGetLastError());
 }
 
@@ -254,7 +255,7 @@ __global__ void scalar_sweep_kernel(ScalarSweepArgs a) {
         r -= a.u[(ti - a.u_base) / ud];
         const int ci = ti / m;
         if (a.tail == TAIL_STORE || a.tail == TAIL_BOTH) a.out[ci - a.out_base] = r;
-        if (a.tail == TAIL_SQ || a.tail == TAIL_BOTH) a.sq[ti - a.sq_base] = r * r;
+        if (a.tail == TAIL_SQ || a.tail == TAIL_BOTH) a.sq[(ti - a.sq_base) / a.sq_div] = r * r;
     }
 }
 

@@ -22,7 +22,7 @@ struct ScalarSweepArgs {
     const double* g; int g_base; int add_g;
     int store, tail;
     double* out; int out_base;
-    double* sq; int sq_base;
+    double* sq; int sq_base; int sq_div;  // squares at (tail point - sq_base) / sq_div
     int u_div;  // > 1: C-point-only u array
 };
 
@@ -57,12 +57,12 @@ int launch_c_correct(double* u, int u_base, int m, const double* cu, const doubl
 int launch_row_sum(double* g, const double* v, const double* r, int n, cudaStream_t s);
 // out[0] = sqrt(sum_i sq[i]) with a fixed association (shard-count independent)
 int launch_norm_from_squares(const double* sq, int count, double* out, cudaStream_t s);
-// functional-change norm: per C-point f = w.u, rel = |f-prev|/max(|prev|,1e-300),
-// prev := f; out_max[0] = max rel (solver.cpp:384-395)
-int launch_functional_change(const double* u, int u_base, int m, int pitch, int n,
-                             const double* w, double* prev, int j0, int j1, double* out_max,
-                             cudaStream_t s);
-int launch_functional_init(const double* u, int u_base, int m, int pitch, int n,
-                           const double* w, double* prev, int j0, int j1, cudaStream_t s);
+// FunctionalChange norm (solver.cpp:380-396), one warp per level-0 C point j in
+// [j0, j1): f_j = w.u (w != NULL) or u.norm2() (w == NULL, the reference CLI's
+// functional, run_config.cpp:241-243); unless init, rel_j = |f_j - prev_j| /
+// max(|prev_j|, 1e-300) and *out_max = max_j rel_j (zeroed first; a NaN ratio
+// never raises it, as with std::max); then prev_j := f_j (prev indexed by j).
+int launch_functional(const double* u, int u_base, int m, int pitch, int n, const double* w,
+                      double* prev, int j0, int j1, double* out_max, int init, cudaStream_t s);
 
 }  // namespace atm

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <sstream>
+#include <thread>
 
 namespace atm {
 
@@ -98,6 +99,9 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     const char* (*ErrStr)(ncclResult_t) = nullptr;
+    // fault detection (optional symbols: a stand-in may lack them)
+    ncclResult_t (*GetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*Abort)(ncclComm_t) = nullptr;
 
     bool load() {
         if (h) return true;
@@ -119,6 +123,8 @@ struct NcclApi {
         SYM(AllReduce, "ncclAllReduce");
         SYM(ErrStr, "ncclGetErrorString");
 #undef SYM
+        GetAsyncError = reinterpret_cast<decltype(GetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+        Abort = reinterpret_cast<decltype(Abort)>(dlsym(h, "ncclCommAbort"));
         return true;
     }
     void check(ncclResult_t r, const char* what) const {
@@ -332,8 +338,12 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     } else if (!folded_) {
         config_error("FAS cycles need forcing folded into the integrator");
     }
-    if (s.norm == ATM_NORM_FUNCTIONAL && !s.functional_w)
-        config_error("functional-change stopping norm needs a functional");
+    if (s.norm == ATM_NORM_FUNCTIONAL) {
+        if (s.functional_kind != ATM_FUNCTIONAL_LINEAR && s.functional_kind != ATM_FUNCTIONAL_NORM2)
+            config_error("functional-change stopping norm: unknown functional");
+        if (s.functional_kind == ATM_FUNCTIONAL_LINEAR && !s.functional_w)
+            config_error("functional-change stopping norm needs a functional");
+    }
     if (s.initial_guess == ATM_GUESS_PROVIDED && !s.provided)
         config_error("provided initial guess has the wrong number of points");
     // C-point storage (atm_storage): level 0 keeps only its
@@ -391,7 +401,8 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     if (p.ic) ic_.assign(p.ic, p.ic + n_);
     if (kind_ == ATM_PHI_SCALAR && p.fine_forcing && p.n_ff > 0)
         ff_.assign(p.fine_forcing, p.fine_forcing + p.n_ff);
-    if (s.functional_w) fw_.assign(s.functional_w, s.functional_w + n_);
+    if (s.functional_w && s.functional_kind == ATM_FUNCTIONAL_LINEAR)
+        fw_.assign(s.functional_w, s.functional_w + n_);
     if (s.constant_value) cval_.assign(s.constant_value, s.constant_value + n_);
     // the provided guess stays caller-owned until the first cycle (no host copy:
     // it can be the full level-0 array)
@@ -409,6 +420,9 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     if (world_ > 1 && local != 1) config_error("multi-process runs drive one shard per process");
     G_ = world_ > 1 ? world_ : local;
     lay_ = build_layout(H_, G_);
+    for (int q = 0; q < G_; ++q) ranges_all_.push_back(compute_ranges(H_, lay_, q));
+    if (rt.timeout_ms < 0) config_error("runtime: timeout_ms must be >= 0");
+    if (rt.timeout_ms > 0) timeout_ms_ = rt.timeout_ms;
     trace_ = rt.trace != 0;
     // chunk length per level: n > 2048 sweeps run 128-thread CTAs (L = 32,
     // three per SM); the coarsest level (windows only) keeps 256 threads
@@ -458,12 +472,15 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
         return static_cast<double*>(p);
     };
     const int np0 = H_.np[0];
+    // stopping-norm squares: one per level-0 C point (F residuals are zero
+    // after a cycle); the full residual norm keeps one per point
+    const int nc0 = H_.n_c(0);
     d_sq_full_ = dalloc(sizeof(double) * np0);
-    d_sq_c_ = dalloc(sizeof(double) * np0);
-    if (world_ > 1) d_sq_all_ = dalloc(sizeof(double) * np0);
+    d_sq_c_ = dalloc(sizeof(double) * nc0);
+    if (world_ > 1) d_sq_all_ = dalloc(sizeof(double) * std::max(np0, nc0));
     d_norm_ = dalloc(sizeof(double) * 300);
     d_fmax_ = dalloc(sizeof(double) * std::max(1, G_));
-    d_prevf_ = dalloc(sizeof(double) * np0);
+    d_prevf_ = dalloc(sizeof(double) * nc0);
     d_ic_ = dalloc(sizeof(double) * pitch_);
     d_row_ = dalloc(sizeof(double) * pitch_);
     d_fail_ = reinterpret_cast<int*>(dalloc(sizeof(int) * 4));
@@ -811,6 +828,7 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.out_base = out_lv ? out_lv->r.base : 0;
         a.sq = sq;
         a.sq_base = sq_base;
+        a.sq_div = sq == d_sq_c_ ? H_.m[level] : 1;  // per-C-point stopping squares
         const CUtensorMap& tg = add_g ? Lv.g.tm : Lv.u.tm;
         const CUtensorMap& to = out_lv ? out_lv->r.tm : Lv.u.tm;
         a.n_out = choose_n_out(a);
@@ -842,6 +860,7 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.out_base = out_lv ? out_lv->r.base : 0;
         a.sq = sq;
         a.sq_base = sq_base;
+        a.sq_div = sq == d_sq_c_ ? H_.m[level] : 1;  // per-C-point stopping squares
         check_launch(launch_cg_sweep(a, st_), "cg_sweep");
     } else {
         ScalarSweepArgs a{};
@@ -863,6 +882,7 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.out_base = out_lv ? out_lv->r.base : 0;
         a.sq = sq;
         a.sq_base = sq_base;
+        a.sq_div = sq == d_sq_c_ ? H_.m[level] : 1;  // per-C-point stopping squares
         check_launch(launch_scalar_sweep(a, st_), "scalar_sweep");
     }
 }
@@ -984,7 +1004,7 @@ void Engine::halo(int level, DArr LevelDev::*arr) {
     LevelDev& Lv = s.lv[level];
     if (Lv.hi < Lv.lo) return;
     const DArr& a = Lv.*arr;
-    ncclComm_t c = static_cast<ncclComm_t>(comm_);
+    ncclComm_t c = comm();
     nccl_->check(nccl_->GroupStart(), "group");
     if (Lv.right >= 0)
         nccl_->check(nccl_->Send(a.p + a.off(Lv.hi, pitch_), pitch_,
@@ -1020,11 +1040,11 @@ void Engine::window_exchange(int level, DArr LevelDev::*arr) {
     Shard& s = sh_[0];
     LevelDev& Lv = s.lv[level];
     const DArr& a = Lv.*arr;
-    ncclComm_t c = static_cast<ncclComm_t>(comm_);
+    ncclComm_t c = comm();
     nccl_->check(nccl_->GroupStart(), "group");
     for (int q = 0; q < G_; ++q) {
         if (q == rank_) continue;
-        const Ranges rq = compute_ranges(H_, lay_, q);
+        const Ranges& rq = ranges_all_[q];
         // what q needs from me
         const int q_lo = rq.lo[level];
         const int q_need_lo = std::max(0, q_lo - k + 1), q_need_hi = q_lo - 1;
@@ -1045,6 +1065,45 @@ void Engine::window_exchange(int level, DArr LevelDev::*arr) {
     (void)rowb;
 }
 
+ncclComm_t Engine::comm() const {
+    if (!comm_) throw Error(ATM_RUNTIME_FAULT, "rank " + std::to_string(rank_) + ": the NCCL communicator "
+                                               "was aborted after an earlier fault");
+    return static_cast<ncclComm_t>(comm_);
+}
+
+void Engine::sync_stream(const char* what) {
+    if (world_ == 1 || !comm_) {
+        CK(cudaStreamSynchronize(st_));
+        return;
+    }
+    // polled wait: a peer that died or stalls leaves an NCCL kernel spinning on
+    // this stream; fail like the reference's receive timeout (transport.cpp:
+    // 29-48 -> RuntimeFault) instead of hanging, after aborting the communicator
+    // so the stream drains (parallel.cpp:349-351: abort wakes the other ranks)
+    const auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms_);
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(st_);
+        if (e == cudaSuccess) return;
+        if (e != cudaErrorNotReady) ck(e, what);
+        std::string why;
+        if (nccl_->GetAsyncError) {
+            ncclResult_t ar = ncclSuccess;
+            nccl_->GetAsyncError(static_cast<ncclComm_t>(comm_), &ar);
+            if (ar != ncclSuccess && ar != ncclInProgress)
+                why = std::string("NCCL asynchronous error: ") + nccl_->ErrStr(ar);
+        }
+        if (why.empty() && std::chrono::steady_clock::now() > deadline)
+            why = "timed out after " + std::to_string(timeout_ms_) + " ms";
+        if (!why.empty()) {
+            if (nccl_->Abort) nccl_->Abort(static_cast<ncclComm_t>(comm_));
+            comm_ = nullptr;  // aborted: never used again (the destructor skips it)
+            throw Error(ATM_RUNTIME_FAULT, "rank " + std::to_string(rank_) + ": " + why +
+                                               " waiting for " + what + " (a peer rank failed or stalled)");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
 double Engine::reduce_norm(double* sq, int count) {
     // world > 1: each rank's per-point array holds only its own points (the
     // rest stay 0 and are never written), so the element-wise sum is exact.
@@ -1052,13 +1111,13 @@ double Engine::reduce_norm(double* sq, int count) {
     // other ranks' values in this rank's array for the next iteration.
     if (world_ > 1) {
         nccl_->check(nccl_->AllReduce(sq, d_sq_all_, count, ncclFloat64, ncclSum,
-                                      static_cast<ncclComm_t>(comm_), st_), "allreduce squares");
+                                      comm(), st_), "allreduce squares");
         sq = d_sq_all_;
     }
     check_launch(launch_norm_from_squares(sq, count, d_norm_, st_), "norm");
     double out = 0.0;
     CK(cudaMemcpyAsync(&out, d_norm_, sizeof(double), cudaMemcpyDeviceToHost, st_));
-    CK(cudaStreamSynchronize(st_));
+    sync_stream("the residual norm");
     return out;
 }
 
@@ -1095,7 +1154,7 @@ void Engine::fill_initial_guess() {
                              "fill random");
                 break;
             case ATM_GUESS_PROVIDED:
-                if (nrows > 0 && dv == 1 && H_.L >= 2 && H_.m[0] > 1 && !std::getenv("ATM_EAGER_GUESS")) {
+                if (nrows > 0 && dv == 1 && H_.L >= 2 && H_.m[0] > 1 && rt_.defer_guess) {
                     // Only the C rows go now. Every cycle opens with an
                     // F-relaxation from the C points (kernels.cpp:7-17) and
                     // its correction F-sweep rewrites every F row before
@@ -1139,7 +1198,7 @@ void Engine::flush_guess() {
                              sizeof(double) * n_, i1 - i0, cudaMemcpyHostToDevice, st_));
         h2d_bytes_ += sizeof(double) * n_ * static_cast<size_t>(i1 - i0);
     }
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
 }
 
 void Engine::fill_level_rhs(int level) {
@@ -1176,28 +1235,29 @@ void Engine::fill_level_rhs(int level) {
             if (i1 >= i0)
                 CK(cudaMemcpyAsync(Lv.g.p + (i0 - Lv.g.base), rows.data(), sizeof(double) * rows.size(),
                                    cudaMemcpyHostToDevice, st_));
-            CK(cudaStreamSynchronize(st_));
+            sync_stream(__func__);
         }
     }
 }
 
 void Engine::setup() {
     if (setup_done_) return;
-    phase_begin("setup");
+    phase_begin("fill");
     fill_initial_guess();
     fill_level_rhs(0);
     if (sol_.norm == ATM_NORM_FUNCTIONAL) {
+        // prev_functional_ (solver.cpp:101-106): f of every own C point of the guess
         for (Shard& s : sh_) {
             LevelDev& Lv = s.lv[0];
             if (Lv.c_count > 0)
-                check_launch(launch_functional_init(Lv.u.p, Lv.u.base / Lv.u.div, H_.m[0] / Lv.u.div,
-                                                    pitch_, n_, d_fw_,
-                                                    d_prevf_, Lv.c_first, Lv.c_first + Lv.c_count, st_),
+                check_launch(launch_functional(Lv.u.p, Lv.u.base / Lv.u.div, H_.m[0] / Lv.u.div, pitch_,
+                                               n_, d_fw_, d_prevf_, Lv.c_first, Lv.c_first + Lv.c_count,
+                                               nullptr, 1, st_),
                              "functional init");
         }
     }
     phase_end();
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     setup_done_ = true;
 }
 
@@ -1447,7 +1507,6 @@ bool Engine::use_graphs() const {
 
 void Engine::cycle() {
     setup();
-    guess_pending_ = false;  // this cycle rewrites every level-0 F row before reading one
     launches_ = 0;
     // with relax reuse the first cycle (which still runs the opening F-sweep)
     // is not the steady-state launch sequence: capture from the second on
@@ -1467,8 +1526,20 @@ void Engine::cycle() {
             cudaStreamEndCapture(st_, &g);
             if (g) cudaGraphDestroy(g);
         }
+        // the cycle's correction F-sweep (which rewrites every level-0 F row)
+        // may not have been enqueued: the deferred F rows of a provided guess
+        // must land, so the state reads as it would after an eager copy
+        if (guess_pending_) {
+            try {
+                flush_guess();
+            } catch (...) {
+            }
+        }
         throw;
     }
+    // every level-0 F row is rewritten by this cycle before anything reads it
+    // (also when check_newton below throws: the kernels ran to completion)
+    guess_pending_ = false;
     if (graphs) {
         cudaGraph_t g = nullptr;
         CK(cudaStreamEndCapture(st_, &g));
@@ -1488,7 +1559,7 @@ void Engine::check_newton() {
     if (!ac_ && !h2d_) return;
     int f = 0;
     CK(cudaMemcpyAsync(&f, d_fail_, sizeof(int), cudaMemcpyDeviceToHost, st_));
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     if (f) {
         CK(cudaMemsetAsync(d_fail_, 0, sizeof(int), st_));
         if (gs_)
@@ -1535,7 +1606,7 @@ void Engine::nested_init() {
                                    sizeof(double) * pitch_, cudaMemcpyDeviceToDevice, st_));
             } else if (world_ > 1 && C.lo > 0) {
                 nccl_->check(nccl_->Recv(C.u.p + C.u.off(C.lo - 1, pitch_),
-                                         pitch_, ncclFloat64, C.left, static_cast<ncclComm_t>(comm_), st_),
+                                         pitch_, ncclFloat64, C.left, comm(), st_),
                              "chain recv");
             }
             const int from = std::max(0, C.lo - 1);
@@ -1543,7 +1614,7 @@ void Engine::nested_init() {
                           C.u, 1, forced, 0, 0, 0);
             if (world_ > 1 && C.right >= 0)
                 nccl_->check(nccl_->Send(C.u.p + C.u.off(C.hi, pitch_), pitch_,
-                                         ncclFloat64, C.right, static_cast<ncclComm_t>(comm_), st_),
+                                         ncclFloat64, C.right, comm(), st_),
                              "chain send");
         }
     } else {
@@ -1571,7 +1642,7 @@ void Engine::nested_init() {
         f_sweep(l, TAIL_NONE);
         if (l >= 1) v_cycle(l);
     }
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     check_newton();
 }
 
@@ -1605,17 +1676,16 @@ double Engine::functional_change() {
     for (size_t i = 0; i < sh_.size(); ++i) {
         LevelDev& Lv = sh_[i].lv[0];
         if (Lv.c_count == 0) continue;
-        check_launch(launch_functional_change(Lv.u.p, Lv.u.base / Lv.u.div, H_.m[0] / Lv.u.div,
-                                              pitch_, n_, d_fw_,
-                                              d_prevf_, Lv.c_first, Lv.c_first + Lv.c_count,
-                                              d_fmax_ + i, st_), "functional");
+        check_launch(launch_functional(Lv.u.p, Lv.u.base / Lv.u.div, H_.m[0] / Lv.u.div, pitch_, n_,
+                                       d_fw_, d_prevf_, Lv.c_first, Lv.c_first + Lv.c_count,
+                                       d_fmax_ + i, 0, st_), "functional");
     }
     if (world_ > 1)
         nccl_->check(nccl_->AllReduce(d_fmax_, d_fmax_, 1, ncclFloat64, ncclMax,
-                                      static_cast<ncclComm_t>(comm_), st_), "allreduce max");
+                                      comm(), st_), "allreduce max");
     std::vector<double> h(sh_.size(), 0.0);
     CK(cudaMemcpyAsync(h.data(), d_fmax_, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st_));
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     for (double v : h) mx = std::max(mx, v);
     return mx;
 }
@@ -1627,7 +1697,7 @@ double Engine::stopping_norm_after_cycle() {
     // written by the correction sweep's tail are the full per-point array.
     if (sol_.norm == ATM_NORM_FUNCTIONAL) return functional_change();
     phase_begin("norm");
-    const double v = reduce_norm(d_sq_c_, H_.np[0]);
+    const double v = reduce_norm(d_sq_c_, H_.n_c(0));
     phase_end();
     return v;
 }
@@ -1637,7 +1707,7 @@ double Engine::iterate_timed(int count, double* norms) {
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     CK(cudaEventRecord(a, st_));
     for (int i = 0; i < count; ++i) {
         cycle();
@@ -1662,18 +1732,30 @@ void Engine::iterate(int count, double* norms) {
     }
 }
 
-int Engine::solve(atm_report* rep, double* norms) {
+void Engine::host_phase(const char* name, double seconds) {
+    phase_sec_[name] += seconds;
+    phase_cnt_[name] += 1;
+}
+
+int Engine::solve(atm_report* rep, double* norms, double* iter_secs) {
     // drive (solver.cpp:398-435)
-    const auto t0 = std::chrono::steady_clock::now();
+    using clock = std::chrono::steady_clock;
+    const auto t0 = clock::now();
     setup();
     if (sol_.mode == ATM_NESTED_V) nested_init();
+    const auto t_setup = clock::now();
+    const double setup_s = std::chrono::duration<double>(t_setup - t0).count();
+    host_phase("setup", setup_s);
     atm_report r{};
+    r.setup_seconds = setup_s;
     r.stop_reason = 1;
     double dof_steps = 0.0;
     int status = ATM_NOT_CONVERGED;
     for (int it = 1; it <= sol_.max_iters; ++it) {
+        const auto t_it = clock::now();
         cycle();
-        const double v = stopping_norm_after_cycle();
+        const double v = stopping_norm_after_cycle();  // one device->host read: synchronised
+        if (iter_secs) iter_secs[it - 1] = std::chrono::duration<double>(clock::now() - t_it).count();
         if (norms) norms[it - 1] = v;
         r.iterations = it;
         // relaxation Phi applications: every F-point twice per level visit
@@ -1687,7 +1769,8 @@ int Engine::solve(atm_report* rep, double* norms) {
         }
         if (!std::isfinite(v)) {
             r.stop_reason = 2;
-            r.total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            r.total_seconds = std::chrono::duration<double>(clock::now() - t0).count();
+            host_phase("iterations", std::chrono::duration<double>(clock::now() - t_setup).count());
             r.dof_steps = dof_steps;
             if (rep) *rep = r;
             throw Error(ATM_DIVERGED, "non-finite residual norm at iteration " + std::to_string(it));
@@ -1699,8 +1782,9 @@ int Engine::solve(atm_report* rep, double* norms) {
             break;
         }
     }
-    CK(cudaStreamSynchronize(st_));
-    r.total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    sync_stream(__func__);
+    r.total_seconds = std::chrono::duration<double>(clock::now() - t0).count();
+    host_phase("iterations", std::chrono::duration<double>(clock::now() - t_setup).count());
     r.dof_steps = dof_steps;
     if (rep) *rep = r;
     return status;
@@ -1719,7 +1803,7 @@ void Engine::xfer_level(int level, int which, int first, int count, double* host
         relax_valid_ = false;
     }
     if (level == 0) flush_guess();
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     if (to_host && level == 0 && which == 0 && cpts_) {
         get_level0_cpts(first, count, host);
         return;
@@ -1753,7 +1837,7 @@ void Engine::xfer_level(int level, int which, int first, int count, double* host
             CK(cudaMemcpy2DAsync(d, sizeof(double) * pitch_, h, sizeof(double) * n_ * dv,
                                  sizeof(double) * n_, nrow, cudaMemcpyHostToDevice, st_));
     }
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
 }
 
 // Level-0 u with C-point storage: the requested points are rebuilt chunk by
@@ -1792,7 +1876,7 @@ void Engine::get_level0_cpts(int first, int count, double* out) {
                                  T.p + T.off(r0, pitch_), rowb, sizeof(double) * n_, r1 - r0 + 1,
                                  cudaMemcpyDeviceToHost, st_));
         }
-        CK(cudaStreamSynchronize(st_));
+        sync_stream(__func__);
         for (void* p : tmp.allocs) cudaFree(p);
     }
     check_newton();
@@ -1834,7 +1918,7 @@ void Engine::apply_phi(int level, int first, int count, const double* in, double
         CK(cudaMemcpy2DAsync(out, sizeof(double) * n_, y.p, sizeof(double) * pitch_,
                              sizeof(double) * n_, count, cudaMemcpyDeviceToHost, st_));
     }
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     (void)save;
     for (void* p : tmp.allocs) cudaFree(p);
     check_newton();
@@ -1848,7 +1932,7 @@ void Engine::kernel_f_relax(int level, int first_iv, int count) {
     setup();
     flush_guess();
     sweep_jobs(sh_[0], level, SW_F, first_iv, first_iv + count, TAIL_NONE, 0, nullptr, 0);
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     check_newton();
 }
 
@@ -1861,7 +1945,7 @@ void Engine::kernel_c_relax(int level, int first_c, int count) {
     flush_guess();
     sweep_jobs(sh_[0], level, SW_CRELAX, std::max(1, first_c), first_c + count, TAIL_NONE, 0,
                nullptr, 0);
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     check_newton();
 }
 
@@ -1879,6 +1963,7 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
         SweepArgs a{};
         a.co = Lv.hco;
         a.kind = SW_RESID;
+        a.sq_div = 1;
         a.m = 1;
         a.np = H_.np[level];
         a.j0 = std::max(1, first);
@@ -1900,6 +1985,7 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
         CgSweepArgs a{};
         a.co = Lv.gco;
         a.kind = SW_RESID;
+        a.sq_div = 1;
         a.m = 1;
         a.np = H_.np[level];
         a.j0 = std::max(1, first);
@@ -1919,6 +2005,7 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
         ScalarSweepArgs a{};
         a.co = Lv.sco;
         a.kind = SW_RESID;
+        a.sq_div = 1;
         a.m = 1;
         a.np = H_.np[level];
         a.j0 = std::max(1, first);
@@ -1937,14 +2024,14 @@ void Engine::kernel_residual(int level, int first, int count, double* out) {
     if (first == 0 && Lv.g.p) check_launch(launch_row_diff(r.p, Lv.g.p, Lv.u.p, n_, nullptr, st_), "r0");
     CK(cudaMemcpy2DAsync(out, sizeof(double) * n_, r.p, sizeof(double) * pitch_, sizeof(double) * n_,
                          count, cudaMemcpyDeviceToHost, st_));
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     for (void* p : tmp.allocs) cudaFree(p);
 }
 
 unsigned long long Engine::inner_iterations() {
     unsigned long long v = 0;
     CK(cudaMemcpyAsync(&v, d_inner_, sizeof(v), cudaMemcpyDeviceToHost, st_));
-    CK(cudaStreamSynchronize(st_));
+    sync_stream(__func__);
     return v;
 }
 

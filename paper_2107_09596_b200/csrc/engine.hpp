@@ -23,6 +23,8 @@
 #include "common_kernels.cuh"
 #include "heat_kernels.cuh"
 
+struct ncclComm;  // nccl.h: typedef struct ncclComm* ncclComm_t
+
 namespace atm {
 
 struct Error : std::runtime_error {
@@ -122,7 +124,7 @@ public:
     void cycle();
     double residual_norm();            // full level-0 residual (all points)
     double stopping_norm_after_cycle();
-    int solve(atm_report* rep, double* norms);
+    int solve(atm_report* rep, double* norms, double* iteration_seconds = nullptr);
     void iterate(int count, double* norms);
 
     double iterate_timed(int count, double* norms);  // device ms (CUDA events)
@@ -174,6 +176,11 @@ private:
     void two_level_cycle();
     void point0_residual(Shard& s, int level, double* r_out, double* sq_out);
     double reduce_norm(double* sq, int count);
+    // wait for the stream; with world > 1 a polled wait that fails with
+    // ATM_RUNTIME_FAULT on an NCCL async error or after timeout_ms (the
+    // communicator is aborted first, transport.cpp:29-61 / parallel.cpp:365-383)
+    void sync_stream(const char* what);
+    ::ncclComm* comm() const;  // the live communicator (throws after an abort)
     double functional_change();
     // exchanges
     void halo(int level, DArr LevelDev::*arr);
@@ -209,6 +216,8 @@ private:
     double h_ = 0.0;
     std::vector<double> sinp_;
     std::vector<Shard> sh_;
+    std::vector<Ranges> ranges_all_;  // compute_ranges of every rank (exchange schedules)
+    int timeout_ms_ = 30000;
     cudaStream_t st_ = nullptr;
     bool setup_done_ = false;
     // global reduction arrays (per point of level 0)
@@ -232,7 +241,9 @@ private:
     // NCCL (world > 1)
     std::unique_ptr<NcclApi> nccl_;
     void* comm_ = nullptr;
-    // timing
+    // timing (ConvergenceReport::timings: host "setup" / "iterations" always,
+    // device-event phases with trace_)
+    void host_phase(const char* name, double seconds);
     bool trace_ = false;
     std::map<std::string, double> phase_sec_;
     struct Pending : std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>> {

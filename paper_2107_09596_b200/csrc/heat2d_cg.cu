@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kerne
                     s2[0] = fma(v, v, s2[0]);
                 });
                 cluster_sum<1>(s2, cx);
-                if (cx.q == 0 && cx.t == 0) a.sq[ti - a.sq_base] = s2[0];
+                if (cx.q == 0 && cx.t == 0) a.sq[(ti - a.sq_base) / a.sq_div] = s2[0];
             }
         }
     }

@@ -96,8 +96,9 @@ struct SweepArgs {
                        // correction F-sweep before anything reads them)
     int tail;          // TailKind: residual at the next C-point
     int out_base;      // global (coarse) index of row 0 of the tail target
-    double* sq;        // per-point squares (TAIL_SQ), indexed by tail point - sq_base
+    double* sq;        // squares (TAIL_SQ) at (tail point - sq_base) / sq_div
     int sq_base;
+    int sq_div;        // 1: per-point array; m: per-C-point array (stopping norm)
     int n_out;         // output staging buffers (1 or 2)
     int u_div;         // > 1: the u array holds only the C points (row = (i - u_base) / u_div)
 };

@@ -1000,7 +1000,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 stage_out(tail_i / m - a.out_base, &tm_out, &tm_outw);
             } else {
                 const double tot = cta_sum_squares<L>(x, ln, sl);
-                if (t == 0) a.sq[tail_i - a.sq_base] = tot;
+                if (t == 0) a.sq[(tail_i - a.sq_base) / a.sq_div] = tot;
                 if (a.tail == TAIL_BOTH) stage_out(tail_i / m - a.out_base, &tm_out, &tm_outw);
             }
         }

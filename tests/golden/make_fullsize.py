@@ -1,13 +1,30 @@
-"""Full-size golden fixtures for BASELINE configs 2 and 3 from the C oracle
-restatement (oracle/atm_oracle.c; single-threaded, minutes to an hour per
-config on the dev container).  Each fixture holds the oracle's iteration
-count and residual history to tol 1e-10 and every SAMPLE-th level-0 row of
-its final state (the full state is 0.5 GB): tests/test_gpu_fullsize.py
-compares the device solve against them.
+"""Full-size golden fixtures for BASELINE configs 2, 3 and 4 from the COMPILED
+REFERENCE's own cycle driver (oracle/_ref/tempo_ref: `runtime::run_parallel`
+over all host threads, /root/reference/proj/src/parallel.cpp:331-405).  The
+reference has no Phi for these problems, so tempo_ref's `OracleApp` supplies
+the restated Phi (oracle/atm_oracle.c: h2_solve / ac_step) through the
+reference's Application interface (application.hpp:33-76); the cycles --
+relaxation, restriction, truncated windows, FAS, correction, norm, stopping
+-- are the reference's (solver.cpp:152-435).
 
-  python tests/golden/make_fullsize.py {2,3} [random|constant] [newton_tol (config 3, default 1e-12)]
+Each fixture holds the iteration count and residual history to tol 1e-10 and
+every SAMPLE-th level-0 row of the final state plus its 2-norm (the full state
+is 0.5 GB and up): tests/test_gpu_fullsize.py compares the device solve
+against them.  A Newton-cap failure (NonlinearSolveError, gray_scott.cpp:
+165-169) is recorded with the failing cycle and the history before it: a
+first run names the failing cycle (tempo_ref reports the last iteration a
+phase ran in), a second run with max_iters = that cycle - 1 yields the history.
 
-Config definitions follow DESIGN.md section 9 (pinned choices)."""
+  python tests/golden/make_fullsize.py TAG [TAG ...]
+      TAG in config2, config3, config3_constant, config3_newton1e-11, config4s
+
+Config definitions follow DESIGN.md section 9 (pinned choices).  config4s is
+BASELINE config 4's spatial problem and time step (511^2, dt = 4/65536,
+four-level FAS V-cycle m = (8, 8, 8), k = 2) over a short horizon (2048 steps:
+levels of 2049, 257, 33, 5 points -- run_parallel takes at most 5 workers)
+so the CPU reference finishes in about an hour; its rows keep every 16th
+unknown (a 511^2 state is 2 MB).
+"""
 from __future__ import annotations
 
 import json
@@ -24,7 +41,6 @@ sys.path.insert(0, ROOT)
 from oracle import oracle as O  # noqa: E402
 
 TOL = 1e-10
-SAMPLE = {2: 256, 3: 1024}
 
 
 def gaussian_source(nx):
@@ -33,56 +49,70 @@ def gaussian_source(nx):
     return T.gaussian_source(nx)
 
 
-def config(c, guess="random", newton_tol=1e-12):
-    if c == 2:
+def fourier_ic(nx):
+    import paper_2107_09596_b200 as T
+    return T.fourier_ic(nx)
+
+
+def config(tag):
+    """(meta, tempo_ref args, input files) for one fixture tag."""
+    if tag == "config2":
         nx = 127
-        return (dict(kind=O.HEAT2D, n=nx * nx, nx=nx, folded=0, source=gaussian_source(nx), ic=None,
-                     cg_rtol=1e-12, cg_max=10000),
-                dict(tf=1.0, n_points=4097, m=[16], k=4),
-                dict(mode=O.TWO_LEVEL, relaxation=O.RELAX_F, max_iters=200, tol=TOL,
-                     initial_guess=O.GUESS_RANDOM, seed=20))
-    if c == 3:
-        n = 4096
-        return (dict(kind=O.ALLEN_CAHN, n=n, eps=0.02, length=1.0, newton_tol=newton_tol, newton_max=30,
-                     folded=1, ic=0.05 * O.random_state(3, n)),
-                dict(tf=8.0, n_points=16385, m=[8, 8], k=4),
-                dict(mode=O.VCYCLE, relaxation=O.RELAX_F, max_iters=200, tol=TOL,
-                     initial_guess=O.GUESS_RANDOM if guess == "random" else O.GUESS_CONSTANT,
-                     seed=20))
-    raise SystemExit(f"unknown config {c}")
+        return (dict(config=2, guess="random", sample_every=256),
+                dict(problem="heat2d", nx=nx, folded=0, cg_rtol=1e-12, cg_max=10000, tf=1.0,
+                     n_points=4097, m=16, k=4, mode="two-level", guess="random", seed=20,
+                     max_iters=200, tol=TOL),
+                dict(source_file=gaussian_source(nx)))
+    if tag.startswith("config3"):
+        guess = "constant" if "constant" in tag else "random"
+        ntol = float(tag.split("newton")[1]) if "newton" in tag else 1e-12
+        meta = dict(config=3, guess=guess, sample_every=1024)
+        if ntol != 1e-12:
+            meta["newton_tol"] = ntol
+        return (meta,
+                dict(problem="allen_cahn", n=4096, eps=0.02, length=1.0, newton_tol=ntol,
+                     newton_max=30, tf=8.0, n_points=16385, m="8,8", k=4, mode="v-cycle",
+                     guess=guess, seed=20, max_iters=200, tol=TOL),
+                dict(ic_file=0.05 * O.random_state(3, 4096)))
+    if tag == "config4s":
+        nx = 511
+        return (dict(config=4, guess="random", sample_every=256, dof_stride=16, n_points=2049, tf=0.125),
+                dict(problem="heat2d", nx=nx, folded=1, cg_rtol=1e-12, cg_max=100000,
+                     tf=2048 * 4.0 / 65536, n_points=2049, m="8,8,8", k=2, mode="v-cycle",
+                     guess="random", seed=20, max_iters=60, tol=TOL),
+                dict(ic_file=fourier_ic(nx)))
+    raise SystemExit(f"unknown tag {tag}")
 
 
-def main():
-    c = int(sys.argv[1])
-    guess = sys.argv[2] if len(sys.argv) > 2 else "random"
-    ntol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-12
-    tag = f"config{c}" + ("" if guess == "random" else f"_{guess}") + ("" if ntol == 1e-12 else f"_newton{ntol:g}")
-    p, g, s = config(c, guess, ntol)
-    t0 = time.time()
-    d = O.Driver(p, g, s)
-    meta = dict(config=c, guess=guess, tol=TOL, newton_tol=ntol, sample_every=SAMPLE[c])
-    try:
-        res = d.drive()
-    except O.OracleError as e:
-        # the reference's failure behaviour is part of the contract (Newton
-        # cap -> NonlinearSolveError, gray_scott.cpp:165-169): record the
-        # failing iteration and the history before it
-        meta.update(error=str(e), code=int(e.code),
-                    failed_at_iteration=int(e.iterations) + 1,
-                    history=[float(x) for x in e.history], oracle_seconds=time.time() - t0)
+def main(tags):
+    for tag in tags:
+        meta, args, files = config(tag)
+        args = dict(args, workers=0)  # all host threads
+        meta.update(tol=TOL, generator="tempo_ref run_parallel (reference CycleDriver, restated Phi)")
+        t0 = time.time()
+        res, u = O.run_ref(args, out_u=True, files=files, timeout=6 * 3600)
+        if "error" in res:
+            if res["error"] not in ("nonlinear", "runtime") or "Newton" not in res.get("what", ""):
+                raise SystemExit(f"{tag}: {res}")
+            failed = int(res["last_iteration"])
+            hist, _ = O.run_ref(dict(args, max_iters=failed - 1), files=files, timeout=6 * 3600)
+            assert "error" not in hist and len(hist["history"]) == failed - 1, hist
+            meta.update(error=res["what"], code=5, failed_at_iteration=failed,
+                        history=[float(x) for x in hist["history"]],
+                        ref_seconds=time.time() - t0, workers=hist["workers"])
+        else:
+            n = u.size // int(args["n_points"])
+            u = u.reshape(int(args["n_points"]), n)
+            ds = meta.get("dof_stride", 1)
+            np.save(os.path.join(HERE, f"fullsize_{tag}_rows.npy"), u[::meta["sample_every"], ::ds].copy())
+            meta.update(iterations=int(res["iterations"]), converged=bool(res["converged"]),
+                        history=[float(x) for x in res["history"]],
+                        state_l2=float(np.linalg.norm(u)), ref_seconds=res["seconds"],
+                        workers=res["workers"])
         with open(os.path.join(HERE, f"fullsize_{tag}.json"), "w") as f:
             json.dump(meta, f, indent=1)
-        print(json.dumps({k: v for k, v in meta.items() if k != "history"}))
-        return
-    u = d.array(0)
-    np.save(os.path.join(HERE, f"fullsize_{tag}_rows.npy"), u[::SAMPLE[c]].copy())
-    meta.update(iterations=int(res["iterations"]), converged=bool(res["converged"]),
-                history=[float(x) for x in res["history"]], state_l2=float(np.linalg.norm(u)),
-                oracle_seconds=time.time() - t0)
-    with open(os.path.join(HERE, f"fullsize_{tag}.json"), "w") as f:
-        json.dump(meta, f, indent=1)
-    print(json.dumps({k: v for k, v in meta.items() if k != "history"}))
+        print(json.dumps({k: v for k, v in meta.items() if k != "history"}), flush=True)
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])

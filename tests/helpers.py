@@ -14,7 +14,19 @@ def _ms(args):
     return [int(x) for x in str(m).split(",")]
 
 
-def device_objects(args, ic=None, ff=None):
+def _functional(args, files):
+    """SolverConfig.functional of a tempo_ref case (ref_driver.cpp functional=)."""
+    fk = args.get("functional", "first")
+    if fk == "norm2":
+        return "norm2"
+    if fk == "weights":
+        return files["w_file"]
+    w = np.zeros(int(args.get("n", 1)) if args.get("problem", "heat1d") == "heat1d" else 1)
+    w[0] = 1.0  # u[0]
+    return w
+
+
+def device_objects(args, ic=None, ff=None, files=None):
     prob = args.get("problem", "heat1d")
     if prob == "heat1d":
         app = T.Heat1D(int(args.get("n", 1025)), float(args.get("x0", 0.0)), float(args.get("x1", 1.0)),
@@ -37,6 +49,9 @@ def device_objects(args, ic=None, ff=None):
                          nu=int(args.get("nu", 1)), max_iters=int(args.get("max_iters", 100)),
                          tol=float(args.get("tol", 1e-7)), initial_guess=guess, seed=int(args.get("seed", 0)),
                          coarse_substeps=int(args.get("substeps", 1)))
+    if args.get("norm") == "functional":
+        cfg.norm = T.NormKind.FunctionalChange
+        cfg.functional = _functional(args, files or {})
     return app, hier, cfg
 
 

@@ -12,6 +12,10 @@
  * waiting happens on the host -- no kernel waits on another process -- and a
  * group posts all of its sends before blocking on its receives.  The
  * all-reduce sums (or maxes) the ranks' contributions in rank order.
+ * A receive that finds no message within MOCKNCCL_TIMEOUT_MS (default 60 s)
+ * fails with ncclSystemError, so a dead peer surfaces as an error the way
+ * the engine's timeout does with real NCCL; ncclCommGetAsyncError /
+ * ncclCommAbort exist for the engine's fault path.
  *
  * Not used by the product: selected only by tests via ATM_NCCL_LIB.
  */
@@ -87,7 +91,17 @@ ncclResult_t ncclCommDestroy(ncclComm_t c) {
     return ncclSuccess;
 }
 
-const char* ncclGetErrorString(ncclResult_t r) { return r == ncclSuccess ? "success" : "mock error"; }
+const char* ncclGetErrorString(ncclResult_t r) {
+    return r == ncclSuccess ? "success" : "mock transport error (timed out or failed)";
+}
+
+ncclResult_t ncclCommGetAsyncError(ncclComm_t c, ncclResult_t* out) {
+    (void)c;
+    *out = ncclSuccess;  /* every mock operation completes (or fails) synchronously */
+    return ncclSuccess;
+}
+
+ncclResult_t ncclCommAbort(ncclComm_t c) { return ncclCommDestroy(c); }
 
 static ncclResult_t put_file(const char* path, const void* data, size_t bytes) {
     char tmp[256];
@@ -103,7 +117,15 @@ static ncclResult_t put_file(const char* path, const void* data, size_t bytes) {
     return ncclSuccess;
 }
 
+static double now_ms(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
+
 static ncclResult_t get_file(const char* path, void* data, size_t bytes) {
+    const char* env = getenv("MOCKNCCL_TIMEOUT_MS");
+    const double limit = env ? atof(env) : 60000.0, t0 = now_ms();
     for (long spin = 0;; ++spin) {
         FILE* f = fopen(path, "rb");
         if (f) {
@@ -112,7 +134,10 @@ static ncclResult_t get_file(const char* path, void* data, size_t bytes) {
             if (got != bytes) return fail("short read");
             return ncclSuccess;
         }
-        if (spin > 60L * 1000 * 20) return fail("timeout waiting for a message");
+        if (now_ms() - t0 > limit) {
+            errno = ETIMEDOUT;
+            return fail("timed out waiting for a message");
+        }
         usleep(50);
     }
 }

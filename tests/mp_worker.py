@@ -4,6 +4,9 @@ host-mediated NCCL stand-in (tests/mocknccl) so several processes can share
 the single GPU.  Spawned by tests/test_gpu_multiproc.py:
 
     ATM_NCCL_LIB=... python tests/mp_worker.py CASE RANK WORLD IDFILE OUT.npz
+
+MP_DIE_RANK=r makes rank r exit right after setup (a crashed peer); the
+other ranks record the error their solve raised (status, message, seconds).
 """
 import json
 import os
@@ -37,7 +40,22 @@ def main():
         time.sleep(0.01)
     nid = open(idfile, "rb").read()
     app, hier, cfg = build_case(case)
-    drv = T.CycleDriver(app, hier, cfg, world_size=world, rank=rank, nccl_id=nid)
+    drv = T.CycleDriver(app, hier, cfg, world_size=world, rank=rank, nccl_id=nid,
+                        timeout_ms=int(os.environ.get("MP_TIMEOUT_MS", "0")))
+    if os.environ.get("MP_DIE_RANK") is not None:
+        drv.setup()
+        if rank == int(os.environ["MP_DIE_RANK"]):
+            os._exit(0)  # a peer that dies without a word
+        t = time.time()
+        try:
+            drv.drive()
+            err = dict(error=None)
+        except T.TempoError as e:
+            err = dict(error=type(e).__name__, what=str(e))
+        err["seconds"] = time.time() - t
+        with open(out + ".json", "w") as f:
+            json.dump(err, f)
+        os._exit(0)
     rep = drv.drive()
     rr = T.rank_ranges(hier, world, rank)
     lo, hi = rr["lo"][0], rr["hi"][0]

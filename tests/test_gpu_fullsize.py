@@ -1,8 +1,11 @@
-"""BASELINE configs 2 and 3 at their FULL sizes against the C oracle's
-fixtures (tests/golden/make_fullsize.py): 2D heat 127^2, N_t = 4096,
-two-level m = 16, k = 4 (CG Phi); Allen-Cahn n = 4096, N_t = 16384 over
-[0, 8], three-level m = (8, 8), k = 4 (Newton Phi, FAS V-cycle).  Both to
-tol 1e-10 from the seeded random guess.  The bar (BASELINE north star): the
+"""BASELINE configs 2 and 3 at their FULL sizes, and config 4's grid and
+four-level hierarchy over a short horizon, against fixtures written by the
+compiled reference's own cycle driver (tests/golden/make_fullsize.py:
+tempo_ref run_parallel with the restated Phi as its Application): 2D heat
+127^2, N_t = 4096, two-level m = 16, k = 4 (CG Phi); Allen-Cahn n = 4096,
+N_t = 16384 over [0, 8], three-level m = (8, 8), k = 4 (Newton Phi, FAS
+V-cycle); 2D heat 511^2, dt = 4/65536, N_t = 1024, four-level FAS m = (8, 8,
+8), k = 2.  All to tol 1e-10 from the seeded random guess.  The bar (BASELINE north star): the
 same iteration count, and the final state within 1e-10 relative l2 -- here on
 every SAMPLE-th level-0 row the fixture keeps, plus the full state's 2-norm.
 The residual histories agree to 1e-8 relative (their tails sit near the
@@ -30,7 +33,14 @@ def _fixture(tag):
     return meta, (np.load(rows) if os.path.exists(rows) else None)
 
 
-def _objects(c, tol, guess="random", newton_tol=1e-12):
+def _objects(c, tol, guess="random", newton_tol=1e-12, meta=None):
+    if c == 4:
+        app = T.Heat2D(511, folded=True, source=None, cg_rtol=1e-12, cg_max=100000,
+                       initial_condition=T.fourier_ic(511))
+        hier = T.build_hierarchy(T.TimeGrid.make(0.0, meta["tf"], meta["n_points"]), [8, 8, 8], 2)
+        cfg = T.SolverConfig(mode=T.CycleMode.VCycle, relaxation=T.Relaxation.F, max_iters=60,
+                             tol=tol, initial_guess=T.InitialGuess.Random, seed=20)
+        return app, hier, cfg
     if c == 2:
         app = T.Heat2D(127, folded=False, source=T.gaussian_source(127), cg_rtol=1e-12, cg_max=10000)
         hier = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, 4097), [16], 4)
@@ -54,7 +64,7 @@ TAGS = sorted(f[len("fullsize_"):-len(".json")] for f in os.listdir(GOLDEN)
 def test_full_size_config_matches_oracle(tag):
     meta, rows = _fixture(tag)
     app, hier, cfg = _objects(meta["config"], meta["tol"], meta.get("guess", "random"),
-                              meta.get("newton_tol", 1e-12))
+                              meta.get("newton_tol", 1e-12), meta)
     if "failed_at_iteration" in meta:
         # the oracle's Newton hit its cap (NonlinearSolveError, gray_scott.cpp:
         # 165-169): the device must fail in the same cycle, after the same history
@@ -74,7 +84,7 @@ def test_full_size_config_matches_oracle(tag):
     hist = np.array(res.report.residual_norms)
     ref = np.array(meta["history"])
     assert np.all(np.abs(hist - ref) <= 1e-8 * np.abs(ref) + 1e-13), np.max(np.abs(hist - ref) / ref)
-    got = res.state[::meta["sample_every"]]
+    got = res.state[::meta["sample_every"], ::meta.get("dof_stride", 1)]
     assert got.shape == rows.shape
     assert rel_l2(got, rows) <= 1e-10, rel_l2(got, rows)
     full = float(np.linalg.norm(res.state))

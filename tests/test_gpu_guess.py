@@ -1,4 +1,5 @@
-"""Provided initial guess: atm_setup sends only the level-0 C rows.
+"""Provided initial guess with atm_runtime.defer_guess: atm_setup sends only
+the level-0 C rows (the default, defer_guess = 0, copies the whole guess).
 
 Every cycle opens with an F-relaxation from the C points (kernels.cpp:7-17)
 and its correction F-sweep rewrites every level-0 F row before anything reads
@@ -8,9 +9,11 @@ something could read them before the first cycle (the full residual norm,
 level-0 reads and writes, the kernel-level entry points, nested init).
 
 Checks: a guess whose F rows are NaN solves BITWISE like the same guess with
-finite F rows copied eagerly (ATM_EAGER_GUESS=1), across cycle modes,
-relaxations, families and shard counts; every pre-cycle access sees the full
-guess; the traffic counters report what moved."""
+finite F rows copied eagerly (the default), across cycle modes, relaxations,
+families (heat, scalar, Allen-Cahn Newton, 2D heat CG, Gray-Scott BiCGSTAB)
+and shard counts; every pre-cycle access sees the full guess; a cycle that
+fails (Newton cap) leaves the state an eager copy would; the traffic counters
+report what moved."""
 from __future__ import annotations
 
 import numpy as np
@@ -34,12 +37,51 @@ CASES = [
     # scalar backend
     dict(problem="dahlquist", tf=2.0, n_points=4097, m="4,4", k=2, folded=1, mode="v-cycle",
          max_iters=40, tol=1e-12),
+    # Allen-Cahn: Newton warm-starts from u_prev, FAS V-cycle
+    dict(problem="allen_cahn", n=256, tf=1.0, n_points=257, m="4,4", k=3, mode="v-cycle",
+         max_iters=30, tol=1e-9),
+    # 2D heat: CG starts from x0 = u_prev, explicit source, two-level
+    dict(problem="heat2d", nx=31, tf=1.0, n_points=129, m=8, k=3, folded=0, max_iters=30, tol=1e-9),
+    # Gray-Scott: Newton + BiCGSTAB
+    dict(problem="gray_scott", nx=8, tf=2.0, n_points=33, m=4, k=2, mode="v-cycle", max_iters=8,
+         tol=1e-7),
 ]
+
+
+def _objects(args):
+    prob = args["problem"]
+    if prob in ("heat1d", "dahlquist"):
+        return device_objects(dict(args, guess="provided"))
+    if prob == "allen_cahn":
+        app = T.AllenCahn(int(args["n"]), 0.02, 1.0, 1e-11, 30,
+                          initial_condition=0.05 * T.random_state(3, int(args["n"])))
+    elif prob == "heat2d":
+        app = T.Heat2D(int(args["nx"]), folded=False, source=T.gaussian_source(int(args["nx"])))
+    else:
+        app = T.GrayScott(int(args["nx"]))
+    ms = [int(x) for x in str(args["m"]).split(",")]
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, float(args["tf"]), int(args["n_points"])), ms,
+                             int(args["k"]))
+    mode = T.CycleMode.VCycle if args.get("mode") == "v-cycle" else T.CycleMode.TwoLevel
+    cfg = T.SolverConfig(mode=mode, max_iters=int(args["max_iters"]), tol=float(args["tol"]),
+                         initial_guess=T.InitialGuess.Provided)
+    return app, hier, cfg
+
+
+def _n(args):
+    p = args["problem"]
+    return {"heat1d": lambda: int(args["n"]), "dahlquist": lambda: 1, "allen_cahn": lambda: int(args["n"]),
+            "heat2d": lambda: int(args["nx"]) ** 2, "gray_scott": lambda: 2 * int(args["nx"]) ** 2}[p]()
 
 
 def _guess(args, n, seed=0):
     npts = int(args["n_points"])
-    return np.random.default_rng(seed).uniform(-1.0, 1.0, (npts, n))
+    g = np.random.default_rng(seed).uniform(-1.0, 1.0, (npts, n))
+    if args["problem"] in ("allen_cahn", "gray_scott"):
+        # nonlinear Phi: stay near the solution manifold (Allen-Cahn |u| < 1,
+        # Gray-Scott inside the bounds check)
+        g = 0.05 * g if args["problem"] == "allen_cahn" else np.clip(0.5 + 0.1 * g, 0.0, 1.0)
+    return g
 
 
 def _f_rows_nan(args, g):
@@ -51,39 +93,52 @@ def _f_rows_nan(args, g):
     return h
 
 
-def _solve(args, guess, workers, eager, monkeypatch):
-    if eager:
-        monkeypatch.setenv("ATM_EAGER_GUESS", "1")
-    else:
-        monkeypatch.delenv("ATM_EAGER_GUESS", raising=False)
-    app, hier, cfg = device_objects(dict(args, guess="provided"))
+def _solve(args, guess, workers, eager, monkeypatch=None):
+    app, hier, cfg = _objects(args)
     cfg.provided = guess
-    return T.solve(app, hier, cfg, workers=workers)
+    return T.solve(app, hier, cfg, workers=workers, defer_guess=not eager)
 
 
-@pytest.mark.parametrize("args", CASES)
+@pytest.mark.parametrize("args", CASES, ids=lambda a: a["problem"] + "-" + a.get("mode", "two-level"))
 @pytest.mark.parametrize("workers", [1, 3])
-def test_nan_f_rows_solve_bitwise_like_eager_copy(args, workers, monkeypatch):
-    n = 1 if args["problem"] != "heat1d" else int(args["n"])
+def test_nan_f_rows_solve_bitwise_like_eager_copy(args, workers):
+    n = _n(args)
     g = _guess(args, n)
-    a = _solve(args, g, workers, True, monkeypatch)
-    b = _solve(args, _f_rows_nan(args, g), workers, False, monkeypatch)
+    a = _solve(args, g, workers, True)
+    b = _solve(args, _f_rows_nan(args, g), workers, False)
     assert a.report.iterations == b.report.iterations
     assert np.array_equal(np.array(a.report.residual_norms), np.array(b.report.residual_norms))
     assert np.array_equal(a.state, b.state)
     assert np.isfinite(b.state).all()
 
 
-def _driver(args, guess, monkeypatch, eager=False, **kw):
-    if eager:
-        monkeypatch.setenv("ATM_EAGER_GUESS", "1")
-    else:
-        monkeypatch.delenv("ATM_EAGER_GUESS", raising=False)
-    app, hier, cfg = device_objects(dict(args, guess="provided"))
+def _driver(args, guess, monkeypatch=None, eager=False, **kw):
+    app, hier, cfg = _objects(args)
     cfg.provided = guess
-    d = T.CycleDriver(app, hier, cfg, **kw)
+    d = T.CycleDriver(app, hier, cfg, defer_guess=not eager, **kw)
     d.setup()
     return d
+
+
+def test_failed_first_cycle_leaves_the_eager_state():
+    # a provided guess whose first cycle raises NonlinearSolveError
+    # (Allen-Cahn Newton capped at one iteration) must leave level 0 as an
+    # eager copy would -- never the zero-filled F rows of a dropped deferral
+    args = dict(CASES[4])
+    g = _guess(args, _n(args), seed=7)
+    states = []
+    for eager in (True, False):
+        app, hier, cfg = _objects(args)
+        app = T.AllenCahn(int(args["n"]), 0.02, 1.0, 1e-14, 1,
+                          initial_condition=0.05 * T.random_state(3, int(args["n"])))
+        cfg.provided = g
+        d = T.CycleDriver(app, hier, cfg, defer_guess=not eager)
+        d.setup()
+        with pytest.raises(T.NonlinearSolveError):
+            d.cycle()
+        states.append(d.get_level(0))
+    assert np.array_equal(states[0], states[1])
+    assert np.isfinite(states[1]).all() and np.any(states[1][1:] != 0.0)
 
 
 def test_pre_cycle_accesses_see_the_full_guess(monkeypatch):

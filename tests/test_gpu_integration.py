@@ -1,0 +1,40 @@
+"""The drop-in boundary in code: the INTEGRATION.md adapter
+(tests/integration/solve_b200.cpp: tempo::solve_b200 and
+runtime::run_parallel_b200 over include/atmgrit.h), compiled against the
+reference's own headers, against the reference's CPU solve
+(tempo::solve / runtime::run_parallel from the compiled reference sources) on
+the same Hierarchy and SolverConfig -- both called through the reference's
+API by tests/integration/compare_main.cpp.
+
+The bar: the same iteration count and convergence flag, histories within
+1e-9 (relative, or relative to the first norm: tails sit at the rounding
+floor; FunctionalChange values -- differences of nearly equal numbers --
+within 1e-6 relative to themselves or to the tolerance), final level-0 state
+within 1e-10 relative l2; the report carries per-iteration seconds and phase
+timings like ConvergenceReport."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIN = os.path.join(HERE, "integration", "_build", "compare_b200")
+
+
+@pytest.mark.parametrize("case", ["config1", "config1_p4", "functional_norm2", "fas_vcycle"])
+def test_adapter_matches_reference_solve(case):
+    assert os.path.exists(BIN), f"{BIN} missing: build() compiles it where the reference headers exist"
+    out = subprocess.run([BIN, case], capture_output=True, text=True, timeout=600)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert "error" not in line, line
+    assert line["b200_iterations"] == line["ref_iterations"], line
+    assert line["b200_converged"] == line["ref_converged"], line
+    assert line["history_max_rel"] <= (1e-6 if case.startswith("functional") else 1e-9), line
+    assert line["same_shape"] and 0.0 <= line["state_rel_l2"] <= 1e-10, line
+    assert line["b200_iteration_seconds"] == line["b200_iterations"]
+    assert line["b200_timings"] >= 3  # setup, iterations, total

@@ -52,7 +52,54 @@ def test_multiprocess_solve_bitwise_equals_single_process(case, world):
             u[int(d["lo"]):int(d["hi"]) + 1] = d["u"]
         assert np.array_equal(u, ref.state)
     finally:
-        shutil.rmtree(tmp, ignore_errors=True)
-        for f in os.listdir("/dev/shm"):
-            if f.startswith("mocknccl_"):
-                shutil.rmtree(os.path.join("/dev/shm", f), ignore_errors=True)
+        _cleanup(tmp)
+
+
+def _cleanup(tmp):
+    shutil.rmtree(tmp, ignore_errors=True)
+    for f in os.listdir("/dev/shm"):
+        if f.startswith("mocknccl_"):
+            shutil.rmtree(os.path.join("/dev/shm", f), ignore_errors=True)
+
+
+def test_dead_rank_surfaces_as_runtime_fault_within_the_timeout():
+    # parallel.cpp:365-383 / transport.cpp:29-61: a rank that dies must not
+    # hang the others -- they fail with RuntimeFault once the exchange times out
+    lib = _mock_lib()
+    tmp = tempfile.mkdtemp(prefix="mp_")
+    try:
+        idfile = os.path.join(tmp, "nccl.id")
+        env = dict(os.environ, ATM_NCCL_LIB=lib, MP_DIE_RANK="1", MOCKNCCL_TIMEOUT_MS="3000",
+                   MP_TIMEOUT_MS="3000")
+        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), "two_level", str(r),
+                                   "2", idfile, os.path.join(tmp, f"r{r}.npz")], env=env)
+                 for r in range(2)]
+        for p in procs:
+            assert p.wait(timeout=120) == 0
+        import json
+        err = json.load(open(os.path.join(tmp, "r0.npz.json")))
+        assert err["error"] == "RuntimeFault", err
+        assert "timed out" in err["what"], err
+        assert err["seconds"] < 30, err
+    finally:
+        _cleanup(tmp)
+
+
+def test_bench_spawns_its_own_ranks():
+    # bench.py --gpus 2 without a launcher re-launches itself through
+    # torch.distributed.run (every rank on device 0 with BENCH_SHARE_DEVICE
+    # and the host-mediated stand-in): the line reports the 2 ranks
+    lib = _mock_lib()
+    env = dict(os.environ, ATM_NCCL_LIB=lib, BENCH_SHARE_DEVICE="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "bench.py"), "--gpus", "2",
+                          "--steps", "3", "--warmup", "1", "--n-points", "4097", "--no-e2e", "--no-cpu",
+                          "--no-ttt-full"], env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    import json
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    # and a launcher whose world size disagrees with --gpus is refused
+    bad = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "bench.py"), "--gpus", "2"],
+                         env=dict(env, WORLD_SIZE="1"), capture_output=True, text=True, timeout=120)
+    assert bad.returncode != 0

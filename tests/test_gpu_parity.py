@@ -151,7 +151,8 @@ def _golden_solve(name, workers=1, tol_hist=1e-9):
     case = golden_cases()[name]
     args = case["args"]
     ic = golden_array(name, "ic") if case.get("has_ic") else None
-    app, hier, cfg = device_objects(args, ic=ic)
+    files = {"w_file": golden_array(name, "w_file")} if args.get("functional") == "weights" else None
+    app, hier, cfg = device_objects(args, ic=ic, files=files)
     res = T.solve(app, hier, cfg, workers=workers)
     assert res.report.converged == case["converged"]
     assert res.report.iterations == case["iterations"], (res.report.iterations, case["iterations"])
@@ -161,10 +162,39 @@ def _golden_solve(name, workers=1, tol_hist=1e-9):
     dev = np.abs(hist - ref) / np.maximum(np.abs(ref), 1e-300)
     ok = (dev <= tol_hist) | (np.abs(hist - ref) <= tol_hist * scale)
     assert ok.all(), (hist, ref)
-    if case.get("store_u"):
-        u_ref = golden_array(name, "u")
-        assert rel_l2(res.state, u_ref) <= SOLVE_RTOL
+    assert_final_state(name, case, res.state)
     return res
+
+
+def assert_final_state(name, case, state):
+    """Final-state bar against the compiled reference: the whole state when
+    the fixture holds it, else every `row_stride`-th point row (plus the last)
+    and the whole state's 2-norm, each within 1e-10 relative."""
+    state = np.asarray(state).reshape(state.shape[0], -1)
+    if case.get("store_u"):
+        assert rel_l2(state, golden_array(name, "u")) <= SOLVE_RTOL
+    stride = case.get("row_stride")
+    if stride:
+        idx = sorted(set(range(0, state.shape[0], stride)) | {state.shape[0] - 1})
+        rows = golden_array(name, "rows")
+        assert rows.shape == (len(idx), state.shape[1]), rows.shape
+        # (not row by row: at t_f = 1 the heat solution has decayed ~1e-10-fold,
+        # and both fp64 paths carry ~1e-18 absolute rounding from 2^14 steps)
+        assert rel_l2(state[idx], rows) <= SOLVE_RTOL, rel_l2(state[idx], rows)
+    if "u_l2" in case:
+        l2 = float(np.linalg.norm(state))
+        assert abs(l2 - case["u_l2"]) <= SOLVE_RTOL * case["u_l2"], (l2, case["u_l2"])
+
+
+@pytest.mark.parametrize("name", ["functional_norm2", "functional_weights", "functional_norm2_5r"])
+@pytest.mark.parametrize("workers", [1, 3])
+def test_functional_change_matches_reference(name, workers):
+    # NormKind::FunctionalChange (solver.cpp:380-396) with the reference CLI's
+    # u.norm2() and a linear w.u: same iteration count as the compiled
+    # reference; the stopping values are relative changes of nearly equal
+    # numbers (cancellation amplifies the summation-order rounding of f), so
+    # the history is held to 1e-6 relative
+    _golden_solve(name, workers=workers, tol_hist=1e-6)
 
 
 def test_config1_matches_reference():
@@ -211,13 +241,18 @@ def test_histories_bitwise_across_shard_counts(name):
 
 
 def test_fused_norm_equals_full_residual_norm():
+    # the stopping norm sums the per-C-point squares the correction sweep's
+    # tail wrote; the full residual norm re-evaluates every point (F residuals
+    # are exactly zero after a cycle): the same squares, summed over arrays of
+    # different length, hence a different fixed association -- equal to
+    # rounding
     case = golden_cases()["heat_det_65"]
     app, hier, cfg = device_objects(case["args"])
     drv = T.CycleDriver(app, hier, cfg)
     drv.setup()
     norms = drv.iterate(3)
     full = drv.residual_norm()
-    assert full == norms[-1]
+    assert abs(full - norms[-1]) <= 4e-16 * full
 
 
 def test_exact_in_nt_iterations_every_k():
@@ -272,11 +307,14 @@ def test_heat_k_study_iteration_counts(k):
     _golden_solve(f"kstudy_k{k}")
 
 
-@pytest.mark.parametrize("k", [4, 8, 1025])
-def test_config5_shape_iteration_counts(k):
-    # BASELINE config 5 discretisation (n=4095, m=16) at N_t = 2^14, tol 1e-10:
-    # same iteration count as the compiled reference and history within 1e-9
-    _golden_solve(f"config5r_k{k}")
+@pytest.mark.parametrize("m,k", [(16, 1), (16, 2), (16, 4), (16, 8), (16, 1025),
+                                 (64, 1), (64, 2), (64, 4), (64, 8), (64, 257)])
+def test_config5_shape_matches_reference(m, k):
+    # BASELINE config 5 discretisation (n=4095) at N_t = 2^14, tol 1e-10, every
+    # (m, k) cell incl. classical k = N_T + 1: same iteration count as the
+    # compiled reference, history within 1e-9, final state (every 256th row,
+    # the last row, the 2-norm) within 1e-10 relative l2
+    _golden_solve(f"config5r_k{k}" if m == 16 else f"config5r_m{m}_k{k}")
 
 
 def test_config5_shape_bitwise_across_shard_counts():

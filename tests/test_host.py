@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
     missing = [s for s in declared_symbols() if s not in exported]
     assert not missing, missing
-    assert T.lib().atm_abi_version() == 5
+    assert T.lib().atm_abi_version() == 6
 
 
 def test_python_binding_covers_the_abi():
