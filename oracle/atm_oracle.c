@@ -9,6 +9,7 @@
  */
 #include "atm_oracle.h"
 
+#include <float.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -419,7 +420,7 @@ static int gs_bicgstab(const orc_driver* d, double dt, const double* w, const do
     double rr = gs_dot(m, r, r);
     if (rr <= tol2) return 0;
     double r0n = rr, rho = 1.0, alpha = 1.0, om = 1.0;
-    const double eps2 = 1e-30;  /* NumTraits<double>::epsilon()^2, rounded */
+    const double eps2 = DBL_EPSILON * DBL_EPSILON;  /* Eigen BiCGSTAB: NumTraits<double>::epsilon()^2 */
     int it = 0, restarts = 0;
     const int maxit = 2 * m;
     while (rr > tol2 && it < maxit) {

@@ -17,6 +17,7 @@
 // tails; windows: linear / FAS / forward / apply / FAS right-hand side)
 // are those of the scalar backend (common_kernels.cu) and the heat kernels,
 // restating kernels.cpp:7-95 of the reference.
+#include <cfloat>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -426,7 +427,7 @@ __device__ void gs_phi(const CgCoefDev& co, Ctx& cx, const GsVec& g) {
                 loop([&](int i) { d1[0] = fma(g.r0[i], g.r[i], d1[0]); });
                 cluster_sum<1>(d1, cx);
                 rho = d1[0];
-                if (fabs(rho) < 1e-30 * r0n) {
+                if (fabs(rho) < DBL_EPSILON * DBL_EPSILON * r0n) {  // Eigen BiCGSTAB restart rule
                     loop([&](int i) { g.r0[i] = g.r[i]; });
                     rho = r0n = rr;
                     if (restarts++ == 0) lit = 0;

@@ -8,8 +8,8 @@ API by tests/integration/compare_main.cpp.
 
 The bar: the same iteration count and convergence flag, histories within
 1e-9 (relative, or relative to the first norm: tails sit at the rounding
-floor; FunctionalChange values -- differences of nearly equal numbers --
-within 1e-6 relative to themselves or to the tolerance), final level-0 state
+floor; FunctionalChange values -- relative changes of nearly equal numbers,
+so their agreement is absolute -- within 1e-6 relative plus 1e-13 absolute), final level-0 state
 within 1e-10 relative l2; the report carries per-iteration seconds and phase
 timings like ConvergenceReport."""
 from __future__ import annotations

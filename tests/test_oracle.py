@@ -313,3 +313,63 @@ def test_oracle_equals_fresh_reference_run():
     r = d.drive()
     assert r["history"].tolist() == res["history"]
     assert np.array_equal(d.array(0).reshape(-1), u)
+
+
+# The reference has no Phi for configs 2-4 / Gray-Scott; tempo_ref's OracleApp
+# runs the restated Phi (ac_step, h2_solve, gs_step) inside the reference's
+# own CycleDriver (solver.cpp:152-435) over run_parallel's worker threads.
+# The oracle's own cycle restatement must agree with it bitwise on the shapes
+# of BASELINE configs 2, 3, 4 (reduced) and the Gray-Scott desk problem.
+def _ref_small_cases():
+    import paper_2107_09596_b200 as T
+    nx2, n3, nx4 = 15, 64, 31
+    src = T.gaussian_source(nx2)
+    ic3 = 0.05 * O.random_state(3, n3)
+    ic4 = T.fourier_ic(nx4)
+    return {
+        "config2_shape": (dict(problem="heat2d", nx=nx2, folded=0, cg_rtol=1e-12, cg_max=10000, tf=1.0,
+                               n_points=257, m="16", k=4, mode="two-level", guess="random", seed=20,
+                               max_iters=100, tol=1e-10), dict(source_file=src)),
+        "config3_shape": (dict(problem="allen_cahn", n=n3, eps=0.02, length=1.0, newton_tol=1e-12,
+                               newton_max=30, tf=8.0, n_points=1025, m="8,8", k=4, mode="v-cycle",
+                               guess="random", seed=20, max_iters=200, tol=1e-10), dict(ic_file=ic3)),
+        "config4_shape": (dict(problem="heat2d", nx=nx4, folded=1, cg_rtol=1e-12, cg_max=100000, tf=0.125,
+                               n_points=257, m="4,4,4", k=2, mode="v-cycle", guess="random", seed=20,
+                               max_iters=60, tol=1e-10), dict(ic_file=ic4)),
+        "grayscott_nested": (dict(problem="gray_scott", nx=16, tf=64.0, n_points=257, m="16", k=8,
+                                  mode="nested-v", guess="constant", seed=0, max_iters=60, tol=1e-7), {}),
+    }
+
+
+def _oracle_from_ref_args(args, files):
+    kind = {"heat2d": O.HEAT2D, "allen_cahn": O.ALLEN_CAHN, "gray_scott": O.GRAY_SCOTT}[args["problem"]]
+    p = dict(kind=kind, folded=args.get("folded", 1))
+    if kind == O.HEAT2D:
+        nx = args["nx"]
+        p.update(n=nx * nx, nx=nx, cg_rtol=args["cg_rtol"], cg_max=args["cg_max"],
+                 source=files.get("source_file"), ic=files.get("ic_file"))
+    elif kind == O.ALLEN_CAHN:
+        p.update(n=args["n"], eps=args["eps"], length=args["length"], newton_tol=args["newton_tol"],
+                 newton_max=args["newton_max"], ic=files["ic_file"])
+    else:
+        p.update(nx=args["nx"], n=2 * args["nx"] ** 2)
+    g = dict(tf=args["tf"], n_points=args["n_points"], m=[int(x) for x in str(args["m"]).split(",")],
+             k=args["k"])
+    mode = {"two-level": O.TWO_LEVEL, "v-cycle": O.VCYCLE, "nested-v": O.NESTED_V}[args["mode"]]
+    s = dict(mode=mode, relaxation=O.RELAX_F, max_iters=args["max_iters"], tol=args["tol"],
+             initial_guess=O.GUESS_RANDOM if args["guess"] == "random" else O.GUESS_CONSTANT,
+             seed=args["seed"])
+    return O.Driver(p, g, s)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="compiled reference not built here")
+@pytest.mark.parametrize("name", ["config2_shape", "config3_shape", "config4_shape", "grayscott_nested"])
+def test_oracle_cycles_equal_reference_cycle_driver_on_restated_phi(name):
+    args, files = _ref_small_cases()[name]
+    res, u = O.run_ref(dict(args, workers=0), out_u=True, files=files)
+    assert "error" not in res, res
+    d = _oracle_from_ref_args(args, files)
+    r = d.drive()
+    assert r["iterations"] == res["iterations"] and r["converged"] == res["converged"]
+    assert r["history"].tolist() == res["history"]
+    assert np.array_equal(d.array(0).reshape(-1), u)
