@@ -29,8 +29,11 @@ struct CgCoefDev {
     unsigned long long* iters;  // running count of inner (CG / BiCGSTAB) iterations, or null
     int x_smem;           // x and r in shared memory (else xg)
     double* xg;           // global scratch: x, r rows per cluster slot
-    int E;                // 0: generic kernel; > 0: register variant, E elements per thread
+    int E;                // 0: generic kernel; > 0: register variant, E elements per thread;
+                          // 1000 + e: strip kernel, e grid rows per thread (see heat2d_cg.cu)
     int nt;               // threads per CTA
+    int strip;            // 1: strip kernel (one-barrier Chronopoulos-Gear CG, vectors in registers)
+    int sWX, sWY;         // strip kernel: warps across a row (32 columns each), warp-rows per CTA
     // Gray-Scott (prob == 1): periodic nx x nx cells, state [u; v]; one CTA
     // per system, every work vector in shared memory
     int prob;

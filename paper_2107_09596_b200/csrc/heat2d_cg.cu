@@ -31,6 +31,7 @@
 
 #include "cg_kernels.cuh"
 #include "heat_kernels.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -55,6 +56,9 @@ struct Ctx {
     double* rs;              // own r (shared) or null
     CgShared* sh;
     int par;
+    double* ex;              // strip kernel: exchange area (strip_area_doubles)
+    int spar;                // strip kernel: exchange parity
+    uint32_t sph;            // strip kernel: mbarrier phase bit per parity
 };
 
 __device__ __forceinline__ void csync(const Ctx& cx) {
@@ -304,6 +308,391 @@ __device__ void cg_phi_reg(const CgCoefDev& co, Ctx& cx, double* xb, int band, b
 }
 
 // ---------------------------------------------------------------------------
+// Strip kernel (systems up to nx = 255): one cluster barrier per CG iteration.
+//
+// The standard CG above needs three cluster-wide synchronisations per
+// iteration (p halos, p.Ap, r.r) and streams p, x, r through shared memory
+// for every stencil -- it is bound by shared-memory bandwidth and barrier
+// latency, not by the FP64 pipe.  Here every vector lives in registers:
+// lane l of warp (wx, wy) of cluster CTA q owns grid column wx*32 + l and the
+// E consecutive rows q*R + wy*E + [0, E) (R = E * WY), so north/south
+// neighbours are the thread's own registers and west/east ones are lane
+// shuffles; only strip ends (one value per thread) and warp-edge columns (E
+// values per warp) cross threads through shared memory / DSMEM.
+//
+// The iteration is Chronopoulos-Gear CG (same Krylov iterates as h2_solve's
+// CG in exact arithmetic: alpha_i = gamma_i / (p_i, A p_i) with
+// (p_i, A p_i) = delta_i - beta_i gamma_i / alpha_{i-1}):
+//     x += alpha p;  r -= alpha s;  w = A r;  gamma = (r, r), delta = (w, r)
+//     [one barrier: the two dots and w's boundary values]
+//     stop if |r| <= rtol |b|;  beta = gamma / gamma_old;
+//     alpha = gamma / (delta - beta gamma / alpha_old);  p = r + beta p;  s = w + beta s
+// w = A r needs the neighbours' NEW r, which is only published after the
+// next barrier; instead every thread MIRRORS its halo points' r and s with the
+// same recurrences (r_h -= alpha s_h, s_h = w_h + beta s_h, explicit fma in
+// both places), fed only by the neighbours' published w.  The mirror is
+// therefore bitwise the neighbour's own value, and the stencil's inputs are
+// complete after a single barrier.  Dot products: warp trees, then every warp
+// pushes its two partials to every CTA of the cluster; after the barrier each
+// warp sums the cs * NW partials in the same fixed order, so all threads hold
+// bitwise the same alpha and beta (shard-count independent).
+template <int E>
+struct Strip {
+    int WX, WY, NW, C, cs, q, nx;
+    int wx, wy, lane, warp, col;
+    bool hasN, hasS, hasW, hasE;
+    double *sN, *sS, *sW, *sE, *mir, *red;
+    uint64_t* bar;       // two mbarriers (one per parity) counting peer CTAs' st.async bytes
+    uint32_t rx_bytes;   // bytes this CTA receives from its peers per exchange
+};
+
+__host__ __device__ inline size_t strip_area_doubles(int WX, int WY, int E, int cs) {
+    const size_t C = static_cast<size_t>(WX) * 32;
+    return 2 * 2 * static_cast<size_t>(WY) * C          // N / S row slots, two parities
+           + 2 * 2 * static_cast<size_t>(WY) * WX * E   // W / E column slots, two parities
+           + 4 * static_cast<size_t>(WY) * WX * E       // reader-owned r / s mirrors of the W / E columns
+           + 2 * static_cast<size_t>(cs) * WX * WY * 2  // dot partials, two parities
+           + 2;                                         // two mbarriers
+}
+
+template <int E>
+__device__ __forceinline__ Strip<E> strip_init(const CgCoefDev& co, const Ctx& cx, double* area) {
+    Strip<E> S;
+    S.WX = co.sWX;
+    S.WY = co.sWY;
+    S.NW = S.WX * S.WY;
+    S.C = S.WX * 32;
+    S.cs = cx.cs;
+    S.q = cx.q;
+    S.nx = co.nx;
+    S.lane = threadIdx.x & 31;
+    S.warp = threadIdx.x >> 5;
+    S.wx = S.warp % S.WX;
+    S.wy = S.warp / S.WX;
+    S.col = S.wx * 32 + S.lane;
+    S.hasN = S.wy > 0 || S.q > 0;
+    S.hasS = S.wy + 1 < S.WY || S.q + 1 < S.cs;
+    S.hasW = S.wx > 0;
+    S.hasE = S.wx + 1 < S.WX;
+    const size_t rowslots = 2 * static_cast<size_t>(S.WY) * S.C;
+    const size_t colslots = 2 * static_cast<size_t>(S.WY) * S.WX * E;
+    S.sN = area;
+    S.sS = S.sN + rowslots;
+    S.sW = S.sS + rowslots;
+    S.sE = S.sW + colslots;
+    S.mir = S.sE + colslots;
+    S.red = S.mir + 2 * colslots;
+    S.bar = reinterpret_cast<uint64_t*>(S.red + 2 * static_cast<size_t>(S.cs) * S.NW * 2);
+    S.rx_bytes = static_cast<uint32_t>((S.cs - 1) * S.NW * 16 + ((S.q > 0) + (S.q + 1 < S.cs)) * S.C * 8);
+    return S;
+}
+
+// once per kernel (strip geometry, cs > 1): the exchange mbarriers, visible
+// to every peer before anyone sends
+__device__ __forceinline__ void strip_bar_init(const CgCoefDev& co, double* area) {
+    // slots and mirrors across the domain boundary are read but never written:
+    // they must hold zeros
+    {
+        const size_t n = strip_area_doubles(co.sWX, co.sWY, co.E % 1000, co.cs) - 2;
+        for (size_t i = threadIdx.x; i < n; i += blockDim.x) area[i] = 0.0;
+        __syncthreads();
+    }
+    if (co.cs > 1) {
+        if (threadIdx.x == 0) {
+            const int WX = co.sWX, WY = co.sWY, E = co.E % 1000;
+            uint64_t* bar = reinterpret_cast<uint64_t*>(area + strip_area_doubles(WX, WY, E, co.cs) - 2);
+            mbar_init(bar, 1);
+            mbar_init(bar + 1, 1);
+            mbar_fence_init();
+        }
+        cg::this_cluster().sync();
+    }
+}
+
+// W / E column slot of warp (wx, wy) at parity par
+template <int E>
+__device__ __forceinline__ size_t strip_cslot(const Strip<E>& S, int par, int wx) {
+    return ((static_cast<size_t>(par) * S.WY + S.wy) * S.WX + wx) * E;
+}
+
+// hand this thread's boundary values of v (and two dot partials) to the
+// threads / CTAs that read them after the next barrier
+template <int E>
+__device__ __forceinline__ void strip_publish(const Strip<E>& S, int par, const double (&v)[E], double g0,
+                                              double g1) {
+    // peers' data arrive by st.async, counted on their mbarrier for this parity
+    const uint32_t bar = smem_u32(S.bar + par);
+    if (S.cs > 1 && threadIdx.x == 0) mbar_expect_tx_u32(bar, S.rx_bytes);
+    // bottom row -> the north slot of the warp-row below; top row -> the
+    // south slot of the warp-row above (next / previous CTA across the band edge)
+    if (S.wy + 1 < S.WY) {
+        S.sN[(static_cast<size_t>(par) * S.WY + S.wy + 1) * S.C + S.col] = v[E - 1];
+    } else if (S.q + 1 < S.cs) {
+        st_async_f64(mapa_u32(smem_u32(&S.sN[(static_cast<size_t>(par) * S.WY) * S.C + S.col]), S.q + 1), v[E - 1],
+                     mapa_u32(bar, S.q + 1));
+    }
+    if (S.wy > 0) {
+        S.sS[(static_cast<size_t>(par) * S.WY + S.wy - 1) * S.C + S.col] = v[0];
+    } else if (S.q > 0) {
+        st_async_f64(mapa_u32(smem_u32(&S.sS[(static_cast<size_t>(par) * S.WY + S.WY - 1) * S.C + S.col]), S.q - 1),
+                     v[0], mapa_u32(bar, S.q - 1));
+    }
+    // east column -> west slot of the warp to the right; west column -> east
+    // slot of the warp to the left
+    if (S.lane == 31 && S.hasE) {
+        double2* d = reinterpret_cast<double2*>(S.sW + strip_cslot(S, par, S.wx + 1));
+#pragma unroll
+        for (int k = 0; k < E; k += 2) d[k >> 1] = make_double2(v[k], v[k + 1]);
+    }
+    if (S.lane == 0 && S.hasW) {
+        double2* d = reinterpret_cast<double2*>(S.sE + strip_cslot(S, par, S.wx - 1));
+#pragma unroll
+        for (int k = 0; k < E; k += 2) d[k >> 1] = make_double2(v[k], v[k + 1]);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        g0 += __shfl_xor_sync(0xffffffffu, g0, off);
+        g1 += __shfl_xor_sync(0xffffffffu, g1, off);
+    }
+    if (S.lane == 0) {
+        const size_t at = ((static_cast<size_t>(par) * S.cs + S.q) * S.NW + S.warp) * 2;
+        *reinterpret_cast<double2*>(&S.red[at]) = make_double2(g0, g1);
+        const uint32_t a = smem_u32(&S.red[at]);
+        for (int rk = 0; rk < S.cs; ++rk)
+            if (rk != S.q) st_async_v2f64(mapa_u32(a, rk), g0, g1, mapa_u32(bar, rk));
+    }
+}
+
+// the exchange's completion: local slots by the CTA barrier, peers' st.async
+// data by this parity's mbarrier phase (no cluster-wide barrier: a CTA can run
+// at most one exchange ahead of a peer, and each parity's buffers are reused
+// only after every peer has consumed them -- they reply before moving on)
+template <int E>
+__device__ __forceinline__ void strip_sync(const Strip<E>& S, int par, uint32_t& phase) {
+    __syncthreads();
+    if (S.cs > 1) {
+        mbar_wait_cluster(smem_u32(S.bar + par), (phase >> par) & 1u);
+        phase ^= 1u << par;
+    }
+}
+
+// the cluster's two dot products: the cs * NW warp partials summed in the
+// same order by every warp of every CTA (lane-strided sums, then an xor tree:
+// commutative pairings, so all lanes agree bitwise)
+template <int E>
+__device__ __forceinline__ void strip_dots(const Strip<E>& S, int par, double& g0, double& g1) {
+    const int tot = S.cs * S.NW;
+    const double* r = S.red + static_cast<size_t>(par) * tot * 2;
+    double a0 = 0.0, a1 = 0.0;
+    for (int i = S.lane; i < tot; i += 32) {
+        const double2 v = *reinterpret_cast<const double2*>(r + 2 * i);
+        a0 += v.x;
+        a1 += v.y;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, off);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+    }
+    g0 = a0;
+    g1 = a1;
+}
+
+// north / south values published for this thread at parity par (0 across
+// the domain boundary)
+template <int E>
+__device__ __forceinline__ void strip_ns(const Strip<E>& S, int par, double& vn, double& vs) {
+    // slots across the domain boundary are never written: they stay at the
+    // zeros of strip_bar_init (Dirichlet)
+    vn = S.sN[(static_cast<size_t>(par) * S.WY + S.wy) * S.C + S.col];
+    vs = S.sS[(static_cast<size_t>(par) * S.WY + S.wy) * S.C + S.col];
+}
+
+// out = A v on this thread's strip (zero outside the grid); hw / he: the W / E
+// column values for lanes 0 / 31 (zeros across the domain boundary).  FULL:
+// every point of the warp's strips is inside the grid (no masking).
+template <int E, bool FULL>
+__device__ __forceinline__ void strip_apply(const Strip<E>& S, const double (&v)[E], double vn, double vs,
+                                            const double* hw, const double* he, const bool (&ok)[E],
+                                            double diag, double c, double (&out)[E]) {
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        // branch-free: every lane loads the (broadcast) halo pair, lanes 0 / 31 select it
+        const double2 hw2 = reinterpret_cast<const double2*>(hw)[k >> 1];
+        const double2 he2 = reinterpret_cast<const double2*>(he)[k >> 1];
+        const double hwk = (k & 1) ? hw2.y : hw2.x, hek = (k & 1) ? he2.y : he2.x;
+        double west = __shfl_up_sync(0xffffffffu, v[k], 1);
+        double east = __shfl_down_sync(0xffffffffu, v[k], 1);
+        west = S.lane == 0 ? hwk : west;
+        east = S.lane == 31 ? hek : east;
+        const double up = k > 0 ? v[k - 1] : vn;
+        const double dn = k < E - 1 ? v[k + 1] : vs;
+        // h2_apply's association: ((west + east) + row above) + row below
+        const double a = diag * v[k] - c * (((west + east) + up) + dn);
+        out[k] = (FULL || ok[k]) ? a : 0.0;
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void strip_apply(const Strip<E>& S, bool full, const double (&v)[E], double vn,
+                                            double vs, const double* hw, const double* he, const bool (&ok)[E],
+                                            double diag, double c, double (&out)[E]) {
+#ifdef ATM_STRIP_FULL_PATH
+    if (full) strip_apply<E, true>(S, v, vn, vs, hw, he, ok, diag, c, out);
+    else
+#endif
+    strip_apply<E, false>(S, v, vn, vs, hw, he, ok, diag, c, out);
+}
+
+template <int E>
+__device__ void cg_phi_strip(const CgCoefDev& co, Ctx& cx, double* xb, int band, bool forced) {
+    const Strip<E> S = strip_init<E>(co, cx, cx.ex);
+    const double c = co.c, diag = co.diag;
+    const int nx = co.nx;
+    const int lrow0 = S.wy * E;
+    uint32_t phase = cx.sph;
+    bool ok[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) ok[k] = S.col < nx && lrow0 + k < cx.rows;
+    // warp-uniform: no grid padding anywhere in this warp's strips
+    const bool full = S.wx * 32 + 31 < nx && lrow0 + E <= cx.rows;
+    const int base = lrow0 * nx + S.col;
+    // reader-owned mirrors of the W / E halo columns: [rW | sW | rE | sE]
+    const size_t mstride = static_cast<size_t>(S.WY) * S.WX * E;
+    double* mrW = S.mir + (static_cast<size_t>(S.wy) * S.WX + S.wx) * E;
+    double* msW = mrW + mstride;
+    double* mrE = msW + mstride;
+    double* msE = mrE + mstride;
+    // mirror-update lanes: lanes [0, E) own W element `lane`, lanes [16, 16 + E) E element `lane - 16`
+    const int mk = S.lane < 16 ? S.lane : S.lane - 16;
+    const bool mlane = mk < E && (S.lane < 16 ? S.hasW : S.hasE);
+    double* mr = S.lane < 16 ? mrW : mrE;
+    double* ms = S.lane < 16 ? msW : msE;
+    double* slotv = S.lane < 16 ? S.sW : S.sE;
+
+    __syncthreads();  // xb was written by the job code with its own thread map
+    for (int sub = 0; sub < co.substeps; ++sub) {
+        double x[E], r[E], p[E], sv[E], w[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) x[k] = ok[k] ? xb[base + k * nx] : 0.0;
+        // ---- r0 = b - A x0 (x0 = u_prev): x's boundary values first
+        int par = cx.spar;
+        strip_publish(S, par, x, 0.0, 0.0);
+        strip_sync(S, par, phase);
+        double xn, xs;
+        strip_ns(S, par, xn, xs);
+        strip_apply(S, full, x, xn, xs, S.sW + strip_cslot(S, par, S.wx), S.sE + strip_cslot(S, par, S.wx), ok, diag,
+                    c, w);
+        par ^= 1;
+        double bb = 0.0, rr = 0.0;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            double b = x[k];
+            if (forced && ok[k]) b += co.sdt * __ldg(co.src + band + base + k * nx);
+            r[k] = ok[k] ? b - w[k] : 0.0;
+            bb = fma(b, b, bb);
+            rr = fma(r[k], r[k], rr);
+        }
+        // ---- r0's boundary values, |b|^2 and |r0|^2
+        strip_publish(S, par, r, bb, rr);
+        strip_sync(S, par, phase);
+        strip_dots(S, par, bb, rr);
+        double rn, rs;
+        strip_ns(S, par, rn, rs);
+        if (mlane) mr[mk] = slotv[strip_cslot(S, par, S.wx) + mk];
+        __syncwarp();
+        par ^= 1;
+        const double stop = co.rtol * sqrt(bb);
+        // h2_solve's test sqrt(rr) > stop without a square root on the
+        // iteration's critical path: decided by rr against stop^2 with a
+        // relative margin far above the rounding of either side, exact
+        // sqrt only inside the margin
+        const double stop2 = stop * stop, s2hi = stop2 * (1.0 + 1e-12), s2lo = stop2 * (1.0 - 1e-12);
+        auto more = [&](double g) { return g > s2hi || (g >= s2lo && sqrt(g) > stop); };
+        double gamma = rr;
+        int it = 0;
+        if (more(gamma)) {
+            // ---- w0 = A r0, delta0; s0 = w0, p0 = r0
+            strip_apply(S, full, r, rn, rs, mrW, mrE, ok, diag, c, w);
+            double delta = 0.0;
+#pragma unroll
+            for (int k = 0; k < E; ++k) delta = fma(w[k], r[k], delta);
+            strip_publish(S, par, w, delta, 0.0);
+            strip_sync(S, par, phase);
+            double dummy;
+            strip_dots(S, par, delta, dummy);
+            double sn, ss;
+            strip_ns(S, par, sn, ss);
+            if (mlane) ms[mk] = slotv[strip_cslot(S, par, S.wx) + mk];
+            __syncwarp();
+            par ^= 1;
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                p[k] = r[k];
+                sv[k] = w[k];
+            }
+            double alpha = gamma / delta;
+            // 1 / gamma and 1 / alpha of the previous iteration, formed off the
+            // critical path (one division per iteration remains on it)
+            double rgamma = 1.0 / gamma, ralpha = delta / gamma;
+            while (true) {
+                if (it >= co.cg_max) {
+                    if (threadIdx.x == 0 && cx.q == 0) atomicExch(co.fail, 1);
+                    break;
+                }
+                // x += alpha p, r -= alpha s (own points and mirrored halo points)
+                double g = 0.0;
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    x[k] = fma(alpha, p[k], x[k]);
+                    r[k] = fma(-alpha, sv[k], r[k]);
+                    g = fma(r[k], r[k], g);
+                }
+                rn = fma(-alpha, sn, rn);
+                rs = fma(-alpha, ss, rs);
+                if (mlane) mr[mk] = fma(-alpha, ms[mk], mr[mk]);
+                __syncwarp();
+                // w = A r, delta = (w, r)
+                strip_apply(S, full, r, rn, rs, mrW, mrE, ok, diag, c, w);
+                double d = 0.0;
+#pragma unroll
+                for (int k = 0; k < E; ++k) d = fma(w[k], r[k], d);
+                strip_publish(S, par, w, g, d);
+                strip_sync(S, par, phase);
+                strip_dots(S, par, g, d);
+                double wn, ws;
+                strip_ns(S, par, wn, ws);
+                const double wh = mlane ? slotv[strip_cslot(S, par, S.wx) + mk] : 0.0;
+                par ^= 1;
+                ++it;
+                if (!more(g)) break;
+                const double beta = g * rgamma;
+                const double den = d - beta * g * ralpha;
+                alpha = g / den;
+                rgamma = 1.0 / g;
+                ralpha = den * rgamma;
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    p[k] = fma(beta, p[k], r[k]);
+                    sv[k] = fma(beta, sv[k], w[k]);
+                }
+                sn = fma(beta, sn, wn);
+                ss = fma(beta, ss, ws);
+                if (mlane) ms[mk] = fma(beta, ms[mk], wh);
+                // (the next mirror read of ms is after this warp's __syncwarp)
+            }
+        }
+        cx.spar = par;
+        cx.sph = phase;
+        if (co.iters && threadIdx.x == 0 && cx.q == 0) atomicAdd(co.iters, static_cast<unsigned long long>(it));
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+            if (ok[k]) xb[base + k * nx] = x[k];
+    }
+    __syncthreads();  // the job code reads xb with its own thread map
+}
+
+// ---------------------------------------------------------------------------
 // Gray-Scott Phi (gray_scott.cpp:91-190): backward Euler sub-steps, Newton
 // on F(w) = w - w_prev - dt f(w) with stop = max(tol, tol |F_0|), the
 // Jacobian J = I - dt f'(w) applied matrix-free, J delta = F by BiCGSTAB with
@@ -514,6 +903,8 @@ __device__ __forceinline__ void cg_phi_any(const CgCoefDev& co, Ctx& cx, double*
         GsVec g{xb, xb + m, xb + 2 * m, xb + 3 * m, xb + 4 * m, xb + 5 * m, xb + 6 * m, xb + 7 * m,
                 xb + 8 * m, xb + 9 * m};
         gs_phi(co, cx, g);
+    } else if constexpr (E >= 1000) {
+        cg_phi_strip<E % 1000>(co, cx, xb, band, forced);
     } else if constexpr (E > 0) {
         cg_phi_reg<E>(co, cx, xb, band, forced);
     } else {
@@ -543,13 +934,17 @@ __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned 
     cx.dr = cx.nt - cx.dq * co.nx;
     cx.sh = reinterpret_cast<CgShared*>(smem);
     cx.ps = reinterpret_cast<double*>(smem + sizeof(CgShared));
-    const size_t psn = co.prob == 1 ? 0 : static_cast<size_t>(co.R + 2) * cx.W;
+    const size_t psn = (co.prob == 1 || co.strip) ? 0 : static_cast<size_t>(co.R + 2) * cx.W;
     cx.xs = co.x_smem ? cx.ps + psn : nullptr;
-    cx.rs = co.x_smem ? cx.ps + psn + static_cast<size_t>(co.R) * co.nx : nullptr;
+    cx.rs = (co.x_smem && !co.strip) ? cx.ps + psn + static_cast<size_t>(co.R) * co.nx : nullptr;
+    cx.ex = co.strip ? cx.ps + static_cast<size_t>(co.R) * co.nx : nullptr;
     cx.par = 0;
+    cx.spar = 0;
+    cx.sph = 0;
     // zero p (padding columns and the domain-boundary halo rows stay zero)
     for (size_t i = threadIdx.x; i < psn; i += blockDim.x) cx.ps[i] = 0.0;
     __syncthreads();
+    if (co.strip) strip_bar_init(co, cx.ex);
 }
 
 // this CTA's band of the cluster's x and r (shared, or two global scratch
@@ -565,7 +960,7 @@ __device__ __forceinline__ double* r_band(const CgCoefDev& co, const Ctx& cx, in
 }
 
 template <int E>
-__global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kernel(const __grid_constant__ CgSweepArgs a) {
+__global__ void __launch_bounds__(E >= 2000 ? 256 : E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kernel(const __grid_constant__ CgSweepArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx cx;
     ctx_init(cx, a.co, smem);
@@ -640,7 +1035,7 @@ __global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kerne
 }
 
 template <int E>
-__global__ void __launch_bounds__(E > 0 ? 512 : kMaxCgThreads, 1) cg_window_kernel(const __grid_constant__ CgWindowArgs a) {
+__global__ void __launch_bounds__(E >= 2000 ? 256 : E > 0 ? 512 : kMaxCgThreads, 1) cg_window_kernel(const __grid_constant__ CgWindowArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx cx;
     ctx_init(cx, a.co, smem);
@@ -759,6 +1154,11 @@ CgKernels cg_kernels(int E) {
         case 4: return cg_k<4>();
         case 8: return cg_k<8>();
         case 16: return cg_k<16>();
+        case 1002: return cg_k<1002>();
+        case 1004: return cg_k<1004>();
+        case 2008: return cg_k<2008>();
+        case 2012: return cg_k<2012>();
+        case 2016: return cg_k<2016>();
         default: return cg_k<0>();
     }
 }
@@ -794,9 +1194,46 @@ int cg_launch(const void* fn, const CgCoefDev& co, int jobs, void** args, cudaSt
 
 }  // namespace
 
+// strip kernel geometry: WX warps across (32 columns each), WY warp-rows of
+// E grid rows per CTA (R = E WY), cs = ceil(nx / R) CTAs per cluster (<= 16),
+// at most 512 threads per CTA (5 E doubles of CG state per thread in
+// registers); false when nx needs more than 16 CTAs of this shape
+static bool strip_geometry(int nx, CgCoefDev& co) {
+    if (const char* e = std::getenv("ATM_CG_STRIP"))
+        if (std::atoi(e) == 0) return false;
+    const int WX = (nx + 31) / 32;
+    if (WX > 16) return false;
+    // E >= 8: 256-thread CTAs (up to 255 registers: 5 E doubles of CG state
+    // per thread plus the stencil's temporaries); E < 8: 512-thread CTAs
+    int Es[5] = {16, 12, 8, 4, 2};
+    if (const char* e = std::getenv("ATM_CG_STRIP_E")) Es[0] = Es[1] = Es[2] = Es[3] = Es[4] = std::atoi(e);
+    for (int E : Es) {
+        const int maxt = E >= 8 ? 256 : 512;
+        if (32 * WX > maxt) continue;
+        int WY = std::min(maxt / (32 * WX), (nx + E - 1) / E);
+        if (const char* e = std::getenv("ATM_CG_STRIP_WY")) WY = std::min(WY, std::atoi(e));
+        if (WY < 1) continue;
+        const int R = E * WY;
+        const int cs = (nx + R - 1) / R;
+        if (cs > 16) continue;
+        co.strip = 1;
+        co.sWX = WX;
+        co.sWY = WY;
+        co.cs = cs;
+        co.R = R;
+        co.x_smem = 1;
+        co.E = (E >= 8 ? 2000 : 1000) + E;
+        co.nt = 32 * WX * WY;
+        return true;
+    }
+    return false;
+}
+
 void cg_geometry(int nx, CgCoefDev& co) {
     co.nx = nx;
     co.n = nx * nx;
+    co.strip = 0;
+    if (strip_geometry(nx, co)) return;
     const size_t red = sizeof(CgShared) + 64;
     // smallest cluster holding p, x and r on chip (up to 4 CTAs); else the
     // smallest cluster holding p, with x and r in global scratch rows
@@ -857,6 +1294,9 @@ bool gs_geometry(int nx, CgCoefDev& co, int cs) {
 
 size_t cg_smem_bytes(const CgCoefDev& co) {
     if (co.prob == 1) return sizeof(CgShared) + (co.x_smem ? 10 * static_cast<size_t>(co.n) * 8 : 0);
+    if (co.strip)
+        return sizeof(CgShared) + static_cast<size_t>(co.R) * co.nx * 8 +
+               strip_area_doubles(co.sWX, co.sWY, co.E % 1000, co.cs) * 8;
     size_t b = sizeof(CgShared) + static_cast<size_t>(co.R + 2) * (co.nx + 2) * 8;
     if (co.x_smem) b += 2 * static_cast<size_t>(co.R) * co.nx * 8;
     return b;
