@@ -67,6 +67,26 @@ def read_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def fp64_peak():
+    """Measured FP64 peak of this GPU (tools/ubench/fp64_peak: independent
+    DFMA chains on every SM, CUDA events), the secondary roofline of the
+    Phi-chain kernels; MEASURED_PEAKS.json carries no FP64 figure."""
+    exe = os.path.join(ROOT, "tools", "ubench", "fp64_peak")
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
+        d = json.loads(out.strip().splitlines()[-1])
+        return float(d["fp64_tflops"]), "measured on this GPU at bench start (tools/ubench/fp64_peak)"
+    except Exception:
+        return 37.13, "fallback: tools/ubench/fp64_peak on a B200 of this pool (profiles/fp64_peak_r02.json)"
+
+
+# algorithmic FP64 work of one heat1d Phi application (SURVEY 8(d)): the
+# serial Thomas solve of heat1d.cpp:47-60 with its constant-coefficient
+# factors precomputed -- one FMA and one MUL forward, one FMA backward per
+# unknown = 5 flops per unknown (an FMA counts 2)
+FLOPS_PER_PHI_DOF = 5.0
+
+
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -393,6 +413,22 @@ def main():
         except Exception:
             traffic = None
     phase_ms = {k: 1e3 * (v[0] - t_before.get(k, (0.0, 0))[0]) / args.steps for k, v in t_after.items()}
+    # FP64 roofline of the two Phi-chain (latency-bound) kernels: the relax
+    # F-sweep (one Phi per fine step of this rank: its F points and the
+    # restriction tails) and the coarse window kernel (window p applies
+    # min(p, k-1) Psi, kernels.cpp:53-61, for this rank's coarse points)
+    fpk, fpk_src = fp64_peak() if rank == 0 else (None, None)
+    relax_phi = my_F + my_iv
+    lo1, hi1 = rr["lo"][1], rr["hi"][1]
+    win_psi = sum(min(p, W["k"] - 1) for p in range(lo1, hi1 + 1))
+    fp64 = {}
+    for name, key, cnt in (("relax F-sweep (heat_sweep_kernel, restriction tail)", "sweep_relax", relax_phi),
+                           ("coarse windows (heat_window_linear_kernel)", "coarse", win_psi)):
+        ms_k = phase_ms.get(key)
+        if ms_k and fpk:
+            tf = FLOPS_PER_PHI_DOF * n * cnt / (ms_k / 1e3) / 1e12
+            fp64[key] = {"kernel": name, "phi_per_launch": cnt, "flops_per_phi": FLOPS_PER_PHI_DOF * n,
+                         "avg_launch_ms": ms_k, "achieved": tf, "frac": tf / fpk}
 
     line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -404,6 +440,8 @@ def main():
                          "kernel": "heat_sweep_kernel<32,128,3> (level-0 correction F-sweep + C-point norm tail)",
                          "algorithmic_bytes_per_launch": sweep_bytes, "avg_launch_ms": sweep_ms,
                          "peak_source": peak_src},
+            "roofline_fp64": {"bound": "fp64 (Phi-chain latency)", "peak": fpk, "unit": "TFLOP/s",
+                              "peak_source": fpk_src, "kernels": fp64},
             "gpu_launches": launches * args.steps,
             "phase_ms_per_step": phase_ms,
             "last_norm": float(norms[-1])}
