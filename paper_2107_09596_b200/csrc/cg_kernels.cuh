@@ -34,6 +34,13 @@ struct CgCoefDev {
     int nt;               // threads per CTA
     int strip;            // 1: strip kernel (one-barrier Chronopoulos-Gear CG, vectors in registers)
     int sWX, sWY;         // strip kernel: warps across a row (32 columns each), warp-rows per CTA
+    // strip kernel, group mode (systems too large for one 16-CTA cluster):
+    // cs CTAs of a cooperative grid per system, exchanging through global
+    // memory (gex: per group rows + partials, gflag: per CTA sequence flags);
+    // p and s in shared memory
+    int glob;
+    double* gex;
+    unsigned long long* gflag;
     // Gray-Scott (prob == 1): periodic nx x nx cells, state [u; v]; one CTA
     // per system, every work vector in shared memory
     int prob;
@@ -74,6 +81,8 @@ void cg_geometry(int nx, CgCoefDev& co);
 // scratch (few concurrent systems: more SMs per Phi)
 bool gs_geometry(int nx, CgCoefDev& co, int cs = 1);
 size_t cg_smem_bytes(const CgCoefDev& co);
+// group mode: doubles of exchange area per group (gex), flags per group = cs
+size_t cg_glob_doubles_per_group(const CgCoefDev& co);
 // clusters that can be resident at once (the number of x scratch rows needed)
 int cg_max_clusters(const CgCoefDev& co);
 int launch_cg_sweep(const CgSweepArgs& a, cudaStream_t s);

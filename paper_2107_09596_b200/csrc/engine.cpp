@@ -730,6 +730,22 @@ void Engine::build_coefs(Shard& s) {
                 }
             }
             c.xg = d_xg_;
+            if (c.glob) {
+                // group mode: per group the exchange rows / partials, and one
+                // sequence flag per CTA (cg_kernels.cuh)
+                const size_t ng = static_cast<size_t>(cg_max_clusters(c));
+                if (!d_gex_) {
+                    const size_t per = cg_glob_doubles_per_group(c);
+                    void* p = nullptr;
+                    CK(cudaMalloc(&p, sizeof(double) * per * ng + sizeof(unsigned long long) * ng * c.cs));
+                    CK(cudaMemset(p, 0, sizeof(double) * per * ng + sizeof(unsigned long long) * ng * c.cs));
+                    gallocs_.push_back(p);
+                    d_gex_ = static_cast<double*>(p);
+                    d_gflag_ = reinterpret_cast<unsigned long long*>(d_gex_ + per * ng);
+                }
+                c.gex = d_gex_;
+                c.gflag = d_gflag_;
+            }
         } else {
             ScalarCoefDev& c = Lv.sco;
             if (kind_ == ATM_PHI_DAHLQUIST) {

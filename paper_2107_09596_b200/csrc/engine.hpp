@@ -236,6 +236,8 @@ private:
     unsigned long long* d_inner_ = nullptr;  // inner CG / BiCGSTAB iterations run so far
     double* d_src_ = nullptr; // heat2d source f
     double* d_xg_ = nullptr;  // heat2d CG x scratch (one row per resident cluster)
+    double* d_gex_ = nullptr;  // heat2d CG group mode: exchange rows / partials per group
+    unsigned long long* d_gflag_ = nullptr;  // heat2d CG group mode: per-CTA sequence flags
     void check_newton();
     std::vector<void*> gallocs_;
     // NCCL (world > 1)

@@ -59,6 +59,7 @@ struct Ctx {
     double* ex;              // strip kernel: exchange area (strip_area_doubles)
     int spar;                // strip kernel: exchange parity
     uint32_t sph;            // strip kernel: mbarrier phase bit per parity
+    unsigned long long gseq; // strip kernel, group mode: exchanges so far in this launch
 };
 
 __device__ __forceinline__ void csync(const Ctx& cx) {
@@ -344,7 +345,18 @@ struct Strip {
     double *sN, *sS, *sW, *sE, *mir, *red;
     uint64_t* bar;       // two mbarriers (one per parity) counting peer CTAs' st.async bytes
     uint32_t rx_bytes;   // bytes this CTA receives from its peers per exchange
+    int rcs, rq;         // dot-partial slots: [par][rcs][NW] (group mode: local, rcs = 1)
+    // group mode: this group's global rows [par][cs][top | bottom][C],
+    // CTA partials [par][cs] and sequence flags [cs]
+    double* grows;
+    double2* gred;
+    unsigned long long* gflag;
+    double *pbuf, *sbuf;  // group mode: p and s, [E][nt] each
 };
+
+__host__ __device__ inline size_t glob_doubles(int cs, int C) {
+    return 2 * 2 * static_cast<size_t>(cs) * C + 2 * 2 * static_cast<size_t>(cs);
+}
 
 __host__ __device__ inline size_t strip_area_doubles(int WX, int WY, int E, int cs) {
     const size_t C = static_cast<size_t>(WX) * 32;
@@ -382,8 +394,23 @@ __device__ __forceinline__ Strip<E> strip_init(const CgCoefDev& co, const Ctx& c
     S.sE = S.sW + colslots;
     S.mir = S.sE + colslots;
     S.red = S.mir + 2 * colslots;
-    S.bar = reinterpret_cast<uint64_t*>(S.red + 2 * static_cast<size_t>(S.cs) * S.NW * 2);
+    S.rcs = co.glob ? 1 : S.cs;
+    S.rq = co.glob ? 0 : S.q;
+    S.bar = reinterpret_cast<uint64_t*>(S.red + 2 * static_cast<size_t>(S.rcs) * S.NW * 2);
     S.rx_bytes = static_cast<uint32_t>((S.cs - 1) * S.NW * 16 + ((S.q > 0) + (S.q + 1 < S.cs)) * S.C * 8);
+    S.grows = nullptr;
+    S.gred = nullptr;
+    S.gflag = nullptr;
+    S.pbuf = S.sbuf = nullptr;
+    if (co.glob) {
+        const int group = blockIdx.x / S.cs;
+        double* gb = co.gex + static_cast<size_t>(group) * glob_doubles(S.cs, S.C);
+        S.grows = gb;
+        S.gred = reinterpret_cast<double2*>(gb + 2 * 2 * static_cast<size_t>(S.cs) * S.C);
+        S.gflag = co.gflag + static_cast<size_t>(group) * S.cs;
+        S.pbuf = reinterpret_cast<double*>(S.bar + 2);
+        S.sbuf = S.pbuf + static_cast<size_t>(E) * blockDim.x;
+    }
     return S;
 }
 
@@ -393,11 +420,11 @@ __device__ __forceinline__ void strip_bar_init(const CgCoefDev& co, double* area
     // slots and mirrors across the domain boundary are read but never written:
     // they must hold zeros
     {
-        const size_t n = strip_area_doubles(co.sWX, co.sWY, co.E % 1000, co.cs) - 2;
+        const size_t n = strip_area_doubles(co.sWX, co.sWY, co.E % 1000, co.glob ? 1 : co.cs) - 2;
         for (size_t i = threadIdx.x; i < n; i += blockDim.x) area[i] = 0.0;
         __syncthreads();
     }
-    if (co.cs > 1) {
+    if (co.cs > 1 && !co.glob) {
         if (threadIdx.x == 0) {
             const int WX = co.sWX, WY = co.sWY, E = co.E % 1000;
             uint64_t* bar = reinterpret_cast<uint64_t*>(area + strip_area_doubles(WX, WY, E, co.cs) - 2);
@@ -417,22 +444,27 @@ __device__ __forceinline__ size_t strip_cslot(const Strip<E>& S, int par, int wx
 
 // hand this thread's boundary values of v (and two dot partials) to the
 // threads / CTAs that read them after the next barrier
-template <int E>
+template <int E, bool G>
 __device__ __forceinline__ void strip_publish(const Strip<E>& S, int par, const double (&v)[E], double g0,
                                               double g1) {
     // peers' data arrive by st.async, counted on their mbarrier for this parity
     const uint32_t bar = smem_u32(S.bar + par);
-    if (S.cs > 1 && threadIdx.x == 0) mbar_expect_tx_u32(bar, S.rx_bytes);
+    if (!G && S.cs > 1 && threadIdx.x == 0) mbar_expect_tx_u32(bar, S.rx_bytes);
     // bottom row -> the north slot of the warp-row below; top row -> the
-    // south slot of the warp-row above (next / previous CTA across the band edge)
+    // south slot of the warp-row above (next / previous CTA across the band
+    // edge: DSMEM st.async, or the group's global rows)
     if (S.wy + 1 < S.WY) {
         S.sN[(static_cast<size_t>(par) * S.WY + S.wy + 1) * S.C + S.col] = v[E - 1];
+    } else if (G) {
+        if (S.q + 1 < S.cs) __stcg(&S.grows[((static_cast<size_t>(par) * S.cs + S.q) * 2 + 1) * S.C + S.col], v[E - 1]);
     } else if (S.q + 1 < S.cs) {
         st_async_f64(mapa_u32(smem_u32(&S.sN[(static_cast<size_t>(par) * S.WY) * S.C + S.col]), S.q + 1), v[E - 1],
                      mapa_u32(bar, S.q + 1));
     }
     if (S.wy > 0) {
         S.sS[(static_cast<size_t>(par) * S.WY + S.wy - 1) * S.C + S.col] = v[0];
+    } else if (G) {
+        if (S.q > 0) __stcg(&S.grows[((static_cast<size_t>(par) * S.cs + S.q) * 2) * S.C + S.col], v[0]);
     } else if (S.q > 0) {
         st_async_f64(mapa_u32(smem_u32(&S.sS[(static_cast<size_t>(par) * S.WY + S.WY - 1) * S.C + S.col]), S.q - 1),
                      v[0], mapa_u32(bar, S.q - 1));
@@ -455,20 +487,91 @@ __device__ __forceinline__ void strip_publish(const Strip<E>& S, int par, const 
         g1 += __shfl_xor_sync(0xffffffffu, g1, off);
     }
     if (S.lane == 0) {
-        const size_t at = ((static_cast<size_t>(par) * S.cs + S.q) * S.NW + S.warp) * 2;
+        const size_t at = ((static_cast<size_t>(par) * S.rcs + S.rq) * S.NW + S.warp) * 2;
         *reinterpret_cast<double2*>(&S.red[at]) = make_double2(g0, g1);
-        const uint32_t a = smem_u32(&S.red[at]);
-        for (int rk = 0; rk < S.cs; ++rk)
-            if (rk != S.q) st_async_v2f64(mapa_u32(a, rk), g0, g1, mapa_u32(bar, rk));
+        if (!G) {
+            const uint32_t a = smem_u32(&S.red[at]);
+            for (int rk = 0; rk < S.cs; ++rk)
+                if (rk != S.q) st_async_v2f64(mapa_u32(a, rk), g0, g1, mapa_u32(bar, rk));
+        }
     }
+}
+
+__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_gpu_add_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// group mode exchange: the CTA's warp partials (local slots at parity par)
+// summed in a fixed tree, published with the boundary rows (already stored)
+// under this CTA's sequence flag; then wait for every CTA of the group.
+// Cooperative launch: all CTAs of the grid are co-resident.
+__device__ __forceinline__ void glob_sync(const double* red_local, int NW, double2* gred, unsigned long long* gflag,
+                                          int cs, int q, int par, unsigned long long seq) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double a0 = 0.0, a1 = 0.0;
+        if (lane < NW) {
+            const double2 v = *reinterpret_cast<const double2*>(red_local + (static_cast<size_t>(par) * NW + lane) * 2);
+            a0 = v.x;
+            a1 = v.y;
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, off);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+        }
+        if (lane == 0) {
+            __stcg(&gred[static_cast<size_t>(par) * cs + q], make_double2(a0, a1));
+            // one arrival on the group's counter, released at gpu scope:
+            // cumulative over the CTA's row stores, ordered before it by the
+            // barrier above; then wait for all cs arrivals of this exchange
+            red_release_gpu_add_u64(&gflag[0], 1ull);
+            const unsigned long long want = seq * static_cast<unsigned long long>(cs);
+            while (ld_acquire_gpu_u64(&gflag[0]) < want) {
+            }
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+}
+
+// group mode: the cs CTA partials, in CTA order, xor tree (all lanes agree)
+__device__ __forceinline__ void glob_dots(const double2* gred, int cs, int par, double& g0, double& g1) {
+    const int lane = threadIdx.x & 31;
+    double a0 = 0.0, a1 = 0.0;
+    for (int i = lane; i < cs; i += 32) {
+        const double2 v = __ldcg(&gred[static_cast<size_t>(par) * cs + i]);
+        a0 += v.x;
+        a1 += v.y;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, off);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+    }
+    g0 = a0;
+    g1 = a1;
 }
 
 // the exchange's completion: local slots by the CTA barrier, peers' st.async
 // data by this parity's mbarrier phase (no cluster-wide barrier: a CTA can run
 // at most one exchange ahead of a peer, and each parity's buffers are reused
 // only after every peer has consumed them -- they reply before moving on)
-template <int E>
-__device__ __forceinline__ void strip_sync(const Strip<E>& S, int par, uint32_t& phase) {
+template <int E, bool G>
+__device__ __forceinline__ void strip_sync(const Strip<E>& S, int par, uint32_t& phase, unsigned long long& seq) {
+    if (G) {
+        glob_sync(S.red, S.NW, S.gred, S.gflag, S.cs, S.q, par, ++seq);
+        return;
+    }
     __syncthreads();
     if (S.cs > 1) {
         mbar_wait_cluster(smem_u32(S.bar + par), (phase >> par) & 1u);
@@ -479,8 +582,12 @@ __device__ __forceinline__ void strip_sync(const Strip<E>& S, int par, uint32_t&
 // the cluster's two dot products: the cs * NW warp partials summed in the
 // same order by every warp of every CTA (lane-strided sums, then an xor tree:
 // commutative pairings, so all lanes agree bitwise)
-template <int E>
+template <int E, bool G>
 __device__ __forceinline__ void strip_dots(const Strip<E>& S, int par, double& g0, double& g1) {
+    if (G) {
+        glob_dots(S.gred, S.cs, par, g0, g1);
+        return;
+    }
     const int tot = S.cs * S.NW;
     const double* r = S.red + static_cast<size_t>(par) * tot * 2;
     double a0 = 0.0, a1 = 0.0;
@@ -500,12 +607,19 @@ __device__ __forceinline__ void strip_dots(const Strip<E>& S, int par, double& g
 
 // north / south values published for this thread at parity par (0 across
 // the domain boundary)
-template <int E>
+template <int E, bool G>
 __device__ __forceinline__ void strip_ns(const Strip<E>& S, int par, double& vn, double& vs) {
     // slots across the domain boundary are never written: they stay at the
     // zeros of strip_bar_init (Dirichlet)
     vn = S.sN[(static_cast<size_t>(par) * S.WY + S.wy) * S.C + S.col];
     vs = S.sS[(static_cast<size_t>(par) * S.WY + S.wy) * S.C + S.col];
+    if (G) {
+        if (S.wy == 0)
+            vn = S.q > 0 ? __ldcg(&S.grows[((static_cast<size_t>(par) * S.cs + S.q - 1) * 2 + 1) * S.C + S.col]) : 0.0;
+        if (S.wy + 1 == S.WY)
+            vs = S.q + 1 < S.cs ? __ldcg(&S.grows[((static_cast<size_t>(par) * S.cs + S.q + 1) * 2) * S.C + S.col])
+                                : 0.0;
+    }
 }
 
 // out = A v on this thread's strip (zero outside the grid); hw / he: the W / E
@@ -544,13 +658,14 @@ __device__ __forceinline__ void strip_apply(const Strip<E>& S, bool full, const 
     strip_apply<E, false>(S, v, vn, vs, hw, he, ok, diag, c, out);
 }
 
-template <int E>
+template <int E, bool G>
 __device__ void cg_phi_strip(const CgCoefDev& co, Ctx& cx, double* xb, int band, bool forced) {
     const Strip<E> S = strip_init<E>(co, cx, cx.ex);
     const double c = co.c, diag = co.diag;
     const int nx = co.nx;
     const int lrow0 = S.wy * E;
     uint32_t phase = cx.sph;
+    unsigned long long seq = cx.gseq;
     bool ok[E];
 #pragma unroll
     for (int k = 0; k < E; ++k) ok[k] = S.col < nx && lrow0 + k < cx.rows;
@@ -569,36 +684,42 @@ __device__ void cg_phi_strip(const CgCoefDev& co, Ctx& cx, double* xb, int band,
     double* mr = S.lane < 16 ? mrW : mrE;
     double* ms = S.lane < 16 ? msW : msE;
     double* slotv = S.lane < 16 ? S.sW : S.sE;
+    // group mode: x stays in the shared band xb, p and s in shared memory
+    // [k][thread]; otherwise all CG vectors are registers
+    double* const pg = S.pbuf + threadIdx.x;
+    double* const sg = S.sbuf + threadIdx.x;
+    const int nt = blockDim.x;
 
     __syncthreads();  // xb was written by the job code with its own thread map
     for (int sub = 0; sub < co.substeps; ++sub) {
-        double x[E], r[E], p[E], sv[E], w[E];
+        // xr: x (registers), or in group mode x0 for the prologue only
+        double xr[E], r[E], w[E], p[G ? 1 : E], sv[G ? 1 : E];
 #pragma unroll
-        for (int k = 0; k < E; ++k) x[k] = ok[k] ? xb[base + k * nx] : 0.0;
+        for (int k = 0; k < E; ++k) xr[k] = ok[k] ? xb[base + k * nx] : 0.0;
         // ---- r0 = b - A x0 (x0 = u_prev): x's boundary values first
         int par = cx.spar;
-        strip_publish(S, par, x, 0.0, 0.0);
-        strip_sync(S, par, phase);
+        strip_publish<E, G>(S, par, xr, 0.0, 0.0);
+        strip_sync<E, G>(S, par, phase, seq);
         double xn, xs;
-        strip_ns(S, par, xn, xs);
-        strip_apply(S, full, x, xn, xs, S.sW + strip_cslot(S, par, S.wx), S.sE + strip_cslot(S, par, S.wx), ok, diag,
+        strip_ns<E, G>(S, par, xn, xs);
+        strip_apply(S, full, xr, xn, xs, S.sW + strip_cslot(S, par, S.wx), S.sE + strip_cslot(S, par, S.wx), ok, diag,
                     c, w);
         par ^= 1;
         double bb = 0.0, rr = 0.0;
 #pragma unroll
         for (int k = 0; k < E; ++k) {
-            double b = x[k];
+            double b = xr[k];
             if (forced && ok[k]) b += co.sdt * __ldg(co.src + band + base + k * nx);
             r[k] = ok[k] ? b - w[k] : 0.0;
             bb = fma(b, b, bb);
             rr = fma(r[k], r[k], rr);
         }
         // ---- r0's boundary values, |b|^2 and |r0|^2
-        strip_publish(S, par, r, bb, rr);
-        strip_sync(S, par, phase);
-        strip_dots(S, par, bb, rr);
+        strip_publish<E, G>(S, par, r, bb, rr);
+        strip_sync<E, G>(S, par, phase, seq);
+        strip_dots<E, G>(S, par, bb, rr);
         double rn, rs;
-        strip_ns(S, par, rn, rs);
+        strip_ns<E, G>(S, par, rn, rs);
         if (mlane) mr[mk] = slotv[strip_cslot(S, par, S.wx) + mk];
         __syncwarp();
         par ^= 1;
@@ -609,87 +730,126 @@ __device__ void cg_phi_strip(const CgCoefDev& co, Ctx& cx, double* xb, int band,
         // sqrt only inside the margin
         const double stop2 = stop * stop, s2hi = stop2 * (1.0 + 1e-12), s2lo = stop2 * (1.0 - 1e-12);
         auto more = [&](double g) { return g > s2hi || (g >= s2lo && sqrt(g) > stop); };
-        double gamma = rr;
         int it = 0;
-        if (more(gamma)) {
-            // ---- w0 = A r0, delta0; s0 = w0, p0 = r0
+        if (more(rr)) {
+            // ---- w0 = A r0, delta0
             strip_apply(S, full, r, rn, rs, mrW, mrE, ok, diag, c, w);
             double delta = 0.0;
 #pragma unroll
             for (int k = 0; k < E; ++k) delta = fma(w[k], r[k], delta);
-            strip_publish(S, par, w, delta, 0.0);
-            strip_sync(S, par, phase);
+            strip_publish<E, G>(S, par, w, delta, 0.0);
+            strip_sync<E, G>(S, par, phase, seq);
             double dummy;
-            strip_dots(S, par, delta, dummy);
-            double sn, ss;
-            strip_ns(S, par, sn, ss);
-            if (mlane) ms[mk] = slotv[strip_cslot(S, par, S.wx) + mk];
-            __syncwarp();
+            strip_dots<E, G>(S, par, delta, dummy);
+            double wn, ws;
+            strip_ns<E, G>(S, par, wn, ws);
+            double wh = mlane ? slotv[strip_cslot(S, par, S.wx) + mk] : 0.0;
             par ^= 1;
-#pragma unroll
-            for (int k = 0; k < E; ++k) {
-                p[k] = r[k];
-                sv[k] = w[k];
-            }
-            double alpha = gamma / delta;
+            double alpha = rr / delta, beta = 0.0;
             // 1 / gamma and 1 / alpha of the previous iteration, formed off the
             // critical path (one division per iteration remains on it)
-            double rgamma = 1.0 / gamma, ralpha = delta / gamma;
-            while (true) {
+            double rgamma = 1.0 / rr, ralpha = delta / rr;
+            // p = s = 0 with beta = 0 makes the first update p0 = r0, s0 = w0
+            double sn = 0.0, ss = 0.0;
+            if (mlane) ms[mk] = 0.0;
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                if constexpr (G) {
+                    pg[k * nt] = 0.0;
+                    sg[k * nt] = 0.0;
+                } else {
+                    p[k] = 0.0;
+                    sv[k] = 0.0;
+                }
+            }
+            bool go = co.cg_max > 0;
+            if (!go && threadIdx.x == 0 && cx.q == 0) atomicExch(co.fail, 1);
+            while (go) {
+                // p = r + beta p, s = w + beta s, x += alpha p, r -= alpha s
+                // (own points and mirrored halo points; explicit fma in both)
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    double pk, sk;
+                    if constexpr (G) {
+                        pk = fma(beta, pg[k * nt], r[k]);
+                        sk = fma(beta, sg[k * nt], w[k]);
+                        pg[k * nt] = pk;
+                        sg[k * nt] = sk;
+                        if (ok[k]) xb[base + k * nx] = fma(alpha, pk, xb[base + k * nx]);
+                    } else {
+                        pk = fma(beta, p[k], r[k]);
+                        sk = fma(beta, sv[k], w[k]);
+                        p[k] = pk;
+                        sv[k] = sk;
+                        xr[k] = fma(alpha, pk, xr[k]);
+                    }
+                    r[k] = fma(-alpha, sk, r[k]);
+                }
+                sn = fma(beta, sn, wn);
+                ss = fma(beta, ss, ws);
+                rn = fma(-alpha, sn, rn);
+                rs = fma(-alpha, ss, rs);
+                if (mlane) {
+                    const double m = fma(beta, ms[mk], wh);
+                    ms[mk] = m;
+                    mr[mk] = fma(-alpha, m, mr[mk]);
+                }
+                __syncwarp();
+                // w = A r, gamma = (r, r), delta = (w, r): one exchange
+                double g = 0.0, d = 0.0;
+                strip_apply(S, full, r, rn, rs, mrW, mrE, ok, diag, c, w);
+#pragma unroll
+                for (int k = 0; k < E; ++k) {
+                    g = fma(r[k], r[k], g);
+                    d = fma(w[k], r[k], d);
+                }
+                strip_publish<E, G>(S, par, w, g, d);
+                strip_sync<E, G>(S, par, phase, seq);
+                strip_dots<E, G>(S, par, g, d);
+                strip_ns<E, G>(S, par, wn, ws);
+                wh = mlane ? slotv[strip_cslot(S, par, S.wx) + mk] : 0.0;
+                par ^= 1;
+                ++it;
+                if (!more(g)) break;
                 if (it >= co.cg_max) {
                     if (threadIdx.x == 0 && cx.q == 0) atomicExch(co.fail, 1);
                     break;
                 }
-                // x += alpha p, r -= alpha s (own points and mirrored halo points)
-                double g = 0.0;
-#pragma unroll
-                for (int k = 0; k < E; ++k) {
-                    x[k] = fma(alpha, p[k], x[k]);
-                    r[k] = fma(-alpha, sv[k], r[k]);
-                    g = fma(r[k], r[k], g);
-                }
-                rn = fma(-alpha, sn, rn);
-                rs = fma(-alpha, ss, rs);
-                if (mlane) mr[mk] = fma(-alpha, ms[mk], mr[mk]);
-                __syncwarp();
-                // w = A r, delta = (w, r)
-                strip_apply(S, full, r, rn, rs, mrW, mrE, ok, diag, c, w);
-                double d = 0.0;
-#pragma unroll
-                for (int k = 0; k < E; ++k) d = fma(w[k], r[k], d);
-                strip_publish(S, par, w, g, d);
-                strip_sync(S, par, phase);
-                strip_dots(S, par, g, d);
-                double wn, ws;
-                strip_ns(S, par, wn, ws);
-                const double wh = mlane ? slotv[strip_cslot(S, par, S.wx) + mk] : 0.0;
-                par ^= 1;
-                ++it;
-                if (!more(g)) break;
-                const double beta = g * rgamma;
+                beta = g * rgamma;
                 const double den = d - beta * g * ralpha;
                 alpha = g / den;
                 rgamma = 1.0 / g;
                 ralpha = den * rgamma;
-#pragma unroll
-                for (int k = 0; k < E; ++k) {
-                    p[k] = fma(beta, p[k], r[k]);
-                    sv[k] = fma(beta, sv[k], w[k]);
-                }
-                sn = fma(beta, sn, wn);
-                ss = fma(beta, ss, ws);
-                if (mlane) ms[mk] = fma(beta, ms[mk], wh);
-                // (the next mirror read of ms is after this warp's __syncwarp)
             }
         }
         cx.spar = par;
         cx.sph = phase;
+        cx.gseq = seq;
         if (co.iters && threadIdx.x == 0 && cx.q == 0) atomicAdd(co.iters, static_cast<unsigned long long>(it));
+        if constexpr (!G) {
 #pragma unroll
-        for (int k = 0; k < E; ++k)
-            if (ok[k]) xb[base + k * nx] = x[k];
+            for (int k = 0; k < E; ++k)
+                if (ok[k]) xb[base + k * nx] = xr[k];
+        }
     }
     __syncthreads();  // the job code reads xb with its own thread map
+}
+
+// group mode: the sum of one value over the group's CTAs (the sweep tails'
+// C-point squares), through the same exchange as the CG dots
+template <int E>
+__device__ double group_sum1(const CgCoefDev& co, Ctx& cx, double v) {
+    const Strip<E> S = strip_init<E>(co, cx, cx.ex);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int par = cx.spar;
+    if (S.lane == 0) *reinterpret_cast<double2*>(&S.red[(static_cast<size_t>(par) * S.NW + S.warp) * 2]) =
+        make_double2(v, 0.0);
+    glob_sync(S.red, S.NW, S.gred, S.gflag, S.cs, S.q, par, ++cx.gseq);
+    double g0, g1;
+    glob_dots(S.gred, S.cs, par, g0, g1);
+    cx.spar = par ^ 1;
+    return g0;
 }
 
 // ---------------------------------------------------------------------------
@@ -903,8 +1063,10 @@ __device__ __forceinline__ void cg_phi_any(const CgCoefDev& co, Ctx& cx, double*
         GsVec g{xb, xb + m, xb + 2 * m, xb + 3 * m, xb + 4 * m, xb + 5 * m, xb + 6 * m, xb + 7 * m,
                 xb + 8 * m, xb + 9 * m};
         gs_phi(co, cx, g);
+    } else if constexpr (E >= 3000) {
+        cg_phi_strip<E % 1000, true>(co, cx, xb, band, forced);
     } else if constexpr (E >= 1000) {
-        cg_phi_strip<E % 1000>(co, cx, xb, band, forced);
+        cg_phi_strip<E % 1000, false>(co, cx, xb, band, forced);
     } else if constexpr (E > 0) {
         cg_phi_reg<E>(co, cx, xb, band, forced);
     } else {
@@ -914,7 +1076,8 @@ __device__ __forceinline__ void cg_phi_any(const CgCoefDev& co, Ctx& cx, double*
 
 __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned char* smem) {
     cx.cs = co.cs;
-    cx.q = (co.cs > 1) ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+    cx.q = co.glob ? static_cast<int>(blockIdx.x % co.cs)
+                   : (co.cs > 1) ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
     cx.rows = max(0, min(co.R, co.nx - cx.q * co.R));
     cx.own = cx.rows * co.nx;
     cx.t = threadIdx.x;
@@ -941,6 +1104,7 @@ __device__ __forceinline__ void ctx_init(Ctx& cx, const CgCoefDev& co, unsigned 
     cx.par = 0;
     cx.spar = 0;
     cx.sph = 0;
+    cx.gseq = 0;
     // zero p (padding columns and the domain-boundary halo rows stay zero)
     for (size_t i = threadIdx.x; i < psn; i += blockDim.x) cx.ps[i] = 0.0;
     __syncthreads();
@@ -960,7 +1124,7 @@ __device__ __forceinline__ double* r_band(const CgCoefDev& co, const Ctx& cx, in
 }
 
 template <int E>
-__global__ void __launch_bounds__(E >= 2000 ? 256 : E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kernel(const __grid_constant__ CgSweepArgs a) {
+__global__ void __launch_bounds__(E >= 3000 ? 512 : E >= 2000 ? 256 : E > 0 ? 512 : kMaxCgThreads, 1) cg_sweep_kernel(const __grid_constant__ CgSweepArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx cx;
     ctx_init(cx, a.co, smem);
@@ -1025,17 +1189,18 @@ __global__ void __launch_bounds__(E >= 2000 ? 256 : E > 0 ? 512 : kMaxCgThreads,
                     v -= uc[idx];
                     s2[0] = fma(v, v, s2[0]);
                 });
-                cluster_sum<1>(s2, cx);
+                if constexpr (E >= 3000) s2[0] = group_sum1<E % 1000>(a.co, cx, s2[0]);
+                else cluster_sum<1>(s2, cx);
                 if (cx.q == 0 && cx.t == 0) a.sq[(ti - a.sq_base) / a.sq_div] = s2[0];
             }
         }
     }
     // no CTA may leave while a peer can still read its shared memory (DSMEM)
-    if (a.co.cs > 1) cg::this_cluster().sync();
+    if (a.co.cs > 1 && !a.co.glob) cg::this_cluster().sync();
 }
 
 template <int E>
-__global__ void __launch_bounds__(E >= 2000 ? 256 : E > 0 ? 512 : kMaxCgThreads, 1) cg_window_kernel(const __grid_constant__ CgWindowArgs a) {
+__global__ void __launch_bounds__(E >= 3000 ? 512 : E >= 2000 ? 256 : E > 0 ? 512 : kMaxCgThreads, 1) cg_window_kernel(const __grid_constant__ CgWindowArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Ctx cx;
     ctx_init(cx, a.co, smem);
@@ -1076,7 +1241,7 @@ __global__ void __launch_bounds__(E >= 2000 ? 256 : E > 0 ? 512 : kMaxCgThreads,
                 });
             }
         }
-        if (a.co.cs > 1) cg::this_cluster().sync();
+        if (a.co.cs > 1 && !a.co.glob) cg::this_cluster().sync();
         return;
     }
     const bool has_pre = a.pre_e1 >= a.pre_e0;
@@ -1131,7 +1296,7 @@ __global__ void __launch_bounds__(E >= 2000 ? 256 : E > 0 ? 512 : kMaxCgThreads,
             if (s >= e0) emit(s);
         }
     }
-    if (a.co.cs > 1) cg::this_cluster().sync();
+    if (a.co.cs > 1 && !a.co.glob) cg::this_cluster().sync();
 }
 
 struct CgKernels {
@@ -1159,6 +1324,11 @@ CgKernels cg_kernels(int E) {
         case 2008: return cg_k<2008>();
         case 2012: return cg_k<2012>();
         case 2016: return cg_k<2016>();
+        case 3008: return cg_k<3008>();
+        case 3010: return cg_k<3010>();
+        case 3012: return cg_k<3012>();
+        case 3014: return cg_k<3014>();
+        case 3016: return cg_k<3016>();
         default: return cg_k<0>();
     }
 }
@@ -1183,10 +1353,20 @@ int cg_launch(const void* fn, const CgCoefDev& co, int jobs, void** args, cudaSt
     cfg.dynamicSmemBytes = cg_smem_bytes(co);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = co.cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    if (co.glob) {
+        // group mode: every CTA of a group spins on its peers' flags, so the
+        // whole grid must be co-resident (cooperative launch); flags restart
+        // at zero for every launch
+        const cudaError_t e = cudaMemsetAsync(co.gflag, 0, sizeof(unsigned long long) * ncl * co.cs, s);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = co.cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+    }
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return static_cast<int>(cudaLaunchKernelExC(&cfg, fn, args));
@@ -1224,8 +1404,33 @@ static bool strip_geometry(int nx, CgCoefDev& co) {
         co.x_smem = 1;
         co.E = (E >= 8 ? 2000 : 1000) + E;
         co.nt = 32 * WX * WY;
+        co.glob = 0;
         return true;
     }
+    // group mode: one warp-row of WX warps per CTA (E grid rows), cs = G CTAs
+    // of a cooperative grid per system; x, r, w in registers, p and s in
+    // shared memory, exchanges through global memory
+    if (const char* e = std::getenv("ATM_CG_GROUP"))
+        if (std::atoi(e) == 0) return false;
+    int Eg[5] = {14, 12, 16, 10, 8};
+    if (const char* e = std::getenv("ATM_CG_STRIP_E")) Eg[0] = Eg[1] = Eg[2] = Eg[3] = Eg[4] = std::atoi(e);
+    for (int E : Eg) {
+        const int WY = 1;
+        const int R = E * WY;
+        const int G = (nx + R - 1) / R;
+        co.strip = 1;
+        co.glob = 1;
+        co.sWX = WX;
+        co.sWY = WY;
+        co.cs = G;
+        co.R = R;
+        co.x_smem = 1;
+        co.E = 3000 + E;
+        co.nt = 32 * WX * WY;
+        if (cg_smem_bytes(co) <= kCgSmemCap) return true;
+    }
+    co.strip = 0;
+    co.glob = 0;
     return false;
 }
 
@@ -1292,11 +1497,16 @@ bool gs_geometry(int nx, CgCoefDev& co, int cs) {
     return true;
 }
 
+size_t cg_glob_doubles_per_group(const CgCoefDev& co) {
+    return co.glob ? glob_doubles(co.cs, co.sWX * 32) : 0;
+}
+
 size_t cg_smem_bytes(const CgCoefDev& co) {
     if (co.prob == 1) return sizeof(CgShared) + (co.x_smem ? 10 * static_cast<size_t>(co.n) * 8 : 0);
     if (co.strip)
         return sizeof(CgShared) + static_cast<size_t>(co.R) * co.nx * 8 +
-               strip_area_doubles(co.sWX, co.sWY, co.E % 1000, co.cs) * 8;
+               strip_area_doubles(co.sWX, co.sWY, co.E % 1000, co.glob ? 1 : co.cs) * 8 +
+               (co.glob ? 2 * static_cast<size_t>(co.E % 1000) * co.nt * 8 : 0);
     size_t b = sizeof(CgShared) + static_cast<size_t>(co.R + 2) * (co.nx + 2) * 8;
     if (co.x_smem) b += 2 * static_cast<size_t>(co.R) * co.nx * 8;
     return b;
@@ -1315,6 +1525,21 @@ int cg_max_clusters(const CgCoefDev& co) {
     const void* fn = cg_kernels(co.E).sweep;
     cg_prepare(fn);
     cg_prepare(cg_kernels(co.E).window);
+    if (co.glob) {
+        // groups of cs co-resident CTAs (both kernels share the geometry)
+        int per_sm = 0, per_sm_w = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, co.nt, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, cg_kernels(co.E).window, co.nt, smem);
+        const int n = std::max(1, std::min(per_sm, per_sm_w) * sms / co.cs);
+        if (std::getenv("ATM_DEBUG_OCC"))
+            std::fprintf(stderr, "cg groups: G %d nt %d smem %zu per_sm %d/%d -> %d\n", co.cs, co.nt, smem, per_sm,
+                         per_sm_w, n);
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = n;
+        return n;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(co.cs * 148);
     cfg.blockDim = dim3(co.nt);
