@@ -337,6 +337,17 @@ __device__ void cg_phi_reg(const CgCoefDev& co, Ctx& cx, double* xb, int band, b
 // pushes its two partials to every CTA of the cluster; after the barrier each
 // warp sums the cs * NW partials in the same fixed order, so all threads hold
 // bitwise the same alpha and beta (shard-count independent).
+// 1 / a: MUFU.RCP64H seed refined by two Newton steps (full fp64 accuracy
+// to a few ulp; no slow path -- the CG scalars are finite and nonzero)
+__device__ __forceinline__ double rcp_nr(double a) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    double e = fma(-a, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-a, y, 1.0);
+    return fma(y, e, y);
+}
+
 template <int E>
 struct Strip {
     int WX, WY, NW, C, cs, q, nx;
@@ -764,6 +775,9 @@ __device__ void cg_phi_strip(const CgCoefDev& co, Ctx& cx, double* xb, int band,
             }
             bool go = co.cg_max > 0;
             if (!go && threadIdx.x == 0 && cx.q == 0) atomicExch(co.fail, 1);
+#ifdef ATM_CG_PROF
+            long long t_upd = 0, t_pub = 0, t_sync = 0, t_dots = 0, t0 = clock64();
+#endif
             while (go) {
                 // p = r + beta p, s = w + beta s, x += alpha p, r -= alpha s
                 // (own points and mirrored halo points; explicit fma in both)
@@ -798,16 +812,38 @@ __device__ void cg_phi_strip(const CgCoefDev& co, Ctx& cx, double* xb, int band,
                 // w = A r, gamma = (r, r), delta = (w, r): one exchange
                 double g = 0.0, d = 0.0;
                 strip_apply(S, full, r, rn, rs, mrW, mrE, ok, diag, c, w);
+                {
+                    // four interleaved partial sums (short FMA chains), fixed order
+                    double ga[4] = {0.0, 0.0, 0.0, 0.0}, da[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                for (int k = 0; k < E; ++k) {
-                    g = fma(r[k], r[k], g);
-                    d = fma(w[k], r[k], d);
+                    for (int k = 0; k < E; ++k) {
+                        ga[k & 3] = fma(r[k], r[k], ga[k & 3]);
+                        da[k & 3] = fma(w[k], r[k], da[k & 3]);
+                    }
+                    g = (ga[0] + ga[1]) + (ga[2] + ga[3]);
+                    d = (da[0] + da[1]) + (da[2] + da[3]);
                 }
+#ifdef ATM_CG_PROF
+                long long t1 = clock64();
+                t_upd += t1 - t0;
+#endif
                 strip_publish<E, G>(S, par, w, g, d);
+#ifdef ATM_CG_PROF
+                long long t2 = clock64();
+                t_pub += t2 - t1;
+#endif
                 strip_sync<E, G>(S, par, phase, seq);
+#ifdef ATM_CG_PROF
+                long long t3 = clock64();
+                t_sync += t3 - t2;
+#endif
                 strip_dots<E, G>(S, par, g, d);
                 strip_ns<E, G>(S, par, wn, ws);
                 wh = mlane ? slotv[strip_cslot(S, par, S.wx) + mk] : 0.0;
+#ifdef ATM_CG_PROF
+                t0 = clock64();
+                t_dots += t0 - t3;
+#endif
                 par ^= 1;
                 ++it;
                 if (!more(g)) break;
@@ -817,10 +853,19 @@ __device__ void cg_phi_strip(const CgCoefDev& co, Ctx& cx, double* xb, int band,
                 }
                 beta = g * rgamma;
                 const double den = d - beta * g * ralpha;
-                alpha = g / den;
-                rgamma = 1.0 / g;
+                // alpha = g / den through a refined reciprocal (two Newton
+                // steps from the hardware seed: a few ulp, identical in every
+                // thread of the group) instead of the IEEE division sequence
+                const double rden = rcp_nr(den);
+                alpha = g * rden;
+                rgamma = rcp_nr(g);
                 ralpha = den * rgamma;
             }
+#ifdef ATM_CG_PROF
+            if ((threadIdx.x == 0 || threadIdx.x == 200) && blockIdx.x < 2 && it > 0)
+                printf("cgprof blk %d thr %d it %d upd %lld pub %lld sync %lld dots %lld (cycles/it)\n", blockIdx.x,
+                       threadIdx.x, it, t_upd / it, t_pub / it, t_sync / it, t_dots / it);
+#endif
         }
         cx.spar = par;
         cx.sph = phase;
