@@ -1,4 +1,6 @@
 #!/bin/bash
+# NOTE: compute-sanitizer is closed on this pool (runs under it left GPUs
+# needing a reset); kept for boxes where it is allowed.
 # compute-sanitizer memcheck / racecheck / synccheck over tools/sanitize_cases.py
 # (one process per case and tool, each bounded), logs to gpurun_out/sanitize/
 mkdir -p gpurun_out/sanitize
