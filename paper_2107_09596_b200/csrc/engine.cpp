@@ -52,7 +52,10 @@ CUtensorMap make_row_map(double* ptr, int rows, int pitch) {
     std::memset(&m, 0, sizeof(m));
     const cuuint64_t dims[2] = {16, static_cast<cuuint64_t>(rows) * (pitch / 16)};
     const cuuint64_t strides[1] = {128};
-    const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(pitch / 16)};
+    // a box holds at most 256 rows of the view: longer point rows (pitch a
+    // multiple of 256) are moved as two half-row boxes (tma_load_row)
+    const int R = pitch / 16;
+    const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(R <= 256 ? R : R / 2)};
     const cuuint32_t es[2] = {1, 1};
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, ptr, dims, strides, box,
                                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -280,7 +283,9 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
             n_ = p.n;
             if (n_ < 1) config_error("heat1d: need at least one spatial unknown");
             if (!(p.x1 > p.x0)) config_error("heat1d: x1 must exceed x0");
-            if (n_ > 4096) config_error("heat1d: n > 4096 exceeds the single-CTA row kernel");
+            // one CTA holds one state vector; the FAS window kernel stages five
+            // rows in shared memory (5 x 42 KB at n = 5376 of the 227 KB)
+            if (n_ > 5376) config_error("heat1d: n > 5376 exceeds the single-CTA row kernels (five staged rows per CTA)");
             heat_ = true;
             folded_ = p.folded != 0;
             break;
@@ -366,6 +371,11 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     // L = 32 row kernels (pitch > 2048): a thread's chunk must not straddle
     // the row end, so rows are whole 32-element chunks
     if (heat_ && !ac_ && pitch_ > 2048) pitch_ = ((n_ + 31) / 32) * 32;
+    // 4096 < n <= 5376: a point row is loaded / stored as two TMA boxes of
+    // half a row each (a box holds at most 256 rows of the [.., 16] view, and
+    // a 128B-swizzled box must start 1024-byte aligned), so the row is padded
+    // to a multiple of 256 (padding stays 0)
+    if (heat_ && !ac_ && pitch_ > 4096) pitch_ = ((n_ + 255) / 256) * 256;
     // host copies of caller-owned inputs
     ic_.assign(n_, 0.0);
     if (heat_ && !ac_) {

@@ -313,10 +313,33 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double r_in, double shift
     return H;
 }
 
+// one point row into shared memory: R = pitch / 16 rows of the tensor map's
+// [rows][16] view -- one box, or past 256 rows (the TMA box limit) two
+// half-row boxes; pitch is then a multiple of 256, so the second half lands
+// 1024-byte aligned and the 128-byte swizzle is that of one box
+__device__ __forceinline__ void tma_load_row(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                             int R) {
+    if (R <= 256) {
+        tma_load_2d(dst, map, c0, c1, bar);
+    } else {  // two half-row boxes (pitch a multiple of 256: 1024-byte aligned halves)
+        tma_load_2d(dst, map, c0, c1, bar);
+        tma_load_2d(static_cast<char*>(dst) + (R / 2) * 128, map, c0, c1 + R / 2, bar);
+    }
+}
+
+// the matching whole-row store (bulk-group completion: one commit covers all boxes)
+__device__ __forceinline__ void tma_store_row(const CUtensorMap* map, int c0, int c1, const void* src, int R) {
+    tma_store_2d(map, c0, c1, src);
+    if (R > 256) tma_store_2d(map, c0, c1 + R / 2, static_cast<const char*>(src) + (R / 2) * 128);
+}
+
 // --------------------------------------------------------------------------
 // device: per-thread state, shared tables and the tridiagonal solve
 
-template <int L>
+// NW: warps per CTA of the instantiation (the cross-warp carry tree)
+__host__ __device__ constexpr int warps_for(int L) { return L >= 32 ? 4 : (L == 16 ? 8 : 16); }
+
+template <int L, int NW = warps_for(L)>
 struct Lane {
     int t, lane, warp, nw, s;
     int q7, qx, qx1, ch0;  // swizzled row-staging geometry (L = 32: two 128-B rows)
@@ -329,8 +352,8 @@ struct Lane {
     double cbwr;         // cyclic: right correction vector's p_b coefficient
 };
 
-template <int L>
-__device__ __forceinline__ void lane_init(Lane<L>& ln, const HeatCoefDev& co) {
+template <int L, int NW>
+__device__ __forceinline__ void lane_init(Lane<L, NW>& ln, const HeatCoefDev& co) {
     ln.t = threadIdx.x;
     ln.lane = ln.t & 31;
     ln.warp = ln.t >> 5;
@@ -400,8 +423,8 @@ __device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev
 // n = k L - 1) is a select with no branch; otherwise a fall-through switch:
 // one jump and L - pad0 moves for that thread instead of L predicated
 // selects in its whole warp.
-template <int L>
-__device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L>& ln) {
+template <int L, int NW>
+__device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L, NW>& ln) {
     x[L - 1] = ln.pad_last ? 0.0 : x[L - 1];
     if (ln.pad0 < L - 1) {
         switch (ln.pad0) {
@@ -446,10 +469,9 @@ __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L>& ln) 
 // the periodic matrix with corner entries a (Allen-Cahn linear part).
 // warps per CTA of the instantiation for chunk length L (a power of two):
 // L = 32 -> 128 threads, L = 16 -> 256, L <= 8 -> 512
-__host__ __device__ constexpr int warps_for(int L) { return L >= 32 ? 4 : (L == 16 ? 8 : 16); }
 
-template <int L, bool CYC = false>
-__device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
+template <int L, bool CYC = false, int NW = warps_for(L)>
+__device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L, NW>& ln,
                                           const Tabs& tb, Slots& sl) {
     // 1. forward local  y_i = beta x_i + gamma y_{i-1}
     double y = 0.0;
@@ -522,7 +544,7 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     double cC, cD, cD0 = 0.0;
     double p0 = 0.0, pN = 0.0;
     {
-        const int v = ln.lane & (warps_for(L) - 1);
+        const int v = ln.lane & (NW - 1);
         const double tf = sl.tf[par][v], ta = sl.ta[par][v];
         const int row = ln.warp * kMaxWarps + v;
         cC = tb.wf[row] * tf;
@@ -533,18 +555,18 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
             pN = fma(tb.xw[2 * kMaxWarps + v], tf, tb.xw[3 * kMaxWarps + v] * ta);
         }
 #pragma unroll
-        for (int off = warps_for(L) / 2; off >= 1; off >>= 1) {
+        for (int off = NW / 2; off >= 1; off >>= 1) {
             cC += __shfl_xor_sync(0xffffffffu, cC, off);
             cD += __shfl_xor_sync(0xffffffffu, cD, off);
         }
         if (far) {
 #pragma unroll
-            for (int off = warps_for(L) / 2; off >= 1; off >>= 1)
+            for (int off = NW / 2; off >= 1; off >>= 1)
                 cD0 += __shfl_xor_sync(0xffffffffu, cD0, off);
         }
         if (CYC && ln.corr) {
 #pragma unroll
-            for (int off = warps_for(L) / 2; off >= 1; off >>= 1) {
+            for (int off = NW / 2; off >= 1; off >>= 1) {
                 p0 += __shfl_xor_sync(0xffffffffu, p0, off);
                 pN += __shfl_xor_sync(0xffffffffu, pN, off);
             }
@@ -583,8 +605,8 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
 
 // Phi_index on this level: S sub-steps, forcing added before each solve
 // when `forced` (heat1d.cpp:66-83).
-template <int L>
-__device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
+template <int L, int NW>
+__device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, Lane<L, NW>& ln,
                                     const Tabs& tb, Slots& sl, int index, int forced) {
     for (int s = 0; s < co.substeps; ++s) {
         if (forced) {
@@ -606,10 +628,10 @@ __device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, Lane<
 // rho <= max(s, 3 dt umax^2 - s) / (1 - dt + s), iterated to rho^K <= eta.
 // Chunk ends travel through smem (one barrier per residual); the residual
 // norm and max u^2 ride on a second barrier.
-template <int L>
+template <int L, int NW>
 __device__ __forceinline__ void ac_residual(const double (&u)[L], const double (&up)[L],
                                             double (&F)[L], const HeatCoefDev& co,
-                                            const Lane<L>& ln, double* ends, double& sq,
+                                            const Lane<L, NW>& ln, double* ends, double& sq,
                                             double& u2) {
     const int nt = blockDim.x;
     ends[ln.t] = u[0];
@@ -634,8 +656,8 @@ __device__ __forceinline__ void ac_residual(const double (&u)[L], const double (
     }
 }
 
-template <int L>
-__device__ __forceinline__ void ac_reduce(double sq, double u2, const Lane<L>& ln, Slots& sl,
+template <int L, int NW>
+__device__ __forceinline__ void ac_reduce(double sq, double u2, const Lane<L, NW>& ln, Slots& sl,
                                           int par, double& res, double& umax2) {
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
@@ -656,8 +678,8 @@ __device__ __forceinline__ void ac_reduce(double sq, double u2, const Lane<L>& l
     res = sqrt(res);
 }
 
-template <int L>
-__device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, Lane<L>& ln,
+template <int L, int NW>
+__device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, Lane<L, NW>& ln,
                                        const Tabs& tb, Slots& sl, double* ends) {
     int rpar = 0;
     for (int s = 0; s < co.substeps; ++s) {
@@ -704,8 +726,8 @@ __device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, La
 }
 
 // problem dispatch: P = 0 heat (forcing optional), P = 1 Allen-Cahn
-template <int P, int L>
-__device__ __forceinline__ void phi_p(double (&x)[L], const HeatCoefDev& co, Lane<L>& ln,
+template <int P, int L, int NW>
+__device__ __forceinline__ void phi_p(double (&x)[L], const HeatCoefDev& co, Lane<L, NW>& ln,
                                       const Tabs& tb, Slots& sl, double* ends, int index,
                                       int forced) {
     if constexpr (P == 1) ac_phi<L>(x, co, ln, tb, sl, ends);
@@ -718,8 +740,8 @@ __device__ __forceinline__ void phi_p(double (&x)[L], const HeatCoefDev& co, Lan
 // position c ^ (q & 7).
 
 // byte offset of element pair c (elements 2c, 2c+1) of this thread's chunk
-template <int L>
-__device__ __forceinline__ int pair_off(const Lane<L>& ln, int c) {
+template <int L, int NW>
+__device__ __forceinline__ int pair_off(const Lane<L, NW>& ln, int c) {
     if constexpr (L == 32) {
         const int half = c >> 3, cc = c & 7;
         return ln.q7 + (half << 7) + ((cc ^ (half ? ln.qx1 : ln.qx)) << 4);
@@ -728,8 +750,8 @@ __device__ __forceinline__ int pair_off(const Lane<L>& ln, int c) {
     }
 }
 
-template <int L>
-__device__ __forceinline__ void row_load(const char* buf, double (&x)[L], const Lane<L>& ln) {
+template <int L, int NW>
+__device__ __forceinline__ void row_load(const char* buf, double (&x)[L], const Lane<L, NW>& ln) {
     if (ln.inside) {
 #pragma unroll
         for (int c = 0; c < L / 2; ++c) {
@@ -743,8 +765,8 @@ __device__ __forceinline__ void row_load(const char* buf, double (&x)[L], const 
     }
 }
 
-template <int L>
-__device__ __forceinline__ void row_store(char* buf, const double (&x)[L], const Lane<L>& ln) {
+template <int L, int NW>
+__device__ __forceinline__ void row_store(char* buf, const double (&x)[L], const Lane<L, NW>& ln) {
     if (ln.inside) {
 #pragma unroll
         for (int c = 0; c < L / 2; ++c)
@@ -753,8 +775,8 @@ __device__ __forceinline__ void row_store(char* buf, const double (&x)[L], const
 }
 
 // x = x + row, or x = x - row
-template <int L>
-__device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], const Lane<L>& ln,
+template <int L, int NW>
+__device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], const Lane<L, NW>& ln,
                                         bool sub) {
     if (ln.inside) {
 #pragma unroll
@@ -773,8 +795,8 @@ __device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], const L
 
 // fixed-order CTA reduction of sum x_e^2 (thread order, then warp xor tree,
 // then warps in order): depends only on the CTA shape
-template <int L>
-__device__ __forceinline__ double cta_sum_squares(const double (&x)[L], const Lane<L>& ln,
+template <int L, int NW>
+__device__ __forceinline__ double cta_sum_squares(const double (&x)[L], const Lane<L, NW>& ln,
                                                   Slots& sl) {
     double s = 0.0;
 #pragma unroll
@@ -833,7 +855,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
     const int R = pitch >> 4;
 
-    Lane<L> ln;
+    Lane<L, NTMAX / 32> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
     tabs_init(tb, sl, a.co);
@@ -882,7 +904,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         } else {
             __syncthreads();
             if (t == 0) {
-                tma_store_2d(map, 0, row * R, o);
+                tma_store_row(map, 0, row * R, o, R);
                 bulk_commit();
             }
         }
@@ -930,7 +952,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (!seed_ready) {
             if (t == 0) {
                 mbar_expect_tx(barS, bytes);
-                tma_load_2d(bufS, &tm_u, 0, ((cpu ? J : start) - ub) * R, barS);
+                tma_load_row(bufS, &tm_u, 0, ((cpu ? J : start) - ub) * R, barS, R);
             }
             mbar_wait(barS, phS);
             phS ^= 1;
@@ -941,7 +963,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         seed_ready = false;
         if (tail_i >= 0 && t == 0) {
             mbar_expect_tx(barS, bytes);
-            tma_load_2d(bufS, &tm_u, 0, ((cpu ? J + 1 : tail_i) - ub) * R, barS);
+            tma_load_row(bufS, &tm_u, 0, ((cpu ? J + 1 : tail_i) - ub) * R, barS, R);
         }
 
         // ---- chain steps u_i = Phi_i(u_{i-1}) (+ g_i)
@@ -960,7 +982,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         } else for (int i = start + 1; i <= end; ++i) {
             if (a.add_g && t == 0) {
                 mbar_expect_tx(barA, bytes);
-                tma_load_2d(bufA, &tm_g, 0, (i - a.g_base) * R, barA);
+                tma_load_row(bufA, &tm_g, 0, (i - a.g_base) * R, barA, R);
             }
             release_staging();
             phi_p<P, L>(x, a.co, ln, tb, sl, ends, i, a.forced);
@@ -982,7 +1004,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (tail_i >= 0) {
             if (a.add_g && t == 0) {
                 mbar_expect_tx(barA, bytes);
-                tma_load_2d(bufA, &tm_g, 0, (tail_i - a.g_base) * R, barA);
+                tma_load_row(bufA, &tm_g, 0, (tail_i - a.g_base) * R, barA, R);
             }
             release_staging();
             if (plain) tri_solve<L>(x, a.co, ln, tb, sl);
@@ -1046,7 +1068,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
     const int R = pitch >> 4;
 
-    Lane<L> ln;
+    Lane<L, NTMAX / 32> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
     tabs_init(tb, sl, a.co);
@@ -1084,7 +1106,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (iq >= Nj) return;
         uint64_t* bar = buf ? barA1 : barA0;
         mbar_expect_tx(bar, bytes);
-        tma_load_2d(buf ? bufA1 : bufA0, &tm_r, 0, (is_ - a.x1_base) * R, bar);
+        tma_load_row(buf ? bufA1 : bufA0, &tm_r, 0, (is_ - a.x1_base) * R, bar, R);
         if (++is_ > ie1) {
             iq += G;
             if (iq < Nj) {
@@ -1126,8 +1148,8 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             bulk_wait_read<0>();  // S free again
             for (int b = 0; b < (NS == 1 ? 1 : NS - 1) && f0 + b <= e1; ++b) {
                 mbar_expect_tx(barS + b, bytes);
-                tma_load_2d(bufS + b * rb, &tm_fine, 0, ((f0 + b) * a.out_stride - a.out_base) * R,
-                            barS + b);
+                tma_load_row(bufS + b * rb, &tm_fine, 0, ((f0 + b) * a.out_stride - a.out_base) * R,
+                            barS + b, R);
             }
         }
         for (int s = lo; s <= e1; ++s) {
@@ -1150,14 +1172,14 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 fence_proxy_async();
                 __syncthreads();
                 if (t == 0) {
-                    tma_store_2d(&tm_fine, 0, (s * a.out_stride - a.out_base) * R, bs);
+                    tma_store_row(&tm_fine, 0, (s * a.out_stride - a.out_base) * R, bs, R);
                     bulk_commit();
                     if (NS == 1) {
                         if (s + 1 <= e1) {
                             bulk_wait_read<0>();
                             mbar_expect_tx(barS, bytes);
-                            tma_load_2d(bufS, &tm_fine, 0, ((s + 1) * a.out_stride - a.out_base) * R,
-                                        barS);
+                            tma_load_row(bufS, &tm_fine, 0, ((s + 1) * a.out_stride - a.out_base) * R,
+                                        barS, R);
                         }
                     } else if (s + NS - 1 <= e1) {
                         // row s + NS - 1 goes to the buffer of emit s - 1 (for
@@ -1166,8 +1188,8 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                         const int nb = (s - f0 + NS - 1) % NS;
                         bulk_wait_read<1>();
                         mbar_expect_tx(barS + nb, bytes);
-                        tma_load_2d(bufS + nb * rb, &tm_fine, 0,
-                                    ((s + NS - 1) * a.out_stride - a.out_base) * R, barS + nb);
+                        tma_load_row(bufS + nb * rb, &tm_fine, 0,
+                                    ((s + NS - 1) * a.out_stride - a.out_base) * R, barS + nb, R);
                     }
                 }
             }
@@ -1207,7 +1229,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
     const int R = pitch >> 4;
 
-    Lane<L> ln;
+    Lane<L, NTMAX / 32> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
     tabs_init(tb, sl, a.co);
@@ -1233,7 +1255,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         fence_proxy_async();
         __syncthreads();
         if (t == 0) {
-            tma_store_2d(&tm_out, 0, (row - a.out_base) * R, o);
+            tma_store_row(&tm_out, 0, (row - a.out_base) * R, o, R);
             bulk_commit();
         }
         ob ^= 1;
@@ -1247,10 +1269,10 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             const uint32_t extra = (a.kind == WK_FAS_RHS) ? 2 * bytes : 0u;
             if (t == 0 && nb + extra) {
                 mbar_expect_tx(barA, nb + extra);
-                if (!a.seed_zero) tma_load_2d(bufA1, &tm_x1, 0, (src - a.x1_base) * R, barA);
+                if (!a.seed_zero) tma_load_row(bufA1, &tm_x1, 0, (src - a.x1_base) * R, barA, R);
                 if (a.kind == WK_FAS_RHS) {
-                    tma_load_2d(bufA2, &tm_x2, 0, (p - a.x2_base) * R, barA);
-                    tma_load_2d(bufA3, &tm_x3, 0, (p - a.x3_base) * R, barA);
+                    tma_load_row(bufA2, &tm_x2, 0, (p - a.x2_base) * R, barA, R);
+                    tma_load_row(bufA3, &tm_x3, 0, (p - a.x3_base) * R, barA, R);
                 }
             }
             if (nb + extra) {
@@ -1293,8 +1315,8 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         const bool fas = (a.kind == WK_FAS);
         if (t == 0) {
             mbar_expect_tx(barA, fas ? 2 * bytes : bytes);
-            tma_load_2d(bufA1, &tm_x1, 0, (lo - a.x1_base) * R, barA);
-            if (fas) tma_load_2d(bufA2, &tm_x2, 0, (lo - a.x2_base) * R, barA);
+            tma_load_row(bufA1, &tm_x1, 0, (lo - a.x1_base) * R, barA, R);
+            if (fas) tma_load_row(bufA2, &tm_x2, 0, (lo - a.x2_base) * R, barA, R);
         }
         mbar_wait(barA, phA);
         phA ^= 1;
@@ -1310,9 +1332,9 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         for (int s = lo + 1; s <= e1; ++s) {
             if (t == 0 && fas) {
                 mbar_expect_tx(barA, 3 * bytes);
-                tma_load_2d(bufA1, &tm_x1, 0, (s - a.x1_base) * R, barA);
-                tma_load_2d(bufA2, &tm_x2, 0, (s - a.x2_base) * R, barA);
-                tma_load_2d(bufA3, &tm_x3, 0, (s - a.x3_base) * R, barA);
+                tma_load_row(bufA1, &tm_x1, 0, (s - a.x1_base) * R, barA, R);
+                tma_load_row(bufA2, &tm_x2, 0, (s - a.x2_base) * R, barA, R);
+                tma_load_row(bufA3, &tm_x3, 0, (s - a.x3_base) * R, barA, R);
             }
             if (t == 0) bulk_wait_read<1>();
             phi_p<P, L>(x, a.co, ln, tb, sl, ends, s, a.forced);
@@ -1375,12 +1397,14 @@ KernelPtrs select(const HeatCoefDev& co) {
     if (co.prob == 1)
         return {reinterpret_cast<const void*>(heat_sweep_kernel<8, 512, 1, 1>), nullptr,
                 reinterpret_cast<const void*>(heat_window_kernel<8, 512, 1, 1>)};
+    // 4096 < n <= 5376: L = 32 with 256 threads (sweeps), L = 16 with up to
+    // 512 (the coarsest level's windows)
     switch (co.L) {
         case 2: return kptrs<2, 512, 1>();
         case 4: return kptrs<4, 512, 1>();
         case 8: return kptrs<8, 512, 1>();
-        case 32: return kptrs<32, 128, 3>();
-        default: return kptrs<16, 256, 2>();
+        case 32: return co.nt > 128 ? kptrs<32, 256, 1>() : kptrs<32, 128, 3>();
+        default: return co.nt > 256 ? kptrs<16, 512, 1>() : kptrs<16, 256, 2>();
     }
 }
 

@@ -9,7 +9,7 @@ import paper_2107_09596_b200 as T  # noqa: E402
 
 n, npts, K = 4095, 2 ** 18 + 1, 10
 app = T.Heat1D(n, manufactured_forcing=False, initial_condition=T.random_state(7, n))
-hier = T.build_hierarchy(T.TimeGrid.make(0.0, 16.0, npts), [16], 8)
+hier = T.build_hierarchy(T.TimeGrid.make(0.0, float(os.environ.get("AB_TF", "1.0")), npts), [16], 8)
 cfg = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=1e-300, max_iters=100,
                      initial_guess=T.InitialGuess.Random, seed=20)
 drv = T.CycleDriver(app, hier, cfg)
