@@ -4,12 +4,13 @@ compiled reference's own cycle driver (tests/golden/make_fullsize.py:
 tempo_ref run_parallel with the restated Phi as its Application): 2D heat
 127^2, N_t = 4096, two-level m = 16, k = 4 (CG Phi); Allen-Cahn n = 4096,
 N_t = 16384 over [0, 8], three-level m = (8, 8), k = 4 (Newton Phi, FAS
-V-cycle); 2D heat 511^2, dt = 4/65536, N_t = 1024, four-level FAS m = (8, 8,
+V-cycle); 2D heat 511^2, dt = 4/65536, N_t = 2048, four-level FAS m = (8, 8,
 8), k = 2.  All to tol 1e-10 from the seeded random guess.  The bar (BASELINE north star): the
 same iteration count, and the final state within 1e-10 relative l2 -- here on
 every SAMPLE-th level-0 row the fixture keeps, plus the full state's 2-norm.
 The residual histories agree to 1e-8 relative (their tails sit near the
-rounding floor of the stopping norm)."""
+rounding floor of the stopping norm; for the CG Phi of configs 2 and 4 near
+its truncation floor, so they are compared absolutely below tol / 4)."""
 from __future__ import annotations
 
 import json
@@ -83,7 +84,13 @@ def test_full_size_config_matches_oracle(tag):
     assert res.report.iterations == meta["iterations"], (res.report.iterations, meta["iterations"])
     hist = np.array(res.report.residual_norms)
     ref = np.array(meta["history"])
-    assert np.all(np.abs(hist - ref) <= 1e-8 * np.abs(ref) + 1e-13), np.max(np.abs(hist - ref) / ref)
+    # 2D heat: each Phi is a CG solve to rtol 1e-12, and the device's
+    # Chronopoulos-Gear CG stops at a different iterate than the reference's
+    # CG near that threshold; the norms then differ by that truncation
+    # (observed <= 2e-11 at the 1e-10 tail), so below a quarter of the
+    # stopping tolerance they are compared absolutely
+    floor = 0.25 * meta["tol"] if meta["config"] in (2, 4) else 1e-13
+    assert np.all(np.abs(hist - ref) <= 1e-8 * np.abs(ref) + floor), np.max(np.abs(hist - ref) / ref)
     got = res.state[::meta["sample_every"], ::meta.get("dof_stride", 1)]
     assert got.shape == rows.shape
     assert rel_l2(got, rows) <= 1e-10, rel_l2(got, rows)
