@@ -42,9 +42,12 @@ def _pair(nx, n_points, tf, ms, k, mode="two-level", folded=False, source=True, 
     return app, hier, cfg, orc
 
 
-# nx = 1, 7, 63: one CTA; 127: cluster of 2 with x, r on chip; 200: cluster
-# of 2 with x, r in global scratch; 511: cluster of 11 (config 4's grid)
-@pytest.mark.parametrize("nx", [1, 7, 63, 127, 200, 511])
+# strip CG (heat2d_cg.cu): nx = 1, 7, 31, 63 one CTA; 127 a 4-CTA cluster
+# (config 2's grid); 200, 255 clusters of 13 and 16 CTAs; 300 and 511 group
+# mode (cooperative groups of 22 and 37 CTAs exchanging through global
+# memory; 511 is config 4's grid); 600 the round-1 cluster CG with x, r in
+# global scratch (grids past 16 warps per row)
+@pytest.mark.parametrize("nx", [1, 7, 31, 63, 127, 200, 255, 300, 511, 600])
 def test_heat2d_phi_matches_oracle(nx):
     app, hier, cfg, orc = _pair(nx, 65, 1.0, [16], 4, substeps=2)
     drv = T.CycleDriver(app, hier, cfg)
@@ -89,7 +92,7 @@ def test_heat2d_config2_shape_two_level():
 
 
 def test_heat2d_config2_grid_short_horizon():
-    # config 2's grid (nx = 127, cluster of 2) over N_t = 64
+    # config 2's grid (nx = 127, 4-CTA strip cluster) over N_t = 64
     app, hier, cfg, orc = _pair(127, 65, 1.0 / 64, [16], 4, tol=1e-10)
     res = T.solve(app, hier, cfg)
     ref = orc.drive()
@@ -125,9 +128,9 @@ def test_heat2d_cg_cap_raises():
 
 
 def test_heat2d_config4_grid_cluster11_cycles():
-    # config 4's grid (nx = 511: an 11-CTA cluster with x, r in global
-    # scratch): two cycles incl. the fused C-point norm (cluster-summed
-    # squares) against the oracle's cycles and full residual norm
+    # config 4's grid (nx = 511: group mode, 37 CTAs per system): two cycles
+    # incl. the fused C-point norm (group-summed squares) against the
+    # oracle's cycles and full residual norm
     app, hier, cfg, orc = _pair(511, 9, 0.01, [4], 2, source=False, ic="fourier", max_iters=2)
     drv = T.CycleDriver(app, hier, cfg)
     drv.setup()
