@@ -162,3 +162,21 @@ def test_heat2d_inner_iteration_counter():
     h.setup()
     h.iterate(1)
     assert h.inner_iterations() == 0
+
+
+@pytest.mark.parametrize("nx,npts", [(127, 65), (300, 17)])
+def test_strip_cg_solves_are_bitwise_repeatable_and_shard_independent(nx, npts):
+    # the strip CG exchanges through DSMEM st.async + mbarriers (127: 4-CTA
+    # clusters) or global memory + a release/acquire counter (300: group
+    # mode); compute-sanitizer is unavailable on this pool, so races would
+    # show here as run-to-run or shard-count differences (the dot products
+    # are summed in one fixed order, so every run must be bitwise identical)
+    app, hier, cfg, orc = _pair(nx, npts, 1.0 / 64, [4], 2, tol=1e-10, max_iters=6)
+    runs = [T.solve(app, hier, cfg) for _ in range(2)] + [T.run_parallel(app, hier, cfg, 3)]
+    for r in runs[1:]:
+        assert r.report.iterations == runs[0].report.iterations
+        assert np.array_equal(np.array(r.report.residual_norms), np.array(runs[0].report.residual_norms))
+        assert np.array_equal(r.state, runs[0].state)
+    ref = orc.drive()
+    assert runs[0].report.iterations == ref["iterations"]
+    assert rel_l2(runs[0].state, orc.array(0)) <= 1e-10
