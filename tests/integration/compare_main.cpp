@@ -134,6 +134,33 @@ void compare(const std::string& name) {
             num += d * d;
             den += ur[i][q] * ur[i][q];
         }
+    // the coarse levels' working arrays, where the device holds them
+    // (nonzero): relative l2 against the reference's
+    std::string coarse;
+    for (int l = 0; l < c.hier.n_levels(); ++l) {
+        const LevelState& lr = ref.state.level(l);
+        const LevelState& lg = gpu.state.level(l);
+        const std::vector<StateVector>* rs[4] = {&lr.u, &lr.g, &lr.v, &lr.r};
+        const std::vector<StateVector>* gs[4] = {&lg.u, &lg.g, &lg.v, &lg.r};
+        const char* nm[4] = {"u", "g", "v", "r"};
+        for (int w = 0; w < 4; ++w) {
+            if (rs[w]->size() != gs[w]->size() || (l == 0 && w == 0)) continue;
+            double dn = 0.0, rn = 0.0, gn = 0.0;
+            for (size_t i = 0; i < rs[w]->size(); ++i)
+                for (size_t q = 0; q < (*rs[w])[i].size() && q < (*gs[w])[i].size(); ++q) {
+                    const double a = (*rs[w])[i][q], b = (*gs[w])[i][q];
+                    dn += (a - b) * (a - b);
+                    rn += a * a;
+                    gn += b * b;
+                }
+            if (gn == 0.0) continue;  // not held by the device
+            char buf[96];
+            std::snprintf(buf, sizeof(buf), "%s\"%s%d\": %.3e", coarse.empty() ? "" : ", ", nm[w], l,
+                          rn > 0 ? std::sqrt(dn / rn) : std::sqrt(dn));
+            coarse += buf;
+        }
+    }
+    std::printf("{\"coarse_rel_l2\": {%s}}\n", coarse.c_str());
     std::printf("{\"case\": \"%s\", \"workers\": %d, \"ref_iterations\": %d, \"b200_iterations\": %d, "
                 "\"ref_converged\": %s, \"b200_converged\": %s, \"history_max_rel\": %.3e, "
                 "\"state_rel_l2\": %.3e, \"same_shape\": %s, \"b200_timings\": %zu, "

@@ -102,20 +102,33 @@ SolveResult run(const Heat1DB200& app, const Hierarchy& hier, const SolverConfig
     if (trace)
         for (int it = 0; it < rep.iterations; ++it) trace(it + 1, 0, "cycle", secs[static_cast<size_t>(it)]);
 
-    // SpaceTimeState (space_time.hpp:20-32): level-0 u read back
-    const int n = p.n, np = g.n_points;
-    std::vector<double> u(static_cast<size_t>(np) * n);
-    if (atm_status e = atm_get_level(ctx, 0, 0, 0, np, u.data())) {
-        const std::string msg = atm_last_error(ctx);
-        atm_destroy(ctx);
-        raise(e, msg);
-    }
+    // SpaceTimeState (space_time.hpp:20-32), shaped as CycleDriver::setup
+    // sizes it (solver.cpp:84-96): u and g on every level, v and r on the
+    // coarse levels.  Level-0 u is the solution; the other arrays are the
+    // solver's working state, read back where the device holds them (the
+    // linear two-level cycle keeps no coarse u, for instance) and zero
+    // otherwise.
+    const int n = p.n;
     out.state.levels.resize(static_cast<size_t>(hier.n_levels()));
-    auto& u0 = out.state.level(0).u;
-    u0.reserve(static_cast<size_t>(np));
-    for (int i = 0; i < np; ++i)
-        u0.emplace_back(std::vector<double>(u.begin() + static_cast<long>(i) * n,
-                                            u.begin() + static_cast<long>(i + 1) * n));
+    for (int l = 0; l < hier.n_levels(); ++l) {
+        const int npl = hier.level(l).n_points;
+        LevelState& ls = out.state.level(l);
+        std::vector<StateVector>* arrs[4] = {&ls.u, &ls.g, &ls.v, &ls.r};  // atm_get_level's `which`
+        for (int which = 0; which < 4; ++which) {
+            if (which >= 2 && l == 0) continue;
+            std::vector<double> buf(static_cast<size_t>(npl) * n, 0.0);
+            if (atm_status e = atm_get_level(ctx, l, which, 0, npl, buf.data())) {
+                const std::string msg = atm_last_error(ctx);
+                atm_destroy(ctx);
+                raise(e, msg);
+            }
+            auto& dst = *arrs[which];
+            dst.reserve(static_cast<size_t>(npl));
+            for (int i = 0; i < npl; ++i)
+                dst.emplace_back(std::vector<double>(buf.begin() + static_cast<long>(i) * n,
+                                                     buf.begin() + static_cast<long>(i + 1) * n));
+        }
+    }
     atm_destroy(ctx);
     return out;
 }
