@@ -218,7 +218,7 @@ def test_direct_window_schedule_delivers_the_two_round_set(n_points, m, k, worke
 
 
 def test_fullsize_fixtures_are_consistent():
-    """tests/golden/fullsize_*.json (oracle runs at BASELINE sizes): histories,
+    """tests/golden/fullsize_*.json (reference runs at BASELINE sizes): histories,
     iteration counts, failure cycles and sampled-row shapes agree."""
     import glob
     import json
@@ -236,5 +236,6 @@ def test_fullsize_fixtures_are_consistent():
         assert meta["converged"] and meta["iterations"] == len(hist)
         assert hist[-1] <= meta["tol"] < min(hist[:-1])
         rows = np.load(p[:-5] + "_rows.npy")
-        npts, n = {2: (4097, 127 * 127), 3: (16385, 4096)}[meta["config"]]
-        assert rows.shape == (len(range(0, npts, meta["sample_every"])), n)
+        npts, n = {2: (4097, 127 * 127), 3: (16385, 4096), 4: (meta.get("n_points"), 511 * 511)}[meta["config"]]
+        ds = meta.get("dof_stride", 1)
+        assert rows.shape == (len(range(0, npts, meta["sample_every"])), len(range(0, n, ds)))
