@@ -340,8 +340,8 @@ class AllenCahn(Application):
 
     def __init__(self, n=4096, eps=0.02, length=1.0, newton_tol=1e-12, newton_max=30,
                  initial_condition=None):
-        if n < 16 or n % 8 or n > 4096:
-            raise ConfigError("allen-cahn: n must be a multiple of 8 in [16, 4096]")
+        if n < 16 or n > 4096:
+            raise ConfigError("allen-cahn: n must be in [16, 4096]")
         if not (eps > 0.0 and length > 0.0):
             raise ConfigError("allen-cahn: bad eps/length")
         self.n, self.eps, self.length = n, eps, length

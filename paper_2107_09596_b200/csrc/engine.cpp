@@ -299,8 +299,7 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
         case ATM_PHI_ALLEN_CAHN:
             // BASELINE config 3 (no reference Phi; oracle/atm_oracle.c ac_step)
             n_ = p.n;
-            if (n_ < 16 || n_ % 8 != 0 || n_ > 4096)
-                config_error("allen-cahn: n must be a multiple of 8 in [16, 4096]");
+            if (n_ < 16 || n_ > 4096) config_error("allen-cahn: n must be in [16, 4096]");
             if (!(p.eps > 0.0) || !(p.length > 0.0)) config_error("allen-cahn: bad eps/length");
             if (!(p.newton_tol > 0.0) || p.newton_max < 1)
                 config_error("allen-cahn: newton_tol > 0 and newton_max >= 1 required");

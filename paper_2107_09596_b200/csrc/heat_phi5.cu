@@ -634,22 +634,32 @@ __device__ __forceinline__ void ac_residual(const double (&u)[L], const double (
                                             const Lane<L, NW>& ln, double* ends, double& sq,
                                             double& u2) {
     const int nt = blockDim.x;
+    // thread tl holds elements [tl L, tl L + pl) with element n-1 last: its
+    // chunk end is u[pl - 1], whose periodic right neighbour is element 0
+    const bool last = ln.t == co.tl;
+    double uend = u[L - 1];
+    if (last) {
+#pragma unroll
+        for (int e = 0; e < L - 1; ++e)
+            if (e == co.pl - 1) uend = u[e];
+    }
     ends[ln.t] = u[0];
-    ends[nt + ln.t] = u[L - 1];
+    ends[nt + ln.t] = uend;
     __syncthreads();
     const bool real = ln.t <= co.tl;
     const double ul = ends[nt + (ln.t == 0 ? co.tl : ln.t - 1)];
-    const double ur = ends[ln.t == co.tl ? 0 : ln.t + 1];
+    const double ur = ends[last ? 0 : ln.t + 1];
+    const int eend = last ? co.pl - 1 : L - 1;  // the chunk's last real element
     const double dt = co.ac_dt, c = co.ac_c;
     sq = 0.0;
     u2 = 0.0;
 #pragma unroll
     for (int e = 0; e < L; ++e) {
         const double a = e == 0 ? ul : u[e - 1];
-        const double b = e == L - 1 ? ur : u[e + 1];
+        const double b = e == eend ? ur : (e == L - 1 ? 0.0 : u[e + 1]);
         const double ui = u[e];
         const double lap = c * (a - 2.0 * ui + b);
-        const double f = real ? ui - dt * (lap + ui - ui * ui * ui) - up[e] : 0.0;
+        const double f = (real && e <= eend) ? ui - dt * (lap + ui - ui * ui * ui) - up[e] : 0.0;
         F[e] = f;
         sq = fma(f, f, sq);
         u2 = fmax(u2, ui * ui);

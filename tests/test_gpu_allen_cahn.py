@@ -38,7 +38,7 @@ def _pair(n, n_points, tf, ms, k, mode="v-cycle", tol=1e-9, max_iters=60, newton
     return app, hier, cfg, orc
 
 
-@pytest.mark.parametrize("n", [16, 64, 264, 1024, 4096])
+@pytest.mark.parametrize("n", [16, 17, 64, 100, 264, 1001, 1024, 4093, 4096])
 @pytest.mark.parametrize("level", [0, 1, 2])
 def test_ac_phi_matches_oracle(n, level):
     app, hier, cfg, orc = _pair(n, 257, 1.0, [8, 8], 4, substeps=2)
@@ -65,7 +65,7 @@ def test_ac_periodic_wrap_and_symmetry():
     assert rel_l2(-got[0], got[2]) <= 1e-13
 
 
-@pytest.mark.parametrize("n,n_points,tf,k", [(256, 513, 0.25, 4), (1024, 1025, 0.5, 2)])
+@pytest.mark.parametrize("n,n_points,tf,k", [(256, 513, 0.25, 4), (1024, 1025, 0.5, 2), (1001, 513, 0.25, 4)])
 def test_ac_fas_vcycle_matches_oracle(n, n_points, tf, k):
     app, hier, cfg, orc = _pair(n, n_points, tf, [8, 8], k)
     res = T.solve(app, hier, cfg)
