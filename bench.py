@@ -88,14 +88,50 @@ FLOPS_PER_PHI_DOF = 5.0
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and clock-event reasons during the timed region (B200_PROFILING.md
+    clocks line): NVML polled every 2 ms from a thread (the timed region of the
+    default run is ~60 ms), nvidia-smi at 200 ms as the fallback."""
 
     def __init__(self, index=0):
         self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
         self.proc = None
         self.index = index
+        self.nv = None
+        self.nv_sm, self.nv_reasons, self.nv_max = [], set(), None
+        try:
+            import threading
+
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv_max = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.stop = threading.Event()
+            self.th = threading.Thread(target=self._poll, daemon=True)
+        except Exception:
+            self.nv = None
+
+    def _poll(self):
+        nv = self.nv
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        while not self.stop.is_set():
+            try:
+                self.nv_sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, b in bits.items():
+                    if r & b:
+                        self.nv_reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __enter__(self):
+        if self.nv is not None:
+            self.th.start()
+            return self
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -109,6 +145,10 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        if self.nv is not None:
+            self.stop.set()
+            self.th.join(1.0)
+            return
         if self.proc:
             self.proc.terminate()
             try:
@@ -117,6 +157,11 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self.nv is not None:
+            sm = self.nv_sm
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.nv_max,
+                    "sm_min_mhz": min(sm) if sm else None, "reasons": sorted(self.nv_reasons),
+                    "samples": len(sm), "source": "NVML, 2 ms polling during the timed region"}
         sm, mx, reasons = [], 0.0, set()
         try:
             for line in open(self.path):
