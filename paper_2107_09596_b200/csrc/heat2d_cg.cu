@@ -218,96 +218,6 @@ __device__ void cg_phi(const CgCoefDev& co, Ctx& cx, double* xb, double* rb, int
     }
 }
 
-// Register variant (systems whose CTA band fits E elements per thread with
-// x on chip): r and A p stay in registers, the smem offsets of the owned
-// elements are computed once per call; one stencil pass per iteration.
-template <int E>
-__device__ void cg_phi_reg(const CgCoefDev& co, Ctx& cx, double* xb, int band, bool forced) {
-    const int W = cx.W;
-    const double c = co.c, diag = co.diag;
-    int off[E];
-    bool ok[E];
-    {
-        int row = cx.row0, col = cx.col0;
-        const int nx = W - 2;
-#pragma unroll
-        for (int k = 0; k < E; ++k) {
-            ok[k] = cx.t + k * cx.nt < cx.own;
-            off[k] = (row + 1) * W + col + 1;
-            col += cx.dr;
-            row += cx.dq;
-            if (col >= nx) {
-                col -= nx;
-                ++row;
-            }
-        }
-    }
-    for (int s = 0; s < co.substeps; ++s) {
-        double r[E];
-#pragma unroll
-        for (int k = 0; k < E; ++k)
-            if (ok[k]) cx.ps[off[k]] = xb[cx.t + k * cx.nt];
-        csync(cx);
-        halos(cx, co.nx, co.R);
-        double v2[2] = {0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < E; ++k) {
-            r[k] = 0.0;
-            if (ok[k]) {
-                double b = cx.ps[off[k]];
-                if (forced) b += co.sdt * __ldg(co.src + band + cx.t + k * cx.nt);
-                r[k] = b - stencil(cx.ps, off[k], W, diag, c);
-                v2[0] = fma(b, b, v2[0]);
-                v2[1] = fma(r[k], r[k], v2[1]);
-            }
-        }
-        cluster_sum<2>(v2, cx);
-        const double stop = co.rtol * sqrt(v2[0]);
-        double rr = v2[1];
-#pragma unroll
-        for (int k = 0; k < E; ++k)
-            if (ok[k]) cx.ps[off[k]] = r[k];
-        int it = 0;
-        while (sqrt(rr) > stop) {
-            if (it >= co.cg_max) {
-                if (cx.t == 0 && cx.q == 0) atomicExch(co.fail, 1);
-                break;
-            }
-            csync(cx);
-            halos(cx, co.nx, co.R);
-            double ap[E];
-            double pap[1] = {0.0};
-#pragma unroll
-            for (int k = 0; k < E; ++k) {
-                ap[k] = 0.0;
-                if (ok[k]) {
-                    ap[k] = stencil(cx.ps, off[k], W, diag, c);
-                    pap[0] = fma(cx.ps[off[k]], ap[k], pap[0]);
-                }
-            }
-            cluster_sum<1>(pap, cx);
-            const double alpha = rr / pap[0];
-            double rn[1] = {0.0};
-#pragma unroll
-            for (int k = 0; k < E; ++k) {
-                if (ok[k]) {
-                    xb[cx.t + k * cx.nt] += alpha * cx.ps[off[k]];
-                    r[k] -= alpha * ap[k];
-                    rn[0] = fma(r[k], r[k], rn[0]);
-                }
-            }
-            cluster_sum<1>(rn, cx);
-            const double beta = rn[0] / rr;
-            rr = rn[0];
-#pragma unroll
-            for (int k = 0; k < E; ++k)
-                if (ok[k]) cx.ps[off[k]] = r[k] + beta * cx.ps[off[k]];
-            ++it;
-        }
-        if (co.iters && cx.t == 0 && cx.q == 0) atomicAdd(co.iters, static_cast<unsigned long long>(it));
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Strip kernel (systems up to nx = 255): one cluster barrier per CG iteration.
 //
@@ -1112,8 +1022,6 @@ __device__ __forceinline__ void cg_phi_any(const CgCoefDev& co, Ctx& cx, double*
         cg_phi_strip<E % 1000, true>(co, cx, xb, band, forced);
     } else if constexpr (E >= 1000) {
         cg_phi_strip<E % 1000, false>(co, cx, xb, band, forced);
-    } else if constexpr (E > 0) {
-        cg_phi_reg<E>(co, cx, xb, band, forced);
     } else {
         cg_phi(co, cx, xb, rb, band, forced);
     }
@@ -1355,15 +1263,12 @@ CgKernels cg_k() {
             reinterpret_cast<const void*>(cg_window_kernel<E>)};
 }
 
-// E = 0: generic (x, r via pointers, A p recomputed); E > 0: register variant
+// E = 0: round-1 cluster CG (p in shared memory, x and r shared or global);
+// E = -1: Gray-Scott; 1000 + e / 2000 + e: strip kernel (512 / 256 threads);
+// 3000 + e: strip kernel, group mode
 CgKernels cg_kernels(int E) {
     switch (E) {
         case -1: return cg_k<-1>();
-        case 1: return cg_k<1>();
-        case 2: return cg_k<2>();
-        case 4: return cg_k<4>();
-        case 8: return cg_k<8>();
-        case 16: return cg_k<16>();
         case 1002: return cg_k<1002>();
         case 1004: return cg_k<1004>();
         case 2008: return cg_k<2008>();
@@ -1517,13 +1422,6 @@ void cg_geometry(int nx, CgCoefDev& co) {
     const int own = co.R * nx;
     co.E = 0;
     co.nt = std::min(kMaxCgThreads, std::max(64, (own + 31) / 32 * 32));
-    if (pick_sm && own <= 512 * 16) {
-        // register variant: up to 512 threads x E elements (E a power of two)
-        int E = 1;
-        while (E < 16 && 512 * E < own) E *= 2;
-        co.E = E;
-        co.nt = std::max(64, ((own + E - 1) / E + 31) / 32 * 32);
-    }
 }
 
 bool gs_geometry(int nx, CgCoefDev& co, int cs) {
