@@ -53,9 +53,11 @@ CUtensorMap make_row_map(double* ptr, int rows, int pitch) {
     const cuuint64_t dims[2] = {16, static_cast<cuuint64_t>(rows) * (pitch / 16)};
     const cuuint64_t strides[1] = {128};
     // a box holds at most 256 rows of the view: longer point rows (pitch a
-    // multiple of 256) are moved as two half-row boxes (tma_load_row)
+    // multiple of 256) are moved as two half-row boxes (tma_load_row), rows
+    // split over a cluster (pitch a multiple of 4096 past 8192) as one box per
+    // CTA part
     const int R = pitch / 16;
-    const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(R <= 256 ? R : R / 2)};
+    const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(R <= 256 ? R : R <= 512 ? R / 2 : 256)};
     const cuuint32_t es[2] = {1, 1};
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, ptr, dims, strides, box,
                                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -283,9 +285,13 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
             n_ = p.n;
             if (n_ < 1) config_error("heat1d: need at least one spatial unknown");
             if (!(p.x1 > p.x0)) config_error("heat1d: x1 must exceed x0");
-            // one CTA holds one state vector; the FAS window kernel stages five
-            // rows in shared memory (5 x 42 KB at n = 5376 of the 227 KB)
-            if (n_ > 5376) config_error("heat1d: n > 5376 exceeds the single-CTA row kernels (five staged rows per CTA)");
+            // one CTA holds one state vector up to n = 5376 (the FAS window
+            // kernel stages five rows, 5 x 42 KB of the 227 KB); past that a
+            // row is split over a cluster of up to 8 CTAs of 4096 elements
+            if (n_ > kMaxCluster * 4096)
+                config_error("heat1d: n > " + std::to_string(kMaxCluster * 4096) +
+                             " exceeds a cluster of " + std::to_string(kMaxCluster) + " row CTAs");
+            if (n_ > 5376) cl_ = (n_ + 4095) / 4096;
             heat_ = true;
             folded_ = p.folded != 0;
             break;
@@ -375,6 +381,8 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     // a 128B-swizzled box must start 1024-byte aligned), so the row is padded
     // to a multiple of 256 (padding stays 0)
     if (heat_ && !ac_ && pitch_ > 4096) pitch_ = ((n_ + 255) / 256) * 256;
+    // rows split over a cluster: CTA q holds elements [4096 q, 4096 q + 4096)
+    if (cl_ > 1) pitch_ = 4096 * cl_;
     // host copies of caller-owned inputs
     ic_.assign(n_, 0.0);
     if (heat_ && !ac_) {
@@ -444,6 +452,7 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
         if (pitch_ > 2048 && (l < H_.coarsest() || std::getenv("ATM_WIN_L32"))) L = 32;
         if (const char* e = std::getenv("ATM_HEAT_L")) L = std::atoi(e);
         if (ac_) L = 8;
+        if (cl_ > 1) L = 32;  // cluster rows: 128 threads x 32 elements per CTA part
         Lvl_[l] = L;
     }
 
@@ -619,10 +628,17 @@ void Engine::build_coefs(Shard& s) {
                                           ((prob_.length / n_) * (prob_.length / n_))
                                     : 0.0;
             const double ac_s = 1.5 * sub_dt;
-            const HeatLevelHost hh =
+            HeatLevelHost hh =
                 ac_ ? heat_level_host(n_, pitch_, Lvl_[l], sub_dt * ac_c, ac_s - sub_dt, S, true)
-                    : heat_level_host(n_, pitch_, Lvl_[l], sub_dt / (h_ * h_), 0.0, S, false);
+                : cl_ > 1 ? heat_cluster_host(n_, cl_, sub_dt / (h_ * h_), S)
+                          : heat_level_host(n_, pitch_, Lvl_[l], sub_dt / (h_ * h_), 0.0, S, false);
             HeatCoefDev& c = Lv.hco;
+            c.cl = cl_;
+            c.blk = c.cS = nullptr;
+            if (cl_ > 1) {
+                c.blk = up(hh.blk);
+                c.cS = up(hh.cS);
+            }
             c.xw = up(hh.xw);
             c.cyclic = hh.cyclic;
             c.ncw_r0 = hh.ncw_r0;
@@ -672,7 +688,7 @@ void Engine::build_coefs(Shard& s) {
                             sub_dt * (-(std::sin(t) - kPi * kPi * std::cos(t)));
                     }
                 c.theta = up(th);
-                std::vector<double> prof(static_cast<size_t>(hh.nt) * hh.L, 0.0);
+                std::vector<double> prof(std::max(static_cast<size_t>(hh.nt) * hh.L, static_cast<size_t>(pitch_)), 0.0);
                 for (int i = 0; i < n_; ++i) prof[i] = sinp_[i];
                 c.prof = up(prof);
             }

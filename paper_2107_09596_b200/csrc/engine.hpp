@@ -235,6 +235,7 @@ private:
     int* d_fail_ = nullptr;   // Allen-Cahn Newton / heat2d CG failure flag
     unsigned long long* d_inner_ = nullptr;  // inner CG / BiCGSTAB iterations run so far
     double* d_src_ = nullptr; // heat2d source f
+    int cl_ = 1;              // heat1d rows split over a cluster of cl_ CTAs (n > 5376)
     double* d_xg_ = nullptr;  // heat2d CG x scratch (one row per resident cluster)
     double* d_gex_ = nullptr;  // heat2d CG group mode: exchange rows / partials per group
     unsigned long long* d_gflag_ = nullptr;  // heat2d CG group mode: per-CTA sequence flags

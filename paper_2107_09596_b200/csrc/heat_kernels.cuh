@@ -18,6 +18,7 @@ namespace atm {
 constexpr int kMaxThreads = 512;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr int kMaxL = 32;
+constexpr int kMaxCluster = 8;  // CTAs per cluster row (heat1d n <= 8 x 4096)
 constexpr int kScanPerThread = 18;  // Mf[5], Pf_ex, Mb[5], Pb_ex, SB, q0, cfw, cbw, pad, cbwr
 
 // Device view of one level's Phi coefficients.
@@ -57,11 +58,23 @@ struct HeatCoefDev {
     int* fail;             // set to 1 when Newton hits newton_max
     int n, pitch, nt, L;
     int substeps;
+    // rows split over a cluster of `cl` CTAs (n > 5376): CTA q of the cluster
+    // holds elements [4096 q, 4096 q + 4096) of every row (nt = 128, L = 32);
+    // the tables above are per block, concatenated ([cl][...]); blk: per-block
+    // ncw, ncw_r0, tl, pl, ql, pbl (8 doubles each); cS: the 2cl x 2cl
+    // Woodbury matrix coupling the blocks (heat_phi5.cu, cluster rows)
+    int cl;
+    const double* blk;
+    const double* cS;
 };
 
 // Host-side construction of a level's coefficients (heat1d.cpp:24-45).
 struct HeatLevelHost {
     std::vector<double> scan, wf, wb, wk, powc, xw;
+    // cyclic: first / last entries of wl = M^{-1} e_0 and wr = M^{-1} e_{n-1}
+    long double w0 = 0, wn = 0, wr0 = 0, wrn = 0;
+    // cluster rows: per-block scalars and the coupling matrix (HeatCoefDev)
+    std::vector<double> blk, cS;
     double r = 0, beta_c = 0, gamma_c = 0, cneg_c = 0, sigma = 0;
     double S[4] = {0, 0, 0, 0}, ql = 0, pbl = 0;
     int cyclic = 0, ncw_r0 = 0, tl = 0, pl = 0;
@@ -71,6 +84,9 @@ struct HeatLevelHost {
 // r = sub_dt/h^2 (a = -r, diagonal 1 + 2r + shift); cyclic: periodic corners
 HeatLevelHost heat_level_host(int n, int pitch, int L, double r, double shift, int substeps,
                               bool cyclic);
+// rows of n > 5376 split over cl CTAs of 4096 elements (L = 32, 128 threads
+// each): per-block tables concatenated, and the block coupling
+HeatLevelHost heat_cluster_host(int n, int cl, double r, int substeps);
 
 // Job kinds of the sweep kernel (one job per C-point index J of a level).
 enum SweepKind { SW_F = 0, SW_FCF = 1, SW_CRELAX = 2, SW_RESID = 3 };

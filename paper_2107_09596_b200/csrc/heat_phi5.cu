@@ -43,6 +43,7 @@
 //   residual / restrict kernels.cpp:30-43, solver.cpp:174-185 -> tails, SW_RESID
 //   window solves       kernels.cpp:53-88     -> heat_window_*_kernel
 //   point squares       kernels.cpp:90-95     -> TAIL_SQ (fixed-order tree)
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -56,6 +57,8 @@
 #include "tma.cuh"
 
 namespace atm {
+
+namespace cg = cooperative_groups;
 
 // --------------------------------------------------------------------------
 // host: fixed-point factors, correction vectors and every scan multiplier
@@ -103,6 +106,10 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double r_in, double shift
             }
         }
     }
+    H.w0 = w[0];
+    H.wn = w[n - 1];
+    H.wr0 = wr[0];
+    H.wrn = wr[n - 1];
     // Woodbury: T = M + U C U^T, U = [e0, e_{n-1}], C = [[delta, a], [a, 0]]
     // (cyclic) or U = e0, C = delta; T^{-1} b = M^{-1} b - W S U^T M^{-1} b,
     // S = (C^{-1} + U^T W)^{-1}
@@ -313,6 +320,103 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double r_in, double shift
     return H;
 }
 
+// Rows split over a cluster (n > 5376): block q = elements [4096 q, 4096 q +
+// n_q) of the row, n_q = min(4096, n - 4096 q), one CTA each.  With M_q =
+// L_c U_c the constant-coefficient factorisation of block q,
+//   T = blockdiag(M_q) + U C U^T,  U = [e_{s_0}, e_{e_0}, e_{s_1}, e_{e_1}, ...]
+// (s_q, e_q: first and last element of block q), C = the Dirichlet delta at
+// every block start and the coupling a between e_q and s_{q+1}; so
+//   x = M^{-1} b - M^{-1} U s,  s = S' U^T M^{-1} b,  S' = (I + C U^T M^{-1} U)^{-1} C.
+// Each block's M_q^{-1} e_{s_q} and M_q^{-1} e_{e_q} are the cyclic solve's
+// two correction vectors (heat_level_host with cyclic = true), applied through
+// the chunk carries exactly as the periodic Allen-Cahn matrix does; U^T M^{-1} b
+// is every block's (x0, xn), exchanged over the cluster (tri_solve, CL).
+HeatLevelHost heat_cluster_host(int n, int cl, double r, int substeps) {
+    using LD = long double;
+    std::vector<HeatLevelHost> B(static_cast<size_t>(cl));
+    for (int q = 0; q < cl; ++q)
+        B[q] = heat_level_host(std::min(4096, n - 4096 * q), 4096, 32, r, 0.0, substeps, true);
+    HeatLevelHost H = B[0];
+    H.n = n;
+    H.pitch = 4096 * cl;
+    H.cyclic = 0;
+    H.scan.clear();
+    H.wf.clear();
+    H.wb.clear();
+    H.wk.clear();
+    H.powc.clear();
+    H.xw.clear();
+    H.blk.assign(static_cast<size_t>(8) * cl, 0.0);
+    for (int q = 0; q < cl; ++q) {
+        const HeatLevelHost& b = B[q];
+        H.scan.insert(H.scan.end(), b.scan.begin(), b.scan.end());
+        H.wf.insert(H.wf.end(), b.wf.begin(), b.wf.end());
+        H.wb.insert(H.wb.end(), b.wb.begin(), b.wb.end());
+        H.wk.insert(H.wk.end(), b.wk.begin(), b.wk.end());
+        H.powc.insert(H.powc.end(), b.powc.begin(), b.powc.end());
+        H.xw.insert(H.xw.end(), b.xw.begin(), b.xw.end());
+        double* bk = &H.blk[static_cast<size_t>(8) * q];
+        bk[0] = b.ncw;
+        bk[1] = b.ncw_r0;
+        bk[2] = b.tl;
+        bk[3] = b.pl;
+        bk[4] = b.ql;
+        bk[5] = b.pbl;
+        H.fit_err = std::max(H.fit_err, b.fit_err);
+    }
+    // S' = (I + C G)^{-1} C, G = U^T M^{-1} U (2x2 blocks on the diagonal)
+    const int m2 = 2 * cl;
+    const LD a = -static_cast<LD>(r), c = -static_cast<LD>(H.cneg_c);
+    const LD delta = a * c;
+    std::vector<LD> G(static_cast<size_t>(m2) * m2, 0.0L), Cm(G), A(G), X(G);
+    for (int q = 0; q < cl; ++q) {
+        const int i = 2 * q;
+        G[i * m2 + i] = B[q].w0;
+        G[i * m2 + i + 1] = B[q].wr0;
+        G[(i + 1) * m2 + i] = B[q].wn;
+        G[(i + 1) * m2 + i + 1] = B[q].wrn;
+        Cm[i * m2 + i] = delta;
+        if (q + 1 < cl) {
+            Cm[(i + 1) * m2 + i + 2] = a;
+            Cm[(i + 2) * m2 + i + 1] = a;
+        }
+    }
+    for (int i = 0; i < m2; ++i)
+        for (int j = 0; j < m2; ++j) {
+            LD v = (i == j) ? 1.0L : 0.0L;
+            for (int k = 0; k < m2; ++k) v += Cm[i * m2 + k] * G[k * m2 + j];
+            A[i * m2 + j] = v;
+            X[i * m2 + j] = Cm[i * m2 + j];
+        }
+    // Gauss-Jordan with partial pivoting: A X = C
+    for (int col = 0; col < m2; ++col) {
+        int piv = col;
+        for (int i = col + 1; i < m2; ++i)
+            if (std::fabs(A[i * m2 + col]) > std::fabs(A[piv * m2 + col])) piv = i;
+        for (int j = 0; j < m2; ++j) {
+            std::swap(A[col * m2 + j], A[piv * m2 + j]);
+            std::swap(X[col * m2 + j], X[piv * m2 + j]);
+        }
+        const LD d = A[col * m2 + col];
+        for (int j = 0; j < m2; ++j) {
+            A[col * m2 + j] /= d;
+            X[col * m2 + j] /= d;
+        }
+        for (int i = 0; i < m2; ++i) {
+            if (i == col) continue;
+            const LD f = A[i * m2 + col];
+            if (f == 0.0L) continue;
+            for (int j = 0; j < m2; ++j) {
+                A[i * m2 + j] -= f * A[col * m2 + j];
+                X[i * m2 + j] -= f * X[col * m2 + j];
+            }
+        }
+    }
+    H.cS.resize(static_cast<size_t>(m2) * m2);
+    for (size_t i = 0; i < H.cS.size(); ++i) H.cS[i] = static_cast<double>(X[i]);
+    return H;
+}
+
 // one point row into shared memory: R = pitch / 16 rows of the tensor map's
 // [rows][16] view -- one box, or past 256 rows (the TMA box limit) two
 // half-row boxes; pitch is then a multiple of 256, so the second half lands
@@ -339,7 +443,7 @@ __device__ __forceinline__ void tma_store_row(const CUtensorMap* map, int c0, in
 // NW: warps per CTA of the instantiation (the cross-warp carry tree)
 __host__ __device__ constexpr int warps_for(int L) { return L >= 32 ? 4 : (L == 16 ? 8 : 16); }
 
-template <int L, int NW = warps_for(L)>
+template <int L, int NW = warps_for(L), bool CL = false>
 struct Lane {
     int t, lane, warp, nw, s;
     int q7, qx, qx1, ch0;  // swizzled row-staging geometry (L = 32: two 128-B rows)
@@ -350,25 +454,47 @@ struct Lane {
     double Mf[5], Pfex, Mb[5], Pbex, SB, q0;
     double cfw, cbw;     // correction carries of the chunk (left vector)
     double cbwr;         // cyclic: right correction vector's p_b coefficient
+    // cluster rows (CL): rank of the CTA in the cluster (its block of the
+    // row) and the block's x_{n-1} pick-up (thread tl, element pl - 1)
+    int q, btl, bpl;
+    double bql, bpbl;
 };
 
-template <int L, int NW>
-__device__ __forceinline__ void lane_init(Lane<L, NW>& ln, const HeatCoefDev& co) {
+template <int L, int NW, bool CL>
+__device__ __forceinline__ void lane_init(Lane<L, NW, CL>& ln, const HeatCoefDev& co) {
     ln.t = threadIdx.x;
     ln.lane = ln.t & 31;
     ln.warp = ln.t >> 5;
     ln.nw = blockDim.x >> 5;
-    ln.s = ln.t * L;
-    ln.corr = ln.warp < co.ncw || ln.warp >= co.ncw_r0;
+    // the staging geometry is local to the CTA's part of the row; element
+    // offsets (padding, forcing profile) and the tables are the row's
+    const int sloc = ln.t * L;
+    ln.q = 0;
+    int gt = ln.t;
+    if constexpr (CL) {
+        ln.q = static_cast<int>(cg::this_cluster().block_rank());
+        gt += ln.q * blockDim.x;
+        const double* b = co.blk + 8 * ln.q;
+        ln.corr = ln.warp < static_cast<int>(b[0]) || ln.warp >= static_cast<int>(b[1]);
+        ln.btl = static_cast<int>(b[2]);
+        ln.bpl = static_cast<int>(b[3]);
+        ln.bql = b[4];
+        ln.bpbl = b[5];
+    } else {
+        ln.corr = ln.warp < co.ncw || ln.warp >= co.ncw_r0;
+        ln.btl = ln.bpl = 0;
+        ln.bql = ln.bpbl = 0.0;
+    }
+    ln.s = gt * L;
     ln.inside = ln.s < co.pitch;  // chunks never straddle pitch (pitch % 16 == 0)
-    ln.q7 = (ln.s >> 4) << 7;
-    ln.qx = (ln.s >> 4) & 7;
-    ln.ch0 = (ln.s & 15) >> 1;
+    ln.q7 = (sloc >> 4) << 7;
+    ln.qx = (sloc >> 4) & 7;
+    ln.ch0 = (sloc & 15) >> 1;
     ln.qx1 = (ln.qx + 1) & 7;
     ln.pad0 = (ln.s + L > co.n) ? max(0, co.n - ln.s) : L;
     ln.pad_last = ln.pad0 == L - 1;
     ln.par = 0;
-    const double* sc = co.scan + ln.t * kScanPerThread;
+    const double* sc = co.scan + gt * kScanPerThread;
 #pragma unroll
     for (int d = 0; d < 5; ++d) {
         ln.Mf[d] = __ldg(sc + d);
@@ -399,18 +525,24 @@ struct Slots {                // small shared scratch
     double z0[2], ra0[2];     // thread 0's z_loc[0] and RA_next (ncw > 1)
     double zl[2], el[2], ral[2];  // cyclic: thread tl's z_loc[pl-1], E, RA_next
     double nrm[2][kMaxWarps][2];  // Newton: per-warp residual square sums, max u^2
+    double cz[2][kMaxCluster][2];  // cluster rows: every block's (x0, xn), by parity
+    double csq[kMaxCluster];       // cluster rows: every block's tail square sum
     uint64_t bar[5];
 };
 
-__device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev& co) {
+// q: the CTA's block of a cluster row (its tables; 0 otherwise)
+__device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev& co, int q = 0) {
+    const double* wf = co.wf + q * kMaxWarps * kMaxWarps;
+    const double* wb = co.wb + q * kMaxWarps * kMaxWarps;
+    const double* wk = co.wk + q * kMaxWarps * kMaxWarps;
     for (int i = threadIdx.x; i < kMaxWarps * kMaxWarps; i += blockDim.x) {
-        tb.wf[i] = co.wf[i];
-        tb.wb[i] = co.wb[i];
-        tb.wk[i] = co.wk[i];
+        tb.wf[i] = wf[i];
+        tb.wb[i] = wb[i];
+        tb.wk[i] = wk[i];
     }
-    for (int i = threadIdx.x; i < 3 * kMaxL; i += blockDim.x) tb.powc[i] = co.powc[i];
-    if (threadIdx.x == 0) tb.pbex0 = co.scan[11];
-    for (int i = threadIdx.x; i < 4 * kMaxWarps; i += blockDim.x) tb.xw[i] = co.xw[i];
+    for (int i = threadIdx.x; i < 3 * kMaxL; i += blockDim.x) tb.powc[i] = co.powc[q * 3 * kMaxL + i];
+    if (threadIdx.x == 0) tb.pbex0 = co.scan[static_cast<size_t>(q) * blockDim.x * kScanPerThread + 11];
+    for (int i = threadIdx.x; i < 4 * kMaxWarps; i += blockDim.x) tb.xw[i] = co.xw[q * 4 * kMaxWarps + i];
     // warp slots beyond the CTA are read with zero weights: keep them finite
     for (int i = threadIdx.x; i < 2 * kMaxWarps; i += blockDim.x) {
         sl.tf[i / kMaxWarps][i % kMaxWarps] = 0.0;
@@ -423,8 +555,8 @@ __device__ __forceinline__ void tabs_init(Tabs& tb, Slots& sl, const HeatCoefDev
 // n = k L - 1) is a select with no branch; otherwise a fall-through switch:
 // one jump and L - pad0 moves for that thread instead of L predicated
 // selects in its whole warp.
-template <int L, int NW>
-__device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L, NW>& ln) {
+template <int L, int NW, bool CL>
+__device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L, NW, CL>& ln) {
     x[L - 1] = ln.pad_last ? 0.0 : x[L - 1];
     if (ln.pad0 < L - 1) {
         switch (ln.pad0) {
@@ -470,8 +602,8 @@ __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L, NW>& 
 // warps per CTA of the instantiation for chunk length L (a power of two):
 // L = 32 -> 128 threads, L = 16 -> 256, L <= 8 -> 512
 
-template <int L, bool CYC = false, int NW = warps_for(L)>
-__device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L, NW>& ln,
+template <int L, bool CYC = false, int NW = warps_for(L), bool CL = false>
+__device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L, NW, CL>& ln,
                                           const Tabs& tb, Slots& sl) {
     // 1. forward local  y_i = beta x_i + gamma y_{i-1}
     double y = 0.0;
@@ -514,18 +646,22 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     const int par = ln.par;
     if (ln.lane == 31) sl.tf[par][ln.warp] = B;
     if (ln.lane == 0) sl.ta[par][ln.warp] = R;
-    const bool far = !CYC && ln.corr && ln.warp > 0;  // correction warp without warp 0's D
+    // CL (cluster rows) runs the cyclic machinery: every block carries a left
+    // and a right correction vector, coupled across the cluster below
+    constexpr bool WB = CYC || CL;
+    const bool far = !WB && ln.corr && ln.warp > 0;  // correction warp without warp 0's D
     double z00 = 0.0, ra0 = 0.0;
-    if (CYC) {
+    if (WB) {
+        const int tl = CL ? ln.btl : co.tl, pl = CL ? ln.bpl : co.pl;
         if (ln.t == 0) {
             sl.z0[par] = x[0];
             sl.ra0[par] = RAn;
         }
-        if (ln.t == co.tl) {
+        if (ln.t == tl) {
             double zl = x[0];
 #pragma unroll
             for (int e = 1; e < L; ++e)
-                if (e == co.pl - 1) zl = x[e];
+                if (e == pl - 1) zl = x[e];
             sl.zl[par] = zl;
             sl.el[par] = E;
             sl.ral[par] = RAn;
@@ -550,7 +686,7 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
         cC = tb.wf[row] * tf;
         cD = fma(tb.wb[row], ta, tb.wk[row] * tf);
         if (far) cD0 = fma(tb.wb[v], ta, tb.wk[v] * tf);
-        if (CYC && ln.corr) {
+        if (WB && ln.corr) {
             p0 = fma(tb.xw[v], tf, tb.xw[kMaxWarps + v] * ta);
             pN = fma(tb.xw[2 * kMaxWarps + v], tf, tb.xw[3 * kMaxWarps + v] * ta);
         }
@@ -564,7 +700,7 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
             for (int off = NW / 2; off >= 1; off >>= 1)
                 cD0 += __shfl_xor_sync(0xffffffffu, cD0, off);
         }
-        if (CYC && ln.corr) {
+        if (WB && ln.corr) {
 #pragma unroll
             for (int off = NW / 2; off >= 1; off >>= 1) {
                 p0 += __shfl_xor_sync(0xffffffffu, p0, off);
@@ -574,7 +710,39 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
     }
     double cf = fma(ln.Pfex, cC, E);
     double cb = fma(ln.Pbex, cD, fma(ln.SB, cC, RAn));
-    if (CYC) {
+    if constexpr (CL) {
+        // cluster rows: T = blockdiag(M_q) + U C U^T over every block's first
+        // and last element (C: the Dirichlet delta at each block start, the
+        // coupling a between neighbouring blocks); x = M^{-1}b - W s with
+        // s = S' U^T M^{-1} b, S' = (I + C U^T W)^{-1} C (host, long double).
+        // Every block's (x0, xn) goes to every CTA; all sum in one order.
+        double x0 = 0.0, xn = 0.0;
+        if (ln.corr) {
+            x0 = fma(tb.powc[kMaxL], sl.ra0[par], sl.z0[par]) + p0;
+            xn = fma(ln.bpbl, sl.ral[par], fma(ln.bql, sl.el[par], sl.zl[par])) + pN;
+        }
+        cg::cluster_group clu = cg::this_cluster();
+        if (ln.t == 0)
+            for (int r = 0; r < co.cl; ++r) {
+                double* d = clu.map_shared_rank(&sl.cz[par][ln.q][0], r);
+                d[0] = x0;
+                d[1] = xn;
+            }
+        clu.sync();
+        if (ln.corr) {
+            const int m2 = 2 * co.cl;
+            const double* r0 = co.cS + static_cast<size_t>(2 * ln.q) * m2;
+            const double* r1 = r0 + m2;
+            double s0 = 0.0, s1 = 0.0;
+            for (int j = 0; j < co.cl; ++j) {
+                const double zj0 = sl.cz[par][j][0], zj1 = sl.cz[par][j][1];
+                s0 = fma(__ldg(r0 + 2 * j), zj0, fma(__ldg(r0 + 2 * j + 1), zj1, s0));
+                s1 = fma(__ldg(r1 + 2 * j), zj0, fma(__ldg(r1 + 2 * j + 1), zj1, s1));
+            }
+            cf = fma(-s0, ln.cfw, cf);
+            cb = fma(-s0, ln.cbw, fma(-s1, ln.cbwr, cb));
+        }
+    } else if (CYC) {
         if (ln.corr) {
             // Woodbury: s = S [x0, xn], x -= s0 wl + s1 wr
             const double x0 = fma(tb.powc[kMaxL], sl.ra0[par], sl.z0[par]) + p0;
@@ -605,8 +773,8 @@ __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co,
 
 // Phi_index on this level: S sub-steps, forcing added before each solve
 // when `forced` (heat1d.cpp:66-83).
-template <int L, int NW>
-__device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, Lane<L, NW>& ln,
+template <int L, int NW, bool CL>
+__device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, Lane<L, NW, CL>& ln,
                                     const Tabs& tb, Slots& sl, int index, int forced) {
     for (int s = 0; s < co.substeps; ++s) {
         if (forced) {
@@ -628,10 +796,10 @@ __device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, Lane<
 // rho <= max(s, 3 dt umax^2 - s) / (1 - dt + s), iterated to rho^K <= eta.
 // Chunk ends travel through smem (one barrier per residual); the residual
 // norm and max u^2 ride on a second barrier.
-template <int L, int NW>
+template <int L, int NW, bool CL>
 __device__ __forceinline__ void ac_residual(const double (&u)[L], const double (&up)[L],
                                             double (&F)[L], const HeatCoefDev& co,
-                                            const Lane<L, NW>& ln, double* ends, double& sq,
+                                            const Lane<L, NW, CL>& ln, double* ends, double& sq,
                                             double& u2) {
     const int nt = blockDim.x;
     // thread tl holds elements [tl L, tl L + pl) with element n-1 last: its
@@ -666,8 +834,8 @@ __device__ __forceinline__ void ac_residual(const double (&u)[L], const double (
     }
 }
 
-template <int L, int NW>
-__device__ __forceinline__ void ac_reduce(double sq, double u2, const Lane<L, NW>& ln, Slots& sl,
+template <int L, int NW, bool CL>
+__device__ __forceinline__ void ac_reduce(double sq, double u2, const Lane<L, NW, CL>& ln, Slots& sl,
                                           int par, double& res, double& umax2) {
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
@@ -688,8 +856,8 @@ __device__ __forceinline__ void ac_reduce(double sq, double u2, const Lane<L, NW
     res = sqrt(res);
 }
 
-template <int L, int NW>
-__device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, Lane<L, NW>& ln,
+template <int L, int NW, bool CL>
+__device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, Lane<L, NW, CL>& ln,
                                        const Tabs& tb, Slots& sl, double* ends) {
     int rpar = 0;
     for (int s = 0; s < co.substeps; ++s) {
@@ -736,8 +904,8 @@ __device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, La
 }
 
 // problem dispatch: P = 0 heat (forcing optional), P = 1 Allen-Cahn
-template <int P, int L, int NW>
-__device__ __forceinline__ void phi_p(double (&x)[L], const HeatCoefDev& co, Lane<L, NW>& ln,
+template <int P, int L, int NW, bool CL>
+__device__ __forceinline__ void phi_p(double (&x)[L], const HeatCoefDev& co, Lane<L, NW, CL>& ln,
                                       const Tabs& tb, Slots& sl, double* ends, int index,
                                       int forced) {
     if constexpr (P == 1) ac_phi<L>(x, co, ln, tb, sl, ends);
@@ -750,8 +918,8 @@ __device__ __forceinline__ void phi_p(double (&x)[L], const HeatCoefDev& co, Lan
 // position c ^ (q & 7).
 
 // byte offset of element pair c (elements 2c, 2c+1) of this thread's chunk
-template <int L, int NW>
-__device__ __forceinline__ int pair_off(const Lane<L, NW>& ln, int c) {
+template <int L, int NW, bool CL>
+__device__ __forceinline__ int pair_off(const Lane<L, NW, CL>& ln, int c) {
     if constexpr (L == 32) {
         const int half = c >> 3, cc = c & 7;
         return ln.q7 + (half << 7) + ((cc ^ (half ? ln.qx1 : ln.qx)) << 4);
@@ -760,8 +928,8 @@ __device__ __forceinline__ int pair_off(const Lane<L, NW>& ln, int c) {
     }
 }
 
-template <int L, int NW>
-__device__ __forceinline__ void row_load(const char* buf, double (&x)[L], const Lane<L, NW>& ln) {
+template <int L, int NW, bool CL>
+__device__ __forceinline__ void row_load(const char* buf, double (&x)[L], const Lane<L, NW, CL>& ln) {
     if (ln.inside) {
 #pragma unroll
         for (int c = 0; c < L / 2; ++c) {
@@ -775,8 +943,8 @@ __device__ __forceinline__ void row_load(const char* buf, double (&x)[L], const 
     }
 }
 
-template <int L, int NW>
-__device__ __forceinline__ void row_store(char* buf, const double (&x)[L], const Lane<L, NW>& ln) {
+template <int L, int NW, bool CL>
+__device__ __forceinline__ void row_store(char* buf, const double (&x)[L], const Lane<L, NW, CL>& ln) {
     if (ln.inside) {
 #pragma unroll
         for (int c = 0; c < L / 2; ++c)
@@ -785,8 +953,8 @@ __device__ __forceinline__ void row_store(char* buf, const double (&x)[L], const
 }
 
 // x = x + row, or x = x - row
-template <int L, int NW>
-__device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], const Lane<L, NW>& ln,
+template <int L, int NW, bool CL>
+__device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], const Lane<L, NW, CL>& ln,
                                         bool sub) {
     if (ln.inside) {
 #pragma unroll
@@ -805,8 +973,8 @@ __device__ __forceinline__ void row_acc(const char* buf, double (&x)[L], const L
 
 // fixed-order CTA reduction of sum x_e^2 (thread order, then warp xor tree,
 // then warps in order): depends only on the CTA shape
-template <int L, int NW>
-__device__ __forceinline__ double cta_sum_squares(const double (&x)[L], const Lane<L, NW>& ln,
+template <int L, int NW, bool CL>
+__device__ __forceinline__ double cta_sum_squares(const double (&x)[L], const Lane<L, NW, CL>& ln,
                                                   Slots& sl) {
     double s = 0.0;
 #pragma unroll
@@ -817,6 +985,16 @@ __device__ __forceinline__ double cta_sum_squares(const double (&x)[L], const La
     __syncthreads();
     double tot = 0.0;
     for (int w = 0; w < ln.nw; ++w) tot += sl.red[w];
+    if constexpr (CL) {
+        // cluster rows: every block's sum to every CTA, added in block order
+        cg::cluster_group clu = cg::this_cluster();
+        if (ln.t == 0)
+            for (int r = 0; r < static_cast<int>(clu.num_blocks()); ++r)
+                *clu.map_shared_rank(&sl.csq[ln.q], r) = tot;
+        clu.sync();
+        tot = 0.0;
+        for (int r = 0; r < static_cast<int>(clu.num_blocks()); ++r) tot += sl.csq[r];
+    }
     return tot;
 }
 
@@ -837,7 +1015,7 @@ __host__ __device__ inline int row_bytes_al(int pitch) { return ((pitch * 8) + 1
 // sweep kernel: F / fused FCF / C-relax / residual jobs over C-point indices
 // smem: [S seed/tail][O0][O1 if n_out=2][A if add_g][Tabs][Slots]
 
-template <int L, int NTMAX, int MINB, int P>
+template <int L, int NTMAX, int MINB, int P, bool CLU = false>
 __global__ void __launch_bounds__(NTMAX, MINB)
     heat_sweep_kernel(const __grid_constant__ SweepArgs a, const __grid_constant__ CUtensorMap tm_u,
                       const __grid_constant__ CUtensorMap tm_g,
@@ -849,8 +1027,11 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     constexpr bool kWarpStore = (L >= 4);
     extern __shared__ unsigned char smem_raw[];
     char* base = smem_base(smem_raw);
+    // CLU: rows split over the cluster -- CTA q stages / moves only its part
+    const int cl_ = CLU ? a.co.cl : 1;
     const int pitch = a.co.pitch;
-    const int rb = row_bytes_al(pitch);
+    const int spitch = pitch / cl_;
+    const int rb = row_bytes_al(spitch);
     const int nob = a.n_out;
     char* bufS = base;
     char* bufO0 = base + rb;
@@ -862,13 +1043,17 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     double* ends = reinterpret_cast<double*>(tl + sizeof(Tabs) + sizeof(Slots));
     uint64_t* barS = &sl.bar[0];
     uint64_t* barA = &sl.bar[1];
-    const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
-    const int R = pitch >> 4;
+    const uint32_t bytes = static_cast<uint32_t>(spitch * 8);
+    const int R = pitch >> 4, RS = spitch >> 4;
 
-    Lane<L, NTMAX / 32> ln;
+    Lane<L, NTMAX / 32, CLU> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
-    tabs_init(tb, sl, a.co);
+    tabs_init(tb, sl, a.co, ln.q);
+    const int qoff = ln.q * RS;  // the part's first row of the [.., 16] view
+    // job distribution over clusters (CLU) or CTAs
+    const int cid = CLU ? static_cast<int>(blockIdx.x) / cl_ : static_cast<int>(blockIdx.x);
+    const int ncid = CLU ? static_cast<int>(gridDim.x) / cl_ : static_cast<int>(gridDim.x);
     if (t == 0) {
         mbar_init(barS, 1);
         mbar_init(barA, 1);
@@ -876,12 +1061,13 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         prefetch_tmap(&tm_u);
     }
     __syncthreads();
+    if constexpr (CLU) cg::this_cluster().sync();  // every part of the row running before DSMEM use
     uint32_t phS = 0, phA = 0;
     int ob = 0;
 
     const long long Nj = a.j1 - a.j0;
-    const int jb = a.j0 + static_cast<int>(Nj * blockIdx.x / gridDim.x);
-    const int je = a.j0 + static_cast<int>(Nj * (blockIdx.x + 1) / gridDim.x);
+    const int jb = a.j0 + static_cast<int>(Nj * cid / ncid);
+    const int je = a.j0 + static_cast<int>(Nj * (cid + 1) / ncid);
     const int m = a.m, last = a.np - 1;
     // C-point-only u (u_div = m, F sweeps only): seed / tail rows J, J + 1
     const bool cpu = a.u_div > 1;
@@ -907,14 +1093,15 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         fence_proxy_async();
         if constexpr (kWarpStore) {
             __syncwarp();
-            if (ln.lane == 0 && ln.warp * 32 * L < pitch) {
-                tma_store_3d(mapw, 0, ln.warp * 2 * L, row, o + ln.warp * 256 * L);
+            const int gw = ln.q * ln.nw + ln.warp;  // warp of the row (cluster rows: CTA q's part)
+            if (ln.lane == 0 && gw * 32 * L < pitch) {
+                tma_store_3d(mapw, 0, gw * 2 * L, row, o + ln.warp * 256 * L);
                 bulk_commit();
             }
         } else {
             __syncthreads();
             if (t == 0) {
-                tma_store_row(map, 0, row * R, o, R);
+                tma_store_row(map, 0, row * R + qoff, o, RS);
                 bulk_commit();
             }
         }
@@ -962,7 +1149,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (!seed_ready) {
             if (t == 0) {
                 mbar_expect_tx(barS, bytes);
-                tma_load_row(bufS, &tm_u, 0, ((cpu ? J : start) - ub) * R, barS, R);
+                tma_load_row(bufS, &tm_u, 0, ((cpu ? J : start) - ub) * R + qoff, barS, RS);
             }
             mbar_wait(barS, phS);
             phS ^= 1;
@@ -973,7 +1160,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         seed_ready = false;
         if (tail_i >= 0 && t == 0) {
             mbar_expect_tx(barS, bytes);
-            tma_load_row(bufS, &tm_u, 0, ((cpu ? J + 1 : tail_i) - ub) * R, barS, R);
+            tma_load_row(bufS, &tm_u, 0, ((cpu ? J + 1 : tail_i) - ub) * R + qoff, barS, RS);
         }
 
         // ---- chain steps u_i = Phi_i(u_{i-1}) (+ g_i)
@@ -992,7 +1179,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         } else for (int i = start + 1; i <= end; ++i) {
             if (a.add_g && t == 0) {
                 mbar_expect_tx(barA, bytes);
-                tma_load_row(bufA, &tm_g, 0, (i - a.g_base) * R, barA, R);
+                tma_load_row(bufA, &tm_g, 0, (i - a.g_base) * R + qoff, barA, RS);
             }
             release_staging();
             phi_p<P, L>(x, a.co, ln, tb, sl, ends, i, a.forced);
@@ -1014,7 +1201,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (tail_i >= 0) {
             if (a.add_g && t == 0) {
                 mbar_expect_tx(barA, bytes);
-                tma_load_row(bufA, &tm_g, 0, (tail_i - a.g_base) * R, barA, R);
+                tma_load_row(bufA, &tm_g, 0, (tail_i - a.g_base) * R + qoff, barA, RS);
             }
             release_staging();
             if (plain) tri_solve<L>(x, a.co, ln, tb, sl);
@@ -1038,6 +1225,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         }
     }
     if (kWarpStore ? (ln.lane == 0) : (t == 0)) bulk_wait<0>();
+    if constexpr (CLU) cg::this_cluster().sync();  // peers may still write our smem (DSMEM)
 }
 
 // --------------------------------------------------------------------------
@@ -1048,15 +1236,18 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 // fetched into S ahead of its emit, updated in place and stored back.
 // smem: [A0][A1][S][Tabs][Slots]
 
-template <int L, int NTMAX, int MINB, int P>
+template <int L, int NTMAX, int MINB, int P, bool CLU = false>
 __global__ void __launch_bounds__(NTMAX, MINB)
     heat_window_linear_kernel(const __grid_constant__ WindowArgs a,
                               const __grid_constant__ CUtensorMap tm_r,
                               const __grid_constant__ CUtensorMap tm_fine) {
     extern __shared__ unsigned char smem_raw[];
     char* base = smem_base(smem_raw);
+    // CLU: rows split over the cluster -- CTA q stages / moves only its part
+    const int cl_ = CLU ? a.co.cl : 1;
     const int pitch = a.co.pitch;
-    const int rb = row_bytes_al(pitch);
+    const int spitch = pitch / cl_;
+    const int rb = row_bytes_al(spitch);
     // r-row stream depth: 2 buffers, or 1 for L = 32 (three 128-thread CTAs
     // per SM need <= 75 KB each; every consume is followed by a Phi that
     // hides the next load except at window starts)
@@ -1075,13 +1266,17 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     uint64_t* barA0 = &sl.bar[0];
     uint64_t* barA1 = &sl.bar[1];
     uint64_t* barS = &sl.bar[2];  // S_b uses sl.bar[2 + b] (Slots.bar has 5)
-    const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
-    const int R = pitch >> 4;
+    const uint32_t bytes = static_cast<uint32_t>(spitch * 8);
+    const int R = pitch >> 4, RS = spitch >> 4;
 
-    Lane<L, NTMAX / 32> ln;
+    Lane<L, NTMAX / 32, CLU> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
-    tabs_init(tb, sl, a.co);
+    tabs_init(tb, sl, a.co, ln.q);
+    const int qoff = ln.q * RS;  // the part's first row of the [.., 16] view
+    // job distribution over clusters (CLU) or CTAs
+    const int cid = CLU ? static_cast<int>(blockIdx.x) / cl_ : static_cast<int>(blockIdx.x);
+    const int ncid = CLU ? static_cast<int>(gridDim.x) / cl_ : static_cast<int>(gridDim.x);
     if (t == 0) {
         mbar_init(barA0, 1);
         mbar_init(barA1, 1);
@@ -1089,13 +1284,14 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         mbar_fence_init();
     }
     __syncthreads();
+    if constexpr (CLU) cg::this_cluster().sync();  // every part of the row running before DSMEM use
     uint32_t ph0 = 0, ph1 = 0, phS = 0;  // phS: bit b = phase of S_b
 
     const bool has_pre = a.pre_e1 >= a.pre_e0;
     const int n_ind = max(0, a.p1 - a.p0 + 1);
     const int Nj = (has_pre ? 1 : 0) + n_ind;
-    const int G = gridDim.x;
-    if (static_cast<int>(blockIdx.x) >= Nj) return;
+    const int G = ncid;
+    if (cid >= Nj) return;  // (a cluster's CTAs share cid: they leave together)
 
     auto job_range = [&](int q, int& lo, int& e0, int& e1) {
         if (has_pre && q == 0) {
@@ -1109,14 +1305,14 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         }
     };
     // issue stream (thread 0): (iq, is_) = next r row to load
-    int iq = blockIdx.x, is_ = 0, ilo = 0, ie0 = 0, ie1 = -1;
+    int iq = cid, is_ = 0, ilo = 0, ie0 = 0, ie1 = -1;
     job_range(iq, ilo, ie0, ie1);
     is_ = ilo;
     auto issue_next = [&](int buf) {
         if (iq >= Nj) return;
         uint64_t* bar = buf ? barA1 : barA0;
         mbar_expect_tx(bar, bytes);
-        tma_load_row(buf ? bufA1 : bufA0, &tm_r, 0, (is_ - a.x1_base) * R, bar, R);
+        tma_load_row(buf ? bufA1 : bufA0, &tm_r, 0, (is_ - a.x1_base) * R + qoff, bar, RS);
         if (++is_ > ie1) {
             iq += G;
             if (iq < Nj) {
@@ -1149,7 +1345,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (NB == 2) cb ^= 1;
     };
 
-    for (int q = blockIdx.x; q < Nj; q += G) {
+    for (int q = cid; q < Nj; q += G) {
         int lo, e0, e1;
         job_range(q, lo, e0, e1);
         consume(false);  // e = r_lo
@@ -1158,8 +1354,8 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             bulk_wait_read<0>();  // S free again
             for (int b = 0; b < (NS == 1 ? 1 : NS - 1) && f0 + b <= e1; ++b) {
                 mbar_expect_tx(barS + b, bytes);
-                tma_load_row(bufS + b * rb, &tm_fine, 0, ((f0 + b) * a.out_stride - a.out_base) * R,
-                            barS + b, R);
+                tma_load_row(bufS + b * rb, &tm_fine, 0, ((f0 + b) * a.out_stride - a.out_base) * R + qoff,
+                            barS + b, RS);
             }
         }
         for (int s = lo; s <= e1; ++s) {
@@ -1182,14 +1378,14 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                 fence_proxy_async();
                 __syncthreads();
                 if (t == 0) {
-                    tma_store_row(&tm_fine, 0, (s * a.out_stride - a.out_base) * R, bs, R);
+                    tma_store_row(&tm_fine, 0, (s * a.out_stride - a.out_base) * R + qoff, bs, RS);
                     bulk_commit();
                     if (NS == 1) {
                         if (s + 1 <= e1) {
                             bulk_wait_read<0>();
                             mbar_expect_tx(barS, bytes);
-                            tma_load_row(bufS, &tm_fine, 0, ((s + 1) * a.out_stride - a.out_base) * R,
-                                        barS, R);
+                            tma_load_row(bufS, &tm_fine, 0, ((s + 1) * a.out_stride - a.out_base) * R + qoff,
+                                        barS, RS);
                         }
                     } else if (s + NS - 1 <= e1) {
                         // row s + NS - 1 goes to the buffer of emit s - 1 (for
@@ -1199,13 +1395,14 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                         bulk_wait_read<1>();
                         mbar_expect_tx(barS + nb, bytes);
                         tma_load_row(bufS + nb * rb, &tm_fine, 0,
-                                    ((s + NS - 1) * a.out_stride - a.out_base) * R, barS + nb, R);
+                                    ((s + NS - 1) * a.out_stride - a.out_base) * R + qoff, barS + nb, RS);
                     }
                 }
             }
         }
     }
     if (t == 0) bulk_wait<0>();
+    if constexpr (CLU) cg::this_cluster().sync();  // peers may still write our smem (DSMEM)
 }
 
 // --------------------------------------------------------------------------
@@ -1214,7 +1411,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
 // given rows, forcing, Psi(v_{j-1})) and the FAS coarse right-hand side
 // (solver.cpp:214-218).  smem: [O0][O1][A1][A2][A3][Tabs][Slots]
 
-template <int L, int NTMAX, int MINB, int P>
+template <int L, int NTMAX, int MINB, int P, bool CLU = false>
 __global__ void __launch_bounds__(NTMAX, MINB)
     heat_window_kernel(const __grid_constant__ WindowArgs a,
                        const __grid_constant__ CUtensorMap tm_x1,
@@ -1223,8 +1420,11 @@ __global__ void __launch_bounds__(NTMAX, MINB)
                        const __grid_constant__ CUtensorMap tm_out) {
     extern __shared__ unsigned char smem_raw[];
     char* base = smem_base(smem_raw);
+    // CLU: rows split over the cluster -- CTA q stages / moves only its part
+    const int cl_ = CLU ? a.co.cl : 1;
     const int pitch = a.co.pitch;
-    const int rb = row_bytes_al(pitch);
+    const int spitch = pitch / cl_;
+    const int rb = row_bytes_al(spitch);
     char* bufO0 = base;
     char* bufO1 = base + rb;
     char* bufA1 = base + 2 * rb;
@@ -1236,18 +1436,23 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     Slots& sl = *reinterpret_cast<Slots*>(tl + sizeof(Tabs));
     double* ends = reinterpret_cast<double*>(tl + sizeof(Tabs) + sizeof(Slots));
     uint64_t* barA = &sl.bar[1];
-    const uint32_t bytes = static_cast<uint32_t>(pitch * 8);
-    const int R = pitch >> 4;
+    const uint32_t bytes = static_cast<uint32_t>(spitch * 8);
+    const int R = pitch >> 4, RS = spitch >> 4;
 
-    Lane<L, NTMAX / 32> ln;
+    Lane<L, NTMAX / 32, CLU> ln;
     lane_init<L>(ln, a.co);
     const int t = ln.t;
-    tabs_init(tb, sl, a.co);
+    tabs_init(tb, sl, a.co, ln.q);
+    const int qoff = ln.q * RS;  // the part's first row of the [.., 16] view
+    // job distribution over clusters (CLU) or CTAs
+    const int cid = CLU ? static_cast<int>(blockIdx.x) / cl_ : static_cast<int>(blockIdx.x);
+    const int ncid = CLU ? static_cast<int>(gridDim.x) / cl_ : static_cast<int>(gridDim.x);
     if (t == 0) {
         mbar_init(barA, 1);
         mbar_fence_init();
     }
     __syncthreads();
+    if constexpr (CLU) cg::this_cluster().sync();  // every part of the row running before DSMEM use
     uint32_t phA = 0;
     int ob = 0;
 
@@ -1265,13 +1470,13 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         fence_proxy_async();
         __syncthreads();
         if (t == 0) {
-            tma_store_row(&tm_out, 0, (row - a.out_base) * R, o, R);
+            tma_store_row(&tm_out, 0, (row - a.out_base) * R + qoff, o, RS);
             bulk_commit();
         }
         ob ^= 1;
     };
 
-    for (int q = blockIdx.x; q < Nj; q += gridDim.x) {
+    for (int q = cid; q < Nj; q += ncid) {
         if (a.kind == WK_APPLY || a.kind == WK_FAS_RHS) {
             const int p = a.p0 + q;
             const int src = (a.kind == WK_FAS_RHS) ? p - 1 : p + a.seed_off;
@@ -1279,10 +1484,10 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             const uint32_t extra = (a.kind == WK_FAS_RHS) ? 2 * bytes : 0u;
             if (t == 0 && nb + extra) {
                 mbar_expect_tx(barA, nb + extra);
-                if (!a.seed_zero) tma_load_row(bufA1, &tm_x1, 0, (src - a.x1_base) * R, barA, R);
+                if (!a.seed_zero) tma_load_row(bufA1, &tm_x1, 0, (src - a.x1_base) * R + qoff, barA, RS);
                 if (a.kind == WK_FAS_RHS) {
-                    tma_load_row(bufA2, &tm_x2, 0, (p - a.x2_base) * R, barA, R);
-                    tma_load_row(bufA3, &tm_x3, 0, (p - a.x3_base) * R, barA, R);
+                    tma_load_row(bufA2, &tm_x2, 0, (p - a.x2_base) * R + qoff, barA, RS);
+                    tma_load_row(bufA3, &tm_x3, 0, (p - a.x3_base) * R + qoff, barA, RS);
                 }
             }
             if (nb + extra) {
@@ -1325,8 +1530,8 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         const bool fas = (a.kind == WK_FAS);
         if (t == 0) {
             mbar_expect_tx(barA, fas ? 2 * bytes : bytes);
-            tma_load_row(bufA1, &tm_x1, 0, (lo - a.x1_base) * R, barA, R);
-            if (fas) tma_load_row(bufA2, &tm_x2, 0, (lo - a.x2_base) * R, barA, R);
+            tma_load_row(bufA1, &tm_x1, 0, (lo - a.x1_base) * R + qoff, barA, RS);
+            if (fas) tma_load_row(bufA2, &tm_x2, 0, (lo - a.x2_base) * R + qoff, barA, RS);
         }
         mbar_wait(barA, phA);
         phA ^= 1;
@@ -1342,9 +1547,9 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         for (int s = lo + 1; s <= e1; ++s) {
             if (t == 0 && fas) {
                 mbar_expect_tx(barA, 3 * bytes);
-                tma_load_row(bufA1, &tm_x1, 0, (s - a.x1_base) * R, barA, R);
-                tma_load_row(bufA2, &tm_x2, 0, (s - a.x2_base) * R, barA, R);
-                tma_load_row(bufA3, &tm_x3, 0, (s - a.x3_base) * R, barA, R);
+                tma_load_row(bufA1, &tm_x1, 0, (s - a.x1_base) * R + qoff, barA, RS);
+                tma_load_row(bufA2, &tm_x2, 0, (s - a.x2_base) * R + qoff, barA, RS);
+                tma_load_row(bufA3, &tm_x3, 0, (s - a.x3_base) * R + qoff, barA, RS);
             }
             if (t == 0) bulk_wait_read<1>();
             phi_p<P, L>(x, a.co, ln, tb, sl, ends, s, a.forced);
@@ -1362,6 +1567,7 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         }
     }
     if (t == 0) bulk_wait<0>();
+    if constexpr (CLU) cg::this_cluster().sync();  // peers may still write our smem (DSMEM)
 }
 
 // --------------------------------------------------------------------------
@@ -1372,9 +1578,12 @@ static size_t ends_bytes(const HeatCoefDev& co) {
     return co.prob == 1 ? sizeof(double) * 4 * static_cast<size_t>(co.nt) : 0;
 }
 
+// staged part of a row per CTA (cluster rows: 1 / cl of it)
+static int staged_pitch(const HeatCoefDev& co) { return co.cl > 1 ? co.pitch / co.cl : co.pitch; }
+
 size_t heat_sweep_smem(const SweepArgs& a) {
     const int rows = 1 + a.n_out + (a.add_g ? 1 : 0);
-    return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) +
+    return 1024 + static_cast<size_t>(rows) * row_bytes_al(staged_pitch(a.co)) + sizeof(Tabs) +
            sizeof(Slots) + ends_bytes(a.co);
 }
 
@@ -1382,7 +1591,7 @@ size_t heat_window_smem(const WindowArgs& a) {
     int rows;
     if (a.kind == WK_LINEAR) rows = (a.co.L == 32 ? 2 : 3) + (a.two_s ? 2 : 0);
     else rows = (a.kind == WK_FAS || a.kind == WK_FAS_RHS) ? 5 : 3;
-    return 1024 + static_cast<size_t>(rows) * row_bytes_al(a.co.pitch) + sizeof(Tabs) +
+    return 1024 + static_cast<size_t>(rows) * row_bytes_al(staged_pitch(a.co)) + sizeof(Tabs) +
            sizeof(Slots) + ends_bytes(a.co);
 }
 
@@ -1394,11 +1603,11 @@ struct KernelPtrs {
     const void* win;
 };
 
-template <int L, int NT, int MB>
+template <int L, int NT, int MB, bool CLU = false>
 KernelPtrs kptrs() {
-    return {reinterpret_cast<const void*>(heat_sweep_kernel<L, NT, MB, 0>),
-            reinterpret_cast<const void*>(heat_window_linear_kernel<L, NT, MB, 0>),
-            reinterpret_cast<const void*>(heat_window_kernel<L, NT, MB, 0>)};
+    return {reinterpret_cast<const void*>(heat_sweep_kernel<L, NT, MB, 0, CLU>),
+            reinterpret_cast<const void*>(heat_window_linear_kernel<L, NT, MB, 0, CLU>),
+            reinterpret_cast<const void*>(heat_window_kernel<L, NT, MB, 0, CLU>)};
 }
 
 // heat: L=16 serves 2048 < n <= 4096 with 256 threads; smaller L use up to
@@ -1407,6 +1616,8 @@ KernelPtrs select(const HeatCoefDev& co) {
     if (co.prob == 1)
         return {reinterpret_cast<const void*>(heat_sweep_kernel<8, 512, 1, 1>), nullptr,
                 reinterpret_cast<const void*>(heat_window_kernel<8, 512, 1, 1>)};
+    // rows split over a cluster (n > 5376): every CTA a 4096-element part
+    if (co.cl > 1) return kptrs<32, 128, 3, true>();
     // 4096 < n <= 5376: L = 32 with 256 threads (sweeps), L = 16 with up to
     // 512 (the coarsest level's windows)
     switch (co.L) {
@@ -1443,19 +1654,72 @@ int occupancy(const void* fn, int nt, size_t smem) {
     return n;
 }
 
-int launch(const void* fn, int grid, int nt, size_t smem, cudaStream_t s, void** args) {
+// cluster rows: clusters of cl CTAs that can be resident at once
+int max_clusters(const void* fn, int nt, size_t smem, int cl) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
     prepare(fn);
-    return static_cast<int>(cudaLaunchKernel(fn, dim3(grid), dim3(nt), args, smem, s));
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(fn, nt, smem, cl);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaLaunchConfig_t cfg{};
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cfg.gridDim = dim3(cl * sms);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = 1;
+    }
+    cache[key] = n;
+    return n;
+}
+
+// grid: CTAs, or for cluster rows (cl > 1) clusters, capped at what fits
+int launch(const void* fn, int grid, int nt, size_t smem, cudaStream_t s, void** args, int cl = 1) {
+    prepare(fn);
+    if (cl <= 1) return static_cast<int>(cudaLaunchKernel(fn, dim3(grid), dim3(nt), args, smem, s));
+    const int ncl = std::min(grid, max_clusters(fn, nt, smem, cl));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ncl * cl);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return static_cast<int>(cudaLaunchKernelExC(&cfg, fn, args));
 }
 
 }  // namespace
 
+// CTAs per SM, or for cluster rows the clusters per SM rounded up (the
+// launch caps the grid at the resident clusters)
 int heat_sweep_occupancy(const SweepArgs& a) {
-    return occupancy(select(a.co).sweep, a.co.nt, heat_sweep_smem(a));
+    const void* fn = select(a.co).sweep;
+    if (a.co.cl > 1) return 1;
+    return occupancy(fn, a.co.nt, heat_sweep_smem(a));
 }
 
 int heat_window_occupancy(const WindowArgs& a) {
     const KernelPtrs k = select(a.co);
+    if (a.co.cl > 1) return 1;
     return occupancy(a.kind == WK_LINEAR ? k.wlin : k.win, a.co.nt, heat_window_smem(a));
 }
 
@@ -1466,7 +1730,7 @@ int launch_heat_sweep(const SweepArgs& a, const CUtensorMap& u, const CUtensorMa
     SweepArgs aa = a;
     CUtensorMap tu = u, tg = g, to = o, tuw = uw, tow = ow;
     void* args[] = {&aa, &tu, &tg, &to, &tuw, &tow};
-    return launch(select(a.co).sweep, grid, a.co.nt, heat_sweep_smem(a), s, args);
+    return launch(select(a.co).sweep, grid, a.co.nt, heat_sweep_smem(a), s, args, a.co.cl);
 }
 
 int launch_heat_window(const WindowArgs& a, const CUtensorMap& x1, const CUtensorMap& x2,
@@ -1478,10 +1742,10 @@ int launch_heat_window(const WindowArgs& a, const CUtensorMap& x1, const CUtenso
     if (a.kind == WK_LINEAR && !k.wlin) return static_cast<int>(cudaErrorInvalidValue);
     if (a.kind == WK_LINEAR) {
         void* args[] = {&aa, &t1, &to};
-        return launch(k.wlin, grid, a.co.nt, heat_window_smem(a), s, args);
+        return launch(k.wlin, grid, a.co.nt, heat_window_smem(a), s, args, a.co.cl);
     }
     void* args[] = {&aa, &t1, &t2, &t3, &to};
-    return launch(k.win, grid, a.co.nt, heat_window_smem(a), s, args);
+    return launch(k.win, grid, a.co.nt, heat_window_smem(a), s, args, a.co.cl);
 }
 
 }  // namespace atm

@@ -72,7 +72,7 @@ def _check_phi(drv, orc, hier, n, level, first, xs, substeps):
         assert rel_l2(got[j], ref) <= max(1e-11, 1.01 * (e_dev + e_ref))
 
 
-@pytest.mark.parametrize("n", [1, 2, 17, 63, 64, 65, 257, 1025, 2049, 4095, 4096, 4097, 5000, 5375, 5376])
+@pytest.mark.parametrize("n", [1, 2, 17, 63, 64, 65, 257, 1025, 2049, 4095, 4096, 4097, 5000, 5375, 5376, 5377, 8191, 12289, 16384])
 @pytest.mark.parametrize("level", [0, 1])
 def test_phi_matches_oracle(n, level):
     args = _heat_case(n, substeps=3)
@@ -354,12 +354,14 @@ def test_two_level_solve_across_chunk_lengths(n):
     assert rel_l2(res.state, orc.array(0)) <= SOLVE_RTOL
 
 
-@pytest.mark.parametrize("n", [4097, 5000, 5376])
+@pytest.mark.parametrize("n", [4097, 5000, 5376, 5377, 8192, 12289, 32768])
 def test_two_level_and_fas_solves_past_4096_unknowns(n):
     # 4096 < n <= 5376: rows padded to a multiple of 256 and moved as two
     # half-row TMA boxes; sweeps run L = 32 with 256 threads, the coarsest
-    # level's windows L = 16 with up to 512 (dt/h^2 ~ 1000, as the other
-    # final-state parity cases)
+    # level's windows L = 16 with up to 512.  n > 5376: rows split over a
+    # cluster of ceil(n / 4096) CTAs coupled by a block Woodbury correction
+    # (heat_cluster_host).  dt/h^2 ~ 1000, as the other final-state parity
+    # cases
     tf = 1000.0 * 256 / (n + 1) ** 2
     for args in (dict(problem="heat1d", n=n, tf=tf, n_points=257, m=8, k=4, manufactured=1,
                       guess="random", seed=13, max_iters=60, tol=1e-9),
