@@ -18,7 +18,7 @@ namespace atm {
 constexpr int kMaxThreads = 512;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr int kMaxL = 32;
-constexpr int kMaxCluster = 8;  // CTAs per cluster row (heat1d n <= 8 x 4096)
+constexpr int kMaxCluster = 16;  // CTAs per cluster row (heat1d n <= 16 x 4096; past 8: non-portable clusters)
 constexpr int kScanPerThread = 18;  // Mf[5], Pf_ex, Mb[5], Pb_ex, SB, q0, cfw, cbw, pad, cbwr
 
 // Device view of one level's Phi coefficients.

@@ -72,7 +72,7 @@ def _check_phi(drv, orc, hier, n, level, first, xs, substeps):
         assert rel_l2(got[j], ref) <= max(1e-11, 1.01 * (e_dev + e_ref))
 
 
-@pytest.mark.parametrize("n", [1, 2, 17, 63, 64, 65, 257, 1025, 2049, 4095, 4096, 4097, 5000, 5375, 5376, 5377, 8191, 12289, 16384])
+@pytest.mark.parametrize("n", [1, 2, 17, 63, 64, 65, 257, 1025, 2049, 4095, 4096, 4097, 5000, 5375, 5376, 5377, 8191, 12289, 16384, 40001])
 @pytest.mark.parametrize("level", [0, 1])
 def test_phi_matches_oracle(n, level):
     args = _heat_case(n, substeps=3)
@@ -354,7 +354,7 @@ def test_two_level_solve_across_chunk_lengths(n):
     assert rel_l2(res.state, orc.array(0)) <= SOLVE_RTOL
 
 
-@pytest.mark.parametrize("n", [4097, 5000, 5376, 5377, 8192, 12289, 32768])
+@pytest.mark.parametrize("n", [4097, 5000, 5376, 5377, 8192, 12289, 32768, 65536])
 def test_two_level_and_fas_solves_past_4096_unknowns(n):
     # 4096 < n <= 5376: rows padded to a multiple of 256 and moved as two
     # half-row TMA boxes; sweeps run L = 32 with 256 threads, the coarsest

@@ -60,10 +60,10 @@ def test_config_errors_before_any_device_work():
         T.TimeGrid.make(0.0, 1.0, 1)
     with pytest.raises(T.ConfigError):
         T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, 3), [4], 2)
-    # heat1d rows: one CTA up to 5376 unknowns, a cluster of up to 8 past that
+    # heat1d rows: one CTA up to 5376 unknowns, a cluster of up to 16 past that
     hier = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, 33), [4], 3)
-    with pytest.raises(T.ConfigError, match="32768"):
-        T.CycleDriver(T.Heat1D(32769, manufactured_forcing=False), hier, T.SolverConfig())
+    with pytest.raises(T.ConfigError, match="65536"):
+        T.CycleDriver(T.Heat1D(65537, manufactured_forcing=False), hier, T.SolverConfig())
 
 
 # ---------------------------------------------------------------- grids
