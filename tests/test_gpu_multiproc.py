@@ -30,7 +30,9 @@ def _mock_lib():
 
 
 @pytest.mark.parametrize("case,world", [("two_level", 2), ("two_level", 3), ("fas_vcycle", 2),
-                                        ("nested_fcf", 3), ("global_coarse", 2)])
+                                        ("nested_fcf", 3), ("global_coarse", 2), ("heat2d_strip", 2),
+                                        ("heat2d_group", 2), ("allen_cahn", 2),
+                                        ("heat1d_cluster_rows", 2), ("gray_scott", 2)])
 def test_multiprocess_solve_bitwise_equals_single_process(case, world):
     lib = _mock_lib()
     app, hier, cfg = build_case(case)
