@@ -467,3 +467,35 @@ def test_config5_shape_large_front_bound_and_sequential_state(m, k):
         err = np.linalg.norm(drv.get_level(0, first=p, count=1)[0] - ref[p]) / u0
         assert err < 1e-11, (p, err)
     drv.close()
+
+
+@pytest.mark.parametrize("variant", ["fcf", "nested_fcf_substeps", "global_coarse", "shards",
+                                     "reuse_cpoints"])
+def test_cluster_rows_across_cycle_variants(variant):
+    # rows split over a 2-CTA cluster (n = 6001) through every sweep / window
+    # job kind: FCF (C-relaxation, stored C rows), nested FCF with coarse
+    # sub-steps (forward windows, FAS right-hand sides), the global coarse
+    # chain (k >= N_T + 1), three time shards, relax reuse + C-point storage
+    n = 6001
+    tf = 1000.0 * 64 / (n + 1) ** 2
+    base = dict(problem="heat1d", n=n, tf=tf, n_points=129, m=8, k=4, manufactured=1,
+                guess="random", seed=11, max_iters=60, tol=1e-9)
+    kw = {}
+    if variant == "fcf":
+        args = dict(base, relax="FCF")
+    elif variant == "nested_fcf_substeps":
+        args = dict(base, folded=1, mode="nested-v", relax="FCF", m="4,4", k=3, substeps=2)
+    elif variant == "global_coarse":
+        args = dict(base, folded=1, mode="nested-v", m="8", k=40)
+    elif variant == "shards":
+        args = dict(base, mode="v-cycle", folded=1, m="4,4", k=3)
+        kw = dict(workers=3)
+    else:
+        args = dict(base, manufactured=0)
+        kw = dict(reuse_relax=True, cpoint_storage=True)
+    app, hier, cfg = device_objects(args)
+    res = T.solve(app, hier, cfg, **kw)
+    orc = oracle_driver(args)
+    ref = orc.drive()
+    assert res.report.iterations == ref["iterations"], (variant, res.report.iterations, ref["iterations"])
+    assert rel_l2(res.state, orc.array(0)) <= SOLVE_RTOL
