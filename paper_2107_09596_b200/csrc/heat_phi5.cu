@@ -1659,11 +1659,12 @@ int max_clusters(const void* fn, int nt, size_t smem, int cl) {
     static std::mutex mu;
     static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
     prepare(fn);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     std::lock_guard<std::mutex> lk(mu);
     auto key = std::make_tuple(fn, nt, smem, cl);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
+    // clusters of 9-16 CTAs are non-portable (opt-in)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg{};
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
