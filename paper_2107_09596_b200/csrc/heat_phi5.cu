@@ -796,15 +796,40 @@ __device__ __forceinline__ void phi(double (&x)[L], const HeatCoefDev& co, Lane<
 // rho <= max(s, 3 dt umax^2 - s) / (1 - dt + s), iterated to rho^K <= eta.
 // Chunk ends travel through smem (one barrier per residual); the residual
 // norm and max u^2 ride on a second barrier.
-template <int L, int NW, bool CL>
+template <int L, int NW, bool CL, bool PART>
 __device__ __forceinline__ void ac_residual(const double (&u)[L], const double (&up)[L],
                                             double (&F)[L], const HeatCoefDev& co,
                                             const Lane<L, NW, CL>& ln, double* ends, double& sq,
                                             double& u2) {
     const int nt = blockDim.x;
+    const bool last = ln.t == co.tl;
+    const double dt = co.ac_dt, c = co.ac_c;
+    sq = 0.0;
+    u2 = 0.0;
+    if constexpr (!PART) {
+        // n a multiple of L: every real chunk is full (the instantiation for
+        // every n % L == 0; PART handles the partial last chunk)
+        ends[ln.t] = u[0];
+        ends[nt + ln.t] = u[L - 1];
+        __syncthreads();
+        const bool real = ln.t <= co.tl;
+        const double ul = ends[nt + (ln.t == 0 ? co.tl : ln.t - 1)];
+        const double ur = ends[last ? 0 : ln.t + 1];
+#pragma unroll
+        for (int e = 0; e < L; ++e) {
+            const double a = e == 0 ? ul : u[e - 1];
+            const double b = e == L - 1 ? ur : u[e + 1];
+            const double ui = u[e];
+            const double lap = c * (a - 2.0 * ui + b);
+            const double f = real ? ui - dt * (lap + ui - ui * ui * ui) - up[e] : 0.0;
+            F[e] = f;
+            sq = fma(f, f, sq);
+            u2 = fmax(u2, ui * ui);
+        }
+        return;
+    } else {
     // thread tl holds elements [tl L, tl L + pl) with element n-1 last: its
     // chunk end is u[pl - 1], whose periodic right neighbour is element 0
-    const bool last = ln.t == co.tl;
     double uend = u[L - 1];
     if (last) {
 #pragma unroll
@@ -818,9 +843,6 @@ __device__ __forceinline__ void ac_residual(const double (&u)[L], const double (
     const double ul = ends[nt + (ln.t == 0 ? co.tl : ln.t - 1)];
     const double ur = ends[last ? 0 : ln.t + 1];
     const int eend = last ? co.pl - 1 : L - 1;  // the chunk's last real element
-    const double dt = co.ac_dt, c = co.ac_c;
-    sq = 0.0;
-    u2 = 0.0;
 #pragma unroll
     for (int e = 0; e < L; ++e) {
         const double a = e == 0 ? ul : u[e - 1];
@@ -831,6 +853,7 @@ __device__ __forceinline__ void ac_residual(const double (&u)[L], const double (
         F[e] = f;
         sq = fma(f, f, sq);
         u2 = fmax(u2, ui * ui);
+    }
     }
 }
 
@@ -856,7 +879,7 @@ __device__ __forceinline__ void ac_reduce(double sq, double u2, const Lane<L, NW
     res = sqrt(res);
 }
 
-template <int L, int NW, bool CL>
+template <int L, int NW, bool CL, bool PART = false>
 __device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, Lane<L, NW, CL>& ln,
                                        const Tabs& tb, Slots& sl, double* ends) {
     int rpar = 0;
@@ -865,7 +888,7 @@ __device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, La
 #pragma unroll
         for (int e = 0; e < L; ++e) up[e] = u[e];
         double sq, u2, res, umax2;
-        ac_residual<L>(u, up, F, co, ln, ends + rpar * 2 * blockDim.x, sq, u2);
+        ac_residual<L, NW, CL, PART>(u, up, F, co, ln, ends + rpar * 2 * blockDim.x, sq, u2);
         ac_reduce<L>(sq, u2, ln, sl, rpar, res, umax2);
         rpar ^= 1;
         const double stop = fmax(co.newton_tol, co.newton_tol * res);
@@ -895,7 +918,7 @@ __device__ __forceinline__ void ac_phi(double (&u)[L], const HeatCoefDev& co, La
             }
 #pragma unroll
             for (int e = 0; e < L; ++e) u[e] += d[e];
-            ac_residual<L>(u, up, F, co, ln, ends + rpar * 2 * blockDim.x, sq, u2);
+            ac_residual<L, NW, CL, PART>(u, up, F, co, ln, ends + rpar * 2 * blockDim.x, sq, u2);
             ac_reduce<L>(sq, u2, ln, sl, rpar, res, umax2);
             rpar ^= 1;
             ++it;
@@ -908,7 +931,7 @@ template <int P, int L, int NW, bool CL>
 __device__ __forceinline__ void phi_p(double (&x)[L], const HeatCoefDev& co, Lane<L, NW, CL>& ln,
                                       const Tabs& tb, Slots& sl, double* ends, int index,
                                       int forced) {
-    if constexpr (P == 1) ac_phi<L>(x, co, ln, tb, sl, ends);
+    if constexpr (P >= 1) ac_phi<L, NW, CL, P == 2>(x, co, ln, tb, sl, ends);
     else phi<L>(x, co, ln, tb, sl, index, forced);
 }
 
@@ -1613,9 +1636,14 @@ KernelPtrs kptrs() {
 // heat: L=16 serves 2048 < n <= 4096 with 256 threads; smaller L use up to
 // 512.  Allen-Cahn (Newton Phi, FAS only): L = 8, up to 512 threads.
 KernelPtrs select(const HeatCoefDev& co) {
-    if (co.prob == 1)
+    if (co.prob == 1) {
+        // P = 2: n not a multiple of L (the last real chunk is partial)
+        if (co.pl != co.L)
+            return {reinterpret_cast<const void*>(heat_sweep_kernel<8, 512, 1, 2>), nullptr,
+                    reinterpret_cast<const void*>(heat_window_kernel<8, 512, 1, 2>)};
         return {reinterpret_cast<const void*>(heat_sweep_kernel<8, 512, 1, 1>), nullptr,
                 reinterpret_cast<const void*>(heat_window_kernel<8, 512, 1, 1>)};
+    }
     // rows split over a cluster (n > 5376): every CTA a 4096-element part
     if (co.cl > 1) return kptrs<32, 128, 3, true>();
     // 4096 < n <= 5376: L = 32 with 256 threads (sweeps), L = 16 with up to
