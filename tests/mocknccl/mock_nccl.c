@@ -162,9 +162,12 @@ static ncclResult_t run_recv(op_t* o) {
     ncclResult_t r = get_file(path, h, o->bytes);
     if (r == ncclSuccess) {
         unlink(path);
-        if (cuStreamSynchronize(o->stream) != CUDA_SUCCESS) r = fail("stream sync");
-        else if (o->bytes && cuMemcpyHtoD((CUdeviceptr)o->buf, h, o->bytes) != CUDA_SUCCESS)
+        /* stream-ordered copy, complete before h is freed: a plain cuMemcpyHtoD
+         * from pageable memory may return before its DMA lands, and the
+         * engine's non-blocking stream does not order after the null stream */
+        if (o->bytes && cuMemcpyHtoDAsync((CUdeviceptr)o->buf, h, o->bytes, o->stream) != CUDA_SUCCESS)
             r = fail("HtoD");
+        else if (cuStreamSynchronize(o->stream) != CUDA_SUCCESS) r = fail("stream sync");
     }
     free(h);
     return r;
@@ -231,7 +234,8 @@ ncclResult_t ncclAllReduce(const void* sb, void* rb, size_t count, ncclDataType_
             else acc[i] += tmp[i];
         }
     }
-    if (r == ncclSuccess && bytes && cuMemcpyHtoD((CUdeviceptr)rb, acc, bytes) != CUDA_SUCCESS)
+    if (r == ncclSuccess && bytes &&
+        (cuMemcpyHtoDAsync((CUdeviceptr)rb, acc, bytes, s) != CUDA_SUCCESS || cuStreamSynchronize(s) != CUDA_SUCCESS))
         r = fail("HtoD");
     /* files of reduction seq-2 can no longer be read by anyone */
     if (seq >= 2) {
