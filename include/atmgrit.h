@@ -118,8 +118,9 @@ typedef struct atm_runtime {
     const void* nccl_id; /* 128-byte ncclUniqueId (world_size > 1)                 */
     int storage;       /* atm_storage                                              */
     int trace;         /* record per-phase cudaEvent timings                       */
-    int reuse_relax;   /* two-level F-relaxation: skip a cycle's opening F-sweep,
-                          whose results the previous correction F-sweep already
+    int reuse_relax;   /* F-relaxation (two-level cycle, and level 0 of FAS V-cycles):
+                          skip a cycle's opening level-0 F-sweep, whose results the
+                          previous cycle's level-0 correction F-sweep already
                           produced (bitwise the same cycle; opt-in)                */
     int defer_guess;   /* 1: atm_setup sends only the C rows of a provided guess;
                           its F rows are dead under cycling (every cycle rewrites

@@ -1121,11 +1121,23 @@ void Engine::sync_stream(const char* what) {
     // this stream; fail like the reference's receive timeout (transport.cpp:
     // 29-48 -> RuntimeFault) instead of hanging, after aborting the communicator
     // so the stream drains (parallel.cpp:349-351: abort wakes the other ranks)
-    const auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms_);
-    for (;;) {
+    // The common case is a wait of tens of microseconds on the critical path
+    // of every iteration (the norm read-back): spin on the stream for the
+    // first 2 ms without sleeping, and look at the clock, NCCL's error state
+    // and the deadline only every 64 polls; a long wait then backs off to
+    // 20 us sleeps.
+    const auto t_start = std::chrono::steady_clock::now();
+    const auto deadline = t_start + std::chrono::milliseconds(timeout_ms_);
+    const auto spin_until = t_start + std::chrono::milliseconds(2);
+    bool spinning = true;
+    for (unsigned poll = 1;; ++poll) {
         const cudaError_t e = cudaStreamQuery(st_);
         if (e == cudaSuccess) return;
         if (e != cudaErrorNotReady) ck(e, what);
+        if (spinning && (poll & 63u)) continue;
+        const auto now = std::chrono::steady_clock::now();
+        if (spinning && now < spin_until) continue;
+        spinning = false;
         std::string why;
         if (nccl_->GetAsyncError) {
             ncclResult_t ar = ncclSuccess;
@@ -1133,7 +1145,7 @@ void Engine::sync_stream(const char* what) {
             if (ar != ncclSuccess && ar != ncclInProgress)
                 why = std::string("NCCL asynchronous error: ") + nccl_->ErrStr(ar);
         }
-        if (why.empty() && std::chrono::steady_clock::now() > deadline)
+        if (why.empty() && now > deadline)
             why = "timed out after " + std::to_string(timeout_ms_) + " ms";
         if (!why.empty()) {
             if (nccl_->Abort) nccl_->Abort(static_cast<ncclComm_t>(comm_));
@@ -1486,7 +1498,7 @@ void Engine::correct_from(int level) {
         check_launch(launch_c_correct(F.u.p, F.u.base / F.u.div, m / F.u.div, C.u.p, C.v.p, C.u.base,
                                       pitch_, n_, F.c_first, F.c_first + F.c_count, st_), "c_correct");
     }
-    f_sweep(level, level == 0 ? TAIL_SQ : TAIL_NONE);
+    f_sweep(level, level != 0 ? TAIL_NONE : reuse_possible() ? TAIL_BOTH : TAIL_SQ);
     if (level == 0)
         for (Shard& s : sh_) point0_residual(s, 0, d_row_, d_sq_c_);
 }
@@ -1497,8 +1509,11 @@ void Engine::v_cycle(int level) {
         coarsest_fas();
         return;
     }
+    // relax reuse (level 0 only): the opening F-sweep would recompute what the
+    // previous cycle's correction sweep left, and its residuals are stored
     phase_begin("relax");
-    relax_level(level, sol_.relaxation == ATM_RELAX_F, true);
+    if (!(level == 0 && reuse_possible() && relax_valid_))
+        relax_level(level, sol_.relaxation == ATM_RELAX_F, true);
     phase_end();
     phase_begin("restrict");
     restrict_to(level);
@@ -1509,14 +1524,17 @@ void Engine::v_cycle(int level) {
     phase_end();
 }
 
-// Relax reuse (opt-in, atm_runtime.reuse_relax): with F-relaxation in the
-// two-level cycle, a cycle's opening F-sweep recomputes from the same C
-// points exactly what the previous cycle's correction F-sweep computed, and
-// its only consumed output is the restriction residual at the C points.  The
-// correction sweep then also stores those residuals (TAIL_BOTH) and the next
-// cycle skips its F-sweep -- bitwise the same cycle.
+// Relax reuse (opt-in, atm_runtime.reuse_relax): with F-relaxation, a
+// cycle's opening level-0 F-sweep recomputes from the same C points exactly
+// what the previous cycle's level-0 correction F-sweep computed, and its only
+// consumed output is the restriction residual at the C points.  The
+// correction sweep then also stores those residuals into level 1's r
+// (TAIL_BOTH; nothing reads r between the restriction and the end of the
+// cycle) and the next cycle skips its F-sweep -- bitwise the same cycle, in
+// the two-level cycle and on level 0 of the FAS V-cycle alike (the coarser
+// levels' states are re-injected every cycle, so only level 0 repeats).
 bool Engine::reuse_possible() const {
-    return rt_.reuse_relax && sol_.mode == ATM_TWO_LEVEL && sol_.relaxation == ATM_RELAX_F;
+    return rt_.reuse_relax && sol_.relaxation == ATM_RELAX_F && H_.L >= 2;
 }
 
 void Engine::two_level_cycle() {
@@ -1559,9 +1577,14 @@ void Engine::cycle() {
     }
     if (graphs) CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
     try {
-        if (sol_.mode == ATM_TWO_LEVEL) two_level_cycle();
-        else v_cycle(0);
+        if (sol_.mode == ATM_TWO_LEVEL) {
+            two_level_cycle();
+        } else {
+            v_cycle(0);
+            relax_valid_ = reuse_possible();
+        }
     } catch (...) {
+        relax_valid_ = false;
         if (graphs) {
             cudaGraph_t g = nullptr;
             cudaStreamEndCapture(st_, &g);
@@ -1591,7 +1614,12 @@ void Engine::cycle() {
         CK(cudaGraphLaunch(graph_exec_, st_));
     }
     last_launches_ = launches_;
-    check_newton();
+    try {
+        check_newton();
+    } catch (...) {
+        relax_valid_ = false;  // a failed Phi leaves no residuals worth keeping
+        throw;
+    }
 }
 
 // NonlinearSolveError (gray_scott.cpp:165-169 analogue): a Newton solve hit
@@ -1804,7 +1832,7 @@ int Engine::solve(atm_report* rep, double* norms, double* iter_secs) {
         const bool reused = reuse_possible() && it > 1;
         for (int l = 0; l + 1 < H_.L; ++l) {
             const double F = static_cast<double>(H_.np[l] - H_.n_c(l));
-            double per = reused ? F : 2.0 * F;
+            double per = (reused && l == 0) ? F : 2.0 * F;
             if (sol_.relaxation == ATM_RELAX_FCF) per += sol_.nu * (F + H_.n_c(l) - 1);
             dof_steps += per * n_;
         }

@@ -63,6 +63,73 @@ def test_cpoint_storage_with_relax_reuse():
     _same(a, b)
 
 
+FAS_REUSE_CASES = [
+    # FAS V-cycles: the level-0 opening F-sweep repeats the previous cycle's
+    # level-0 correction sweep (the coarser levels are re-injected each cycle)
+    dict(problem="heat1d", n=255, tf=1.0, n_points=1025, m="4,4", k=3, folded=1, manufactured=1,
+         mode="v-cycle", guess="random", seed=7, max_iters=60, tol=1e-10),
+    dict(problem="heat1d", n=1025, tf=1.0, n_points=2049, m="16", k=4, folded=1, manufactured=1,
+         mode="v-cycle", guess="random", seed=9, max_iters=60, tol=1e-10),
+    dict(problem="heat1d", n=255, tf=1.0, n_points=1025, m="8,4", k=2, folded=1, manufactured=1,
+         mode="nested-v", guess="random", seed=8, max_iters=60, tol=1e-10),
+    dict(problem="heat1d", n=127, tf=1.0, n_points=1025, m="4,4,4", k=2, folded=1, manufactured=0,
+         mode="v-cycle", guess="random", seed=5, substeps=2, max_iters=60, tol=1e-10),
+    dict(problem="dahlquist", tf=2.0, n_points=4097, m="4,4", k=2, folded=1, mode="v-cycle",
+         guess="random", seed=3, max_iters=60, tol=1e-12),
+]
+
+
+@pytest.mark.parametrize("args", FAS_REUSE_CASES)
+@pytest.mark.parametrize("workers", [1, 3])
+def test_relax_reuse_in_fas_vcycles_bitwise_equals_full_cycles(args, workers):
+    app, hier, cfg = device_objects(args)
+    a = T.solve(app, hier, cfg, workers=workers)
+    b = T.solve(app, hier, cfg, workers=workers, reuse_relax=True)
+    _same(a, b)
+    if a.report.iterations > 1:
+        assert b.report.dof_steps < a.report.dof_steps
+    if not int(args.get("manufactured", 0)) or int(args.get("folded", 0)):
+        _same(a, T.solve(app, hier, cfg, workers=workers, reuse_relax=True, cpoint_storage=True))
+
+
+def test_relax_reuse_fas_allen_cahn_heat2d_gray_scott():
+    ic = 0.05 * T.random_state(3, 256)
+    app = T.AllenCahn(256, 0.02, 1.0, 1e-12, 30, initial_condition=ic)
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, 513), [8, 4], 3)
+    cfg = T.SolverConfig(mode=T.CycleMode.VCycle, max_iters=40, tol=1e-9,
+                         initial_guess=T.InitialGuess.Random, seed=20)
+    a = T.solve(app, hier, cfg, workers=2)
+    _same(a, T.solve(app, hier, cfg, workers=2, reuse_relax=True))
+    _same(a, T.solve(app, hier, cfg, workers=2, reuse_relax=True, cpoint_storage=True))
+    app = T.Heat2D(31, folded=True, source=T.gaussian_source(31), cg_rtol=1e-12, cg_max=10000)
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, 1.0, 257), [8, 4], 2)
+    for mode in (T.CycleMode.VCycle, T.CycleMode.NestedV):
+        cfg = T.SolverConfig(mode=mode, max_iters=40, tol=1e-9, initial_guess=T.InitialGuess.Random, seed=20)
+        a = T.solve(app, hier, cfg)
+        _same(a, T.solve(app, hier, cfg, reuse_relax=True))
+        _same(a, T.solve(app, hier, cfg, reuse_relax=True, cpoint_storage=True))
+    app = T.GrayScott(16)
+    hier = T.build_hierarchy(T.TimeGrid.make(0.0, 8.0, 129), [8], 4)
+    cfg = T.SolverConfig(mode=T.CycleMode.NestedV, max_iters=30, tol=1e-7)
+    _same(T.solve(app, hier, cfg), T.solve(app, hier, cfg, reuse_relax=True))
+
+
+def test_relax_reuse_fas_invalidated_by_set_level():
+    args = dict(problem="heat1d", n=63, tf=1.0, n_points=257, m="4,4", k=3, folded=1, manufactured=1,
+                mode="v-cycle", guess="random", seed=4, max_iters=20, tol=1e-14)
+    app, hier, cfg = device_objects(args)
+    drv_a = T.CycleDriver(app, hier, cfg)
+    drv_b = T.CycleDriver(app, hier, cfg, reuse_relax=True)
+    for d in (drv_a, drv_b):
+        d.setup()
+        d.iterate(2)
+        u = d.get_level(0)
+        u[5:40] *= 0.5  # perturb F and C points between cycles
+        d.set_level(0, u)
+    assert np.array_equal(drv_a.iterate(3), drv_b.iterate(3))
+    assert np.array_equal(drv_a.get_level(0), drv_b.get_level(0))
+
+
 def test_cpoint_storage_provided_guess_and_partial_reads():
     args = dict(problem="heat1d", n=127, tf=1.0, n_points=801, m=8, k=3, folded=0, manufactured=0,
                 guess="provided", max_iters=4, tol=1e-300)

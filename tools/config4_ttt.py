@@ -4,7 +4,10 @@ Fourier u0, random guess (seed 20), tol 1e-10.  Level 0 uses C-point storage
 (the full level-0 array, 137 GB, does not fit one GPU with the other levels).
 One JSON line per cycle (flushed) so a cut-off run still reports progress.
 
-  python tools/config4_ttt.py out.jsonl [max_cycles]"""
+  python tools/config4_ttt.py out.jsonl [max_cycles] [reuse]
+
+`reuse` adds the relax-reuse opt-in (the level-0 opening F-sweep of every
+cycle after the first is skipped; bitwise the same cycles)."""
 import json
 import os
 import sys
@@ -16,14 +19,15 @@ import paper_2107_09596_b200 as T  # noqa: E402
 
 out = open(sys.argv[1], "w")
 max_cycles = int(sys.argv[2]) if len(sys.argv) > 2 else 80
+reuse = len(sys.argv) > 3 and sys.argv[3] == "reuse"
 app = T.Heat2D(511, folded=True, source=None, cg_rtol=1e-12, initial_condition=T.fourier_ic(511))
 hier = T.build_hierarchy(T.TimeGrid.make(0.0, 4.0, 65537), [8, 8, 8], 2)
 cfg = T.SolverConfig(mode=T.CycleMode.VCycle, relaxation=T.Relaxation.F, max_iters=max_cycles, tol=1e-10,
                      initial_guess=T.InitialGuess.Random, seed=20)
 t0 = time.perf_counter()
-drv = T.CycleDriver(app, hier, cfg, cpoint_storage=True)
+drv = T.CycleDriver(app, hier, cfg, cpoint_storage=True, reuse_relax=reuse)
 drv.setup()
-out.write(json.dumps({"setup_s": time.perf_counter() - t0}) + "\n")
+out.write(json.dumps({"setup_s": time.perf_counter() - t0, "relax_reuse": reuse}) + "\n")
 out.flush()
 for it in range(1, max_cycles + 1):
     v = float(drv.iterate(1)[0])

@@ -67,37 +67,39 @@ def configs():
     return c
 
 
-def dof_steps(hier, n, relax, nu=1):
+def dof_steps(hier, n, relax, nu=1, reuse=False):
     tot = 0.0
     for l in range(hier.n_levels() - 1):
         np_l = hier.level(l).n_points
         nc = (np_l - 1) // hier.m[l] + 1
         F = np_l - nc
-        per = 2.0 * F
+        # relax reuse: the level-0 opening F-sweep is not run
+        per = F if (reuse and l == 0 and relax == T.Relaxation.F) else 2.0 * F
         if relax == T.Relaxation.FCF:
             per += nu * (F + nc - 1)
         tot += per * n
     return tot
 
 
-def run(cfg):
+def run(cfg, reuse=False):
     app = cfg["app"]()
     t0, tf, npts, ms, k = cfg["grid"]
     hier = T.build_hierarchy(T.TimeGrid.make(t0, tf, npts), ms, k)
     sc = T.SolverConfig(mode=cfg["mode"], relaxation=cfg["relax"], max_iters=100, tol=cfg.get("tol", 1e-10),
                         initial_guess=cfg.get("guess", T.InitialGuess.Random), seed=20)
-    drv = T.CycleDriver(app, hier, sc, cpoint_storage=cfg.get("cpts", False))
+    reuse = reuse and cfg["relax"] == T.Relaxation.F
+    drv = T.CycleDriver(app, hier, sc, cpoint_storage=cfg.get("cpts", False), reuse_relax=reuse)
     w0 = time.perf_counter()
     drv.setup()
     if cfg["mode"] == T.CycleMode.NestedV:
         drv.nested_init()
-    drv.iterate(cfg.get("warm", 1))
+    drv.iterate(max(cfg.get("warm", 1), 1) if reuse else cfg.get("warm", 1))
     setup_s = time.perf_counter() - w0
     it0 = drv.inner_iterations()
     norms, ms_dev = drv.iterate_timed(cfg["iters"])
     inner = drv.inner_iterations() - it0
-    ds = dof_steps(hier, app.vector_size(), cfg["relax"]) * cfg["iters"]
-    r = dict(config=cfg["name"], n=app.vector_size(), iterations_timed=cfg["iters"],
+    ds = dof_steps(hier, app.vector_size(), cfg["relax"], reuse=reuse) * cfg["iters"]
+    r = dict(config=cfg["name"] + ("+relax_reuse" if reuse else ""), n=app.vector_size(), iterations_timed=cfg["iters"],
              ms_per_iteration=ms_dev / cfg["iters"], dof_steps_per_s=ds / (ms_dev * 1e-3),
              setup_plus_first_iteration_s=setup_s, norms=[float(v) for v in norms])
     if inner:
@@ -159,11 +161,13 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--only", default="1,2,3,4,6")
     ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--reuse", action="store_true",
+                    help="opt-in relax reuse (skip the level-0 opening F-sweep; bitwise the same cycles)")
     a = ap.parse_args()
     res = []
     cs = configs()
     for i in [int(x) for x in a.only.split(",")]:
-        r = run(cs[i])
+        r = run(cs[i], a.reuse)
         if a.cpu:
             r.update(run_cpu(i, cs[i]))
         print(json.dumps(r), flush=True)
