@@ -672,6 +672,13 @@ void Engine::build_coefs(Shard& s) {
             c.cneg_c = hh.cneg_c;
             c.sigma = hh.sigma;
             c.ncw = hh.ncw;
+            c.sb_m = hh.sb_m;
+            c.sb_af = hh.sb_af;
+            c.sb_ab = hh.sb_ab;
+            for (int e = 0; e < 8; ++e) {
+                c.sb_q[e] = hh.sb_q[e];
+                c.sb_pb[e] = hh.sb_pb[e];
+            }
             c.n = n_;
             c.pitch = pitch_;
             c.nt = hh.nt;

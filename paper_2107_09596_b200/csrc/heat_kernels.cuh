@@ -40,11 +40,21 @@ struct HeatCoefDev {
     const double* wb;      // [kMaxWarps][kMaxWarps] (backward)
     const double* wk;      // [kMaxWarps][kMaxWarps] forward-into-backward coupling weights
     const double* powc;    // [3][kMaxL] q, p_b of interior threads; q of the padded last thread
+                           // (sb_m > 0: the two q rows hold one table per sub-block)
     const double* theta;   // [np*S] forcing amplitude per (index, substep) or null
     const double* prof;    // [nt*L] forcing profile sin(pi x_i) or null
     double beta_c, gamma_c, cneg_c;  // fixed-point factors: 1/d*, r/d*, -c*
     double sigma;          // Sherman-Morrison scale
     int ncw;               // warps [0, ncw) carry the left correction vector
+    // sub-block local passes (plain heat rows, L >= 16): every chunk runs as
+    // L / sb_m independent chains of sb_m elements; sb_af = gamma^sb_m and
+    // sb_ab = (-c)^sb_m carry between the sub-blocks (heat_phi5.cu, tri_solve_sb)
+    int sb_m;
+    double sb_af, sb_ab;
+    // the interior sub-block's q and p_b, read as constant-bank operands (no
+    // shared-memory table reads in the fix-up); the thread holding element
+    // n-1 folds its shorter sub-blocks into its c_b (powc row 2: kappa_b)
+    double sb_q[8], sb_pb[8];
     int ncw_r0;            // cyclic: warps [ncw_r0, nw) carry the right one
     // cyclic (periodic) matrices: Woodbury capacitance S (2x2) and the
     // x_{n-1} pick-up of thread tl (element pl-1)
@@ -77,6 +87,8 @@ struct HeatLevelHost {
     std::vector<double> blk, cS;
     double r = 0, beta_c = 0, gamma_c = 0, cneg_c = 0, sigma = 0;
     double S[4] = {0, 0, 0, 0}, ql = 0, pbl = 0;
+    int sb_m = 0;
+    double sb_af = 0, sb_ab = 0, sb_q[8] = {0}, sb_pb[8] = {0};
     int cyclic = 0, ncw_r0 = 0, tl = 0, pl = 0;
     double fit_err = 0;  // max |w - (cfw q + cbw p_b)| / max |w| over the correction chunks
     int ncw = 0, n = 0, pitch = 0, nt = 0, L = 0, substeps = 1;

@@ -317,6 +317,40 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double r_in, double shift
         H.ql = ql;
         H.pbl = pbl;
     }
+    // Sub-block local passes (plain heat rows with L = 16; tri_solve_sb): a chunk
+    // runs as S = L / M independent chains of M elements.  sb_q = U^{-1} p_f
+    // local to a fully real sub-block and sb_pb[e] = (-c)^{M - e} go to the
+    // kernels as constant-bank operands.  A sub-block with only `real` < M
+    // leading elements inside the row has q' = q - kappa p_b on them,
+    // kappa = sum_{j >= real} (-c)^{j - M} gamma^{j + 1}: the thread holding
+    // element n-1 folds kappa_b (powc row 2) into its sub-block c_b.
+    if (!cyclic && L == 16) {
+        constexpr int M = 8;
+        const int S = L / M;
+        const LD g = static_cast<LD>(H.gamma_c), cn = static_cast<LD>(H.cneg_c);
+        LD gp[M + 1], cp[M + 1];  // powers
+        gp[0] = cp[0] = 1.0L;
+        for (int e = 1; e <= M; ++e) {
+            gp[e] = gp[e - 1] * g;
+            cp[e] = cp[e - 1] * cn;
+        }
+        H.sb_m = M;
+        H.sb_af = static_cast<double>(gp[M]);
+        H.sb_ab = static_cast<double>(cp[M]);
+        LD z = 0.0L;
+        for (int e = M - 1; e >= 0; --e) {
+            z = cn * z + gp[e + 1];
+            H.sb_q[e] = static_cast<double>(z);
+            H.sb_pb[e] = static_cast<double>(cp[M - e]);
+        }
+        const int tl = (n - 1) / L, pl = n - tl * L;  // the thread holding element n-1
+        for (int b = 0; b < S; ++b) {
+            const int real = std::max(0, std::min(M, pl - b * M));
+            LD kap = 0.0L;
+            for (int j = real; j < M; ++j) kap += gp[j + 1] / cp[M - j];
+            H.powc[2 * kMaxL + b] = static_cast<double>(kap);
+        }
+    }
     return H;
 }
 
@@ -453,6 +487,11 @@ struct Lane {
     bool corr, inside;   // carries the boundary correction; chunk inside the row
     double Mf[5], Pfex, Mb[5], Pbex, SB, q0;
     double cfw, cbw;     // correction carries of the chunk (left vector)
+    // sub-block solve, the thread holding element n-1: kappa of its last
+    // sub-block (and kappa (-c)^M) when only that one is short -- folded
+    // off the carry chain; edge_slow: some other sub-block is short too
+    double kapl, kapab;
+    bool edge_slow;
     double cbwr;         // cyclic: right correction vector's p_b coefficient
     // cluster rows (CL): rank of the CTA in the cluster (its block of the
     // row) and the block's x_{n-1} pick-up (thread tl, element pl - 1)
@@ -504,6 +543,19 @@ __device__ __forceinline__ void lane_init(Lane<L, NW, CL>& ln, const HeatCoefDev
     ln.Pbex = __ldg(sc + 11);
     ln.SB = __ldg(sc + 12);
     ln.q0 = __ldg(sc + 13);
+    ln.kapl = ln.kapab = 0.0;
+    ln.edge_slow = false;
+    if constexpr (L == 16 && !CL) {
+        if (co.sb_m > 0 && ln.pad0 > 0 && ln.pad0 < L) {
+            constexpr int S = L / 8;
+            const double* kap = co.powc + 2 * kMaxL;
+            for (int b = 0; b < S - 1; ++b) ln.edge_slow = ln.edge_slow || __ldg(kap + b) != 0.0;
+            if (!ln.edge_slow) {
+                ln.kapl = __ldg(kap + S - 1);
+                ln.kapab = ln.kapl * co.sb_ab;
+            }
+        }
+    }
     ln.cfw = ln.corr ? __ldg(sc + 14) : 0.0;
     ln.cbw = ln.corr ? __ldg(sc + 15) : 0.0;
     ln.cbwr = ln.corr ? __ldg(sc + 17) : 0.0;
@@ -597,6 +649,167 @@ __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L, NW, C
     }
 }
 
+// The blocked solve with sub-block local passes (plain heat rows with L = 16:
+// the coarsest level's windows of config 5, every level of 1024 < n <= 2048;
+// the L = 32 level-0 sweeps keep tri_solve -- see profiles/README.md, round 2).
+// Every chunk is S = L / M sub-blocks whose M-long local chains run
+// independently (4-way ILP on the FP64 pipe instead of 2 x L dependent
+// DFMAs), and the sub-block carries are folded into the fix-up the blocked
+// solve applies anyway: sub-block b gets its own pair (c_f, c_b),
+//   c_f[b+1] = Y_b + gamma^M c_f[b]            (Y_b: the sub-block's local end)
+//   c_b[b]   = z_{b+1} + c_f[b+1] q[0] + (-c)^M c_b[b+1]
+// (z_{b+1}: first local backward value of sub-block b + 1), started from the
+// thread's carries c_f[0] = c_f, c_b[S-1] = c_b.  Before the barrier the
+// same two chains with zero thread carries give the thread's forward end B
+// and first backward value zeta that the warp scans combine.  All fully real
+// sub-blocks share one q and one p_b of M entries, read as constant-bank
+// operands: the fix-up makes no shared-memory table reads (the LSU data
+// pipe was the busiest unit of the Phi-bound sweeps).  The thread holding
+// element n-1 has shorter sub-blocks: q' = q - kappa_b p_b there, folded
+// into its c_b.  The thread-level tables (scan multipliers, cross-warp
+// weights, boundary correction: a shift of the thread's two carries) are
+// those of tri_solve.
+template <int L, int NW, bool CL>
+__device__ __forceinline__ void tri_solve_sb(double (&x)[L], const HeatCoefDev& co, Lane<L, NW, CL>& ln,
+                                             const Tabs& tb, Slots& sl) {
+    constexpr int M = 8, S = L / M;
+    const double ab = co.sb_ab, q0c = co.sb_q[0];
+    // sub-block carry multipliers: gamma^M across a fully real sub-block, 0
+    // once the sub-block holds a padding element
+    double af[S];
+#pragma unroll
+    for (int b = 0; b < S; ++b) af[b] = ((b + 1) * M <= ln.pad0) ? co.sb_af : 0.0;
+    // effective right-carry coefficients ce[b] of the sub-blocks for forward
+    // carries f[b] and the thread's right carry c; returns the chunk's first
+    // backward value.  The chain ce[b] = ce[b+1] (-c)^M + T_b carries one FMA
+    // per sub-block; kappa of a short last sub-block enters T_{S-2} and
+    // ce[S-1] off the chain (kapl = 0 on every other thread).
+    auto back_carries = [&](const double (&f)[S], double c, double (&ce)[S]) {
+        double T[S];
+#pragma unroll
+        for (int b = 0; b < S - 1; ++b) T[b] = fma(f[b + 1], q0c, x[(b + 1) * M]);
+        T[S - 2] = fma(-ln.kapab, f[S - 1], T[S - 2]);
+        ce[S - 1] = fma(-ln.kapl, f[S - 1], c);
+        ce[S - 2] = fma(c, ab, T[S - 2]);
+#pragma unroll
+        for (int b = S - 3; b >= 0; --b) ce[b] = fma(ce[b + 1], ab, T[b]);
+        if (ln.edge_slow) {  // a short sub-block before the last one (n % L <= L - M)
+            const double* kap = tb.powc + 2 * kMaxL;
+            ce[S - 1] = fma(-kap[S - 1], f[S - 1], c);
+#pragma unroll
+            for (int b = S - 2; b >= 0; --b)
+                ce[b] = fma(-kap[b], f[b], fma(ce[b + 1], ab, fma(f[b + 1], q0c, x[(b + 1) * M])));
+        }
+        return fma(ce[0], ab, fma(f[0], q0c, x[0]));
+    };
+    // 1. forward local, S independent chains
+    {
+        const double bb = co.beta_c, gg = co.gamma_c;
+#pragma unroll
+        for (int e = 0; e < M; ++e) {
+#pragma unroll
+            for (int b = 0; b < S; ++b) {
+                const double prev = e == 0 ? 0.0 : x[b * M + e - 1];
+                x[b * M + e] = fma(gg, prev, bb * x[b * M + e]);
+            }
+        }
+        zero_padding<L>(x, ln);
+    }
+    double Y[S], eb[S];
+#pragma unroll
+    for (int b = 0; b < S; ++b) Y[b] = x[b * M + M - 1];
+    eb[0] = 0.0;
+    eb[1] = Y[0];
+#pragma unroll
+    for (int b = 2; b < S; ++b) eb[b] = fma(af[b - 1], eb[b - 1], Y[b - 1]);
+    // 2. forward warp scan of the chunk ends
+    double B = fma(af[S - 1], eb[S - 1], Y[S - 1]);
+#pragma unroll
+    for (int d = 0; d < 5; ++d) B = fma(ln.Mf[d], __shfl_up_sync(0xffffffffu, B, 1 << d), B);
+    double E = __shfl_up_sync(0xffffffffu, B, 1);
+    if (ln.lane == 0) E = 0.0;
+    // 3. backward local on the uncorrected forward values, S independent chains
+    {
+        const double cc = co.cneg_c;
+#pragma unroll
+        for (int e = M - 2; e >= 0; --e) {
+#pragma unroll
+            for (int b = 0; b < S; ++b) x[b * M + e] = fma(cc, x[b * M + e + 1], x[b * M + e]);
+        }
+    }
+    // the chunk's first backward value with zero carries into the thread
+    double ce[S];
+    const double zeta = back_carries(eb, 0.0, ce);
+    // 4. backward warp scan of a = zeta + E q0
+    double R = fma(E, ln.q0, zeta);
+#pragma unroll
+    for (int d = 0; d < 5; ++d) R = fma(ln.Mb[d], __shfl_down_sync(0xffffffffu, R, 1 << d), R);
+    double RAn = __shfl_down_sync(0xffffffffu, R, 1);
+    if (ln.lane == 31) RAn = 0.0;
+    // 5. publish warp totals; one barrier; cross-warp carries (tri_solve)
+    const int par = ln.par;
+    if (ln.lane == 31) sl.tf[par][ln.warp] = B;
+    if (ln.lane == 0) sl.ta[par][ln.warp] = R;
+    const bool far = ln.corr && ln.warp > 0;
+    double z00 = 0.0, ra0 = 0.0;
+    if (co.ncw > 1) {
+        if (ln.t == 0) {
+            sl.z0[par] = zeta;
+            sl.ra0[par] = RAn;
+        }
+    } else if (ln.corr) {
+        z00 = __shfl_sync(0xffffffffu, zeta, 0);
+        ra0 = __shfl_sync(0xffffffffu, RAn, 0);
+    }
+    __syncthreads();
+    ln.par ^= 1;
+    double cC, cD, cD0 = 0.0;
+    {
+        const int v = ln.lane & (NW - 1);
+        const double tf = sl.tf[par][v], ta = sl.ta[par][v];
+        const int row = ln.warp * kMaxWarps + v;
+        cC = tb.wf[row] * tf;
+        cD = fma(tb.wb[row], ta, tb.wk[row] * tf);
+        if (far) cD0 = fma(tb.wb[v], ta, tb.wk[v] * tf);
+#pragma unroll
+        for (int off = NW / 2; off >= 1; off >>= 1) {
+            cC += __shfl_xor_sync(0xffffffffu, cC, off);
+            cD += __shfl_xor_sync(0xffffffffu, cD, off);
+        }
+        if (far) {
+#pragma unroll
+            for (int off = NW / 2; off >= 1; off >>= 1)
+                cD0 += __shfl_xor_sync(0xffffffffu, cD0, off);
+        }
+    }
+    double cf = fma(ln.Pfex, cC, E);
+    double cb = fma(ln.Pbex, cD, fma(ln.SB, cC, RAn));
+    if (ln.corr) {
+        if (co.ncw > 1) {
+            z00 = sl.z0[par];
+            ra0 = sl.ra0[par];
+        }
+        const double x0 = fma(fma(tb.pbex0, far ? cD0 : cD, ra0), tb.powc[kMaxL], z00);
+        const double ms = -co.sigma * x0;
+        cf = fma(ms, ln.cfw, cf);
+        cb = fma(ms, ln.cbw, cb);
+    }
+    // 6. sub-block carries, then x = z_loc + c_f[b] q + c_b[b] p_b
+    {
+        double cfb[S];
+        cfb[0] = cf;
+#pragma unroll
+        for (int b = 1; b < S; ++b) cfb[b] = fma(af[b - 1], cfb[b - 1], Y[b - 1]);
+        back_carries(cfb, cb, ce);
+#pragma unroll
+        for (int e = 0; e < M; ++e)
+#pragma unroll
+            for (int b = 0; b < S; ++b)
+                x[b * M + e] = fma(ce[b], co.sb_pb[e], fma(cfb[b], co.sb_q[e], x[b * M + e]));
+        zero_padding<L>(x, ln);
+    }
+}
+
 // (I + sub_dt L) x = x, in place, over the CTA (heat1d.cpp:47-60); CYC:
 // the periodic matrix with corner entries a (Allen-Cahn linear part).
 // warps per CTA of the instantiation for chunk length L (a power of two):
@@ -605,6 +818,12 @@ __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L, NW, C
 template <int L, bool CYC = false, int NW = warps_for(L), bool CL = false>
 __device__ __forceinline__ void tri_solve(double (&x)[L], const HeatCoefDev& co, Lane<L, NW, CL>& ln,
                                           const Tabs& tb, Slots& sl) {
+#ifndef ATM_NO_SUBBLOCK
+    if constexpr (!CYC && !CL && L == 16) {
+        tri_solve_sb<L>(x, co, ln, tb, sl);
+        return;
+    }
+#endif
     // 1. forward local  y_i = beta x_i + gamma y_{i-1}
     double y = 0.0;
     {

@@ -64,6 +64,31 @@ __global__ void k_dfma_tp(double* out, long long* cyc, double a, int n) {
     out[threadIdx.x] = s;
     if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
+// single-warp issue rate: NI independent DFMA chains per thread
+template <int NI>
+__global__ void k_dfma_ilp(double* out, long long* cyc, double a, int n) {
+    double x[NI];
+    for (int j = 0; j < NI; ++j) x[j] = threadIdx.x + j;
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+#pragma unroll
+        for (int j = 0; j < NI; ++j) x[j] = fma(a, x[j], 1.0);
+    }
+    long long t1 = clock64();
+    double s = 0;
+    for (int j = 0; j < NI; ++j) s += x[j];
+    out[threadIdx.x] = s;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+template <int NI>
+void run_ilp(double* o, long long* c, int n) {
+    long long h;
+    for (int nt : {32, 64, 128, 256, 384}) {
+        k_dfma_ilp<NI><<<1, nt>>>(o, c, 0.999, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+        printf("DFMA ILP %d, %d thr: %.2f cyc per warp-DFMA per warp, %.3f warp-DFMA/cyc/SM\n", NI, nt,
+               double(h) / (double(NI) * n), (nt / 32) * double(NI) * n / double(h));
+    }
+}
 int main() {
     double* o; long long* c; long long h;
     cudaMalloc(&o, 8 * 1024); cudaMalloc(&c, 8);
@@ -82,5 +107,10 @@ int main() {
         k_dfma_tp<<<1, nt>>>(o, c, 0.999, n); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
         printf("DFMA throughput %d thr: %.3f warp-DFMA/cyc/SM\n", nt, (nt / 32) * 8.0 * n / double(h));
     }
+    run_ilp<1>(o, c, n);
+    run_ilp<2>(o, c, n);
+    run_ilp<4>(o, c, n);
+    run_ilp<8>(o, c, n);
+    run_ilp<16>(o, c, n);
     return 0;
 }
