@@ -460,6 +460,11 @@ Engine::Engine(const atm_problem& p, const atm_grid& g, const atm_solver& s, con
     int dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev));
+    {
+        int l2 = 0;
+        CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+        l2_bytes_ = static_cast<size_t>(std::max(l2, 0));
+    }
     CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
 
     if (world_ > 1) {
@@ -880,6 +885,11 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         const CUtensorMap& tg = add_g ? Lv.g.tm : Lv.u.tm;
         const CUtensorMap& to = out_lv ? out_lv->r.tm : Lv.u.tm;
         a.n_out = choose_n_out(a);
+        // streaming rows: an array several times the L2 cannot be re-read from it,
+        // so its row stores are marked evict_first (config-5 correction sweep
+        // 0.95 -> 0.99 of the HBM peak); smaller levels keep the default policy
+        a.st_hint = sizeof(double) * pitch_ * static_cast<size_t>(Lv.u.rows) > 2 * l2_bytes_ ? 1 : 0;
+        if (const char* e = std::getenv("ATM_ST_HINT")) a.st_hint = std::atoi(e);
         int grid = grid_for(j1 - j0, heat_sweep_occupancy(a));
         if (const char* e = std::getenv("ATM_GRID_SWEEP")) grid = std::min(grid, std::atoi(e));
         if (std::getenv("ATM_DEBUG_OCC"))

@@ -211,6 +211,7 @@ private:
     void get_level0_cpts(int first, int count, double* out);
     std::vector<int> Lvl_;   // row-kernel chunk length per level
     int sms_ = 148;
+    size_t l2_bytes_ = 0;  // device L2 size: rows of arrays well past it are stored evict_first
     int world_ = 1, rank_ = 0, G_ = 1;
     std::vector<double> ic_, ff_, fw_, cval_, prov_, src_;
     double h_ = 0.0;

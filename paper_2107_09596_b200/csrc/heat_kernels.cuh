@@ -129,6 +129,7 @@ struct SweepArgs {
     int sq_div;        // 1: per-point array; m: per-C-point array (stopping norm)
     int n_out;         // output staging buffers (1 or 2)
     int u_div;         // > 1: the u array holds only the C points (row = (i - u_base) / u_div)
+    int st_hint;       // L2 policy of the per-warp row stores: 0 default, 1 evict_first, 2 evict_last
 };
 
 enum WindowKind { WK_LINEAR = 0, WK_FAS = 1, WK_FORWARD = 2, WK_APPLY = 3, WK_FAS_RHS = 4 };

@@ -1337,7 +1337,12 @@ __global__ void __launch_bounds__(NTMAX, MINB)
             __syncwarp();
             const int gw = ln.q * ln.nw + ln.warp;  // warp of the row (cluster rows: CTA q's part)
             if (ln.lane == 0 && gw * 32 * L < pitch) {
-                tma_store_3d(mapw, 0, gw * 2 * L, row, o + ln.warp * 256 * L);
+                // streaming u rows (an array far larger than the L2): evict_first;
+                // the policy is made here so that no register holds it across the Phi
+                if (a.st_hint && mapw == &tm_uw)
+                    tma_store_3d_hint(mapw, 0, gw * 2 * L, row, o + ln.warp * 256 * L,
+                                      a.st_hint == 2 ? l2_policy_evict_last() : l2_policy_evict_first());
+                else tma_store_3d(mapw, 0, gw * 2 * L, row, o + ln.warp * 256 * L);
                 bulk_commit();
             }
         } else {
