@@ -650,8 +650,8 @@ __device__ __forceinline__ void zero_padding(double (&x)[L], const Lane<L, NW, C
 }
 
 // The blocked solve with sub-block local passes (plain heat rows with L = 16:
-// the coarsest level's windows of config 5, every level of 1024 < n <= 2048;
-// the L = 32 level-0 sweeps keep tri_solve -- see profiles/README.md, round 2).
+// the coarsest level of 2048 < n <= 5376, i.e. config 5's windows; the L = 32
+// sweeps keep tri_solve -- see profiles/README.md, round 2).
 // Every chunk is S = L / M sub-blocks whose M-long local chains run
 // independently (4-way ILP on the FP64 pipe instead of 2 x L dependent
 // DFMAs), and the sub-block carries are folded into the fix-up the blocked

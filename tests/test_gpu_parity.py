@@ -339,9 +339,13 @@ def test_config5_shape_bitwise_across_shard_counts():
         assert np.array_equal(u, base[1]), workers
 
 
-@pytest.mark.parametrize("n", [2047, 2048, 2049, 3001, 4096])
+@pytest.mark.parametrize("n", [2047, 2048, 2049, 2053, 2056, 3001, 4090, 4095, 4096])
 def test_two_level_solve_across_chunk_lengths(n):
-    # n around the L = 16 / L = 32 switch (pitch > 2048) and the exact fit
+    # n around the L = 16 / L = 32 switch (pitch > 2048) and the exact fit;
+    # past 2048 the coarsest level's windows run the sub-block solve
+    # (tri_solve_sb, two 8-element chains per chunk): n % 16 = 1, 5 puts the
+    # row end inside the first sub-block of its thread (kappa of both
+    # sub-blocks), 8 on the sub-block boundary, 9, 10, 15 inside the second
     # (dt/h^2 ~ 1000, the stiffness of the BASELINE configs; at 1e4 the
     # reference's own fp64 Thomas error alone reaches ~1e-10 of the state)
     args = dict(problem="heat1d", n=n, tf=1.0 / 64, n_points=257, m=8, k=4, manufactured=1,
