@@ -465,6 +465,12 @@ __device__ __forceinline__ void tma_load_row(void* dst, const CUtensorMap* map, 
     }
 }
 
+// whole-row reduction global += shared (same boxes as the store)
+__device__ __forceinline__ void tma_reduce_row(const CUtensorMap* map, int c0, int c1, const void* src, int R) {
+    tma_reduce_add_2d(map, c0, c1, src);
+    if (R > 256) tma_reduce_add_2d(map, c0, c1 + R / 2, static_cast<const char*>(src) + (R / 2) * 128);
+}
+
 // the matching whole-row store (bulk-group completion: one commit covers all boxes)
 __device__ __forceinline__ void tma_store_row(const CUtensorMap* map, int c0, int c1, const void* src, int R) {
     tma_store_2d(map, c0, c1, src);
@@ -1495,17 +1501,21 @@ __global__ void __launch_bounds__(NTMAX, MINB)
     const int pitch = a.co.pitch;
     const int spitch = pitch / cl_;
     const int rb = row_bytes_al(spitch);
-    // r-row stream depth: 2 buffers, or 1 for L = 32 (three 128-thread CTAs
-    // per SM need <= 75 KB each; every consume is followed by a Phi that
-    // hides the next load except at window starts)
-    constexpr int NB = (L == 32) ? 1 : 2;
+    // L = 32 (three 128-thread CTAs per SM need <= 75 KB each): two r-row
+    // stream buffers and no fine-row buffer -- an emit stages e into the
+    // stream buffer it has just consumed and adds it to the fine C row with a
+    // TMA reduction (fp64 add in the L2; one window per row, so the sum is
+    // the load-add-store's), then refills the buffer once the reduction has
+    // read it
+    constexpr bool RED = (L == 32);
+    constexpr int NB = 2;
     char* bufA0 = base;
     char* bufA1 = base + (NB - 1) * rb;
     // fine C rows: one buffer, or three (a.two_s: long prefix chains, whose
     // emits are back to back: row s + 2 is fetched at emit s into the buffer
     // of emit s - 1, whose store has had a whole step to drain, so neither
     // the store's smem read nor the load sits on the chain)
-    const int NS = a.two_s ? 3 : 1;
+    const int NS = RED ? 0 : (a.two_s ? 3 : 1);
     char* bufS = base + NB * rb;
     Tabs& tb = *reinterpret_cast<Tabs*>(base + (NB + NS) * rb);
     Slots& sl = *reinterpret_cast<Slots*>(base + (NB + NS) * rb + sizeof(Tabs));
@@ -1592,6 +1602,44 @@ __global__ void __launch_bounds__(NTMAX, MINB)
         if (NB == 2) cb ^= 1;
     };
 
+    if constexpr (RED) {
+        // consume row s of the stream; when the step emits, the consumed
+        // buffer carries e to the fine row before it is refilled
+        auto step = [&](bool add, bool emit, int s) {
+            if (cb) {
+                mbar_wait(barA1, ph1);
+                ph1 ^= 1;
+            } else {
+                mbar_wait(barA0, ph0);
+                ph0 ^= 1;
+            }
+            char* buf = cb ? bufA1 : bufA0;
+            if (add) row_acc<L>(buf, x, ln, false);
+            else row_load<L>(buf, x, ln);
+            if (emit) row_store<L>(buf, x, ln);  // each thread rewrites only what it read
+            fence_proxy_async();  // reads before the refill (WAR), writes before the reduction
+            __syncthreads();
+            if (t == 0) {
+                if (emit) {
+                    tma_reduce_row(&tm_fine, 0, (s * a.out_stride - a.out_base) * R + qoff, buf, RS);
+                    bulk_commit();
+                    bulk_wait_read<0>();
+                }
+                issue_next(cb);
+            }
+            cb ^= 1;
+        };
+        for (int q = cid; q < Nj; q += G) {
+            int lo, e0, e1;
+            job_range(q, lo, e0, e1);
+            step(false, lo >= e0, lo);  // e = r_lo
+            for (int s = lo + 1; s <= e1; ++s) {
+                if (plain) tri_solve<L>(x, a.co, ln, tb, sl);
+                else phi_p<P, L>(x, a.co, ln, tb, sl, ends, s, a.forced);
+                step(true, s >= e0, s);  // e = Psi(e) + r_s
+            }
+        }
+    } else
     for (int q = cid; q < Nj; q += G) {
         int lo, e0, e1;
         job_range(q, lo, e0, e1);

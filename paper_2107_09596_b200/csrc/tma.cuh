@@ -55,6 +55,17 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
                  : "memory");
 }
 
+// 2D tiled TMA reduction shared -> global: global += shared, element-wise in
+// the tensor map's type (fp64 add performed in the L2; bulk-group completion).
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, int c0, int c1,
+                                                  const void* src) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(c0), "r"(c1), "r"(smem_u32(src))
+        : "memory");
+}
+
 // 3D tiled TMA store shared -> global (bulk-group completion); out-of-range
 // parts of the box are clipped by the hardware.
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2,
