@@ -401,24 +401,32 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo", rank=rank, world_size=world)
         pg = dist
+
+    def new_nccl_id():
+        # one NCCL unique id per communicator (an id cannot be reused for a
+        # second ncclCommInitRank): rank 0 draws it, gloo carries it
+        if world == 1:
+            return None
         import ctypes as C
         buf = (C.c_char * 128)()
         if rank == 0:
             assert T.lib().atm_nccl_unique_id(buf) == 0, "NCCL unavailable"
         obj = [bytes(buf) if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        pg.broadcast_object_list(obj, src=0)
+        return obj[0]
 
     ic = T.random_state(W["u0_seed"], n)
     hier = T.build_hierarchy(T.TimeGrid.make(0.0, W["tf"], W["n_points"]), [W["m"]], W["k"])
     cfg = T.SolverConfig(mode=T.CycleMode.TwoLevel, relaxation=T.Relaxation.F, tol=W["tol"],
                          max_iters=1_000_000, initial_guess=T.InitialGuess.Random, seed=W["guess_seed"])
     app = T.Heat1D(n, manufactured_forcing=False, initial_condition=ic)
-    drv = T.CycleDriver(app, hier, cfg, device=dev, trace=True,
-                        world_size=world, rank=rank, nccl_id=nccl_id)
+    # the timed region runs the cycle as a user gets it (untraced: a single
+    # process replays the captured CUDA graph); the phase split and the
+    # dominant kernel's duration come from the same K iterations repeated
+    # under per-phase CUDA events right after (`ms_per_step_traced`)
+    drv = T.CycleDriver(app, hier, cfg, device=dev, world_size=world, rank=rank, nccl_id=new_nccl_id())
     drv.setup()
     drv.iterate(args.warmup)
-    t_before = drv.timings(with_counts=True)
     launches = drv.last_iteration_launches()
     if pg:
         pg.barrier()
@@ -433,7 +441,18 @@ def main():
         t = torch.tensor([ms], dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ms = float(t.item())
-    t_after = drv.timings(with_counts=True)
+    drv.close()
+    tr = T.CycleDriver(app, hier, cfg, device=dev, trace=True, world_size=world, rank=rank,
+                       nccl_id=new_nccl_id())
+    tr.setup()
+    tr.iterate(args.warmup)
+    t_before = tr.timings(with_counts=True)
+    if pg:
+        pg.barrier()
+    norms_tr, ms_traced = tr.iterate_timed(args.steps)
+    t_after = tr.timings(with_counts=True)
+    tr.close()
+    assert np.array_equal(norms, norms_tr), "traced and untraced cycles must be the same iterations"
 
     per_iter = dof_steps_per_iter(n, W["n_points"], W["m"])
     value = per_iter * args.steps / (ms / 1e3)
@@ -451,7 +470,9 @@ def main():
     peak, peak_src = read_peaks()
     achieved = sweep_bytes / (sweep_ms / 1e3) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_sweep_summary_r02.json")
+    if not os.path.exists(prof):
+        prof = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
@@ -491,6 +512,7 @@ def main():
             "roofline_fp64": {"bound": "fp64 (Phi-chain latency)", "peak": fpk, "unit": "TFLOP/s",
                               "peak_source": fpk_src, "kernels": fp64},
             "gpu_launches": launches * args.steps,
+            "ms_per_step_traced": ms_traced / args.steps,
             "phase_ms_per_step": phase_ms,
             "last_norm": float(norms[-1])}
     if sampler:
@@ -520,7 +542,7 @@ def main():
         # defer_guess: atm_setup sends the guess's C rows; its F rows are dead
         # under cycling (rewritten before any read), so they never move
         drv2 = T.CycleDriver(app, hier, cfg2, device=dev, defer_guess=True,
-                             world_size=world, rank=rank, nccl_id=nccl_id)
+                             world_size=world, rank=rank, nccl_id=new_nccl_id())
         if pg:
             pg.barrier()
         t0 = time.perf_counter()
@@ -556,7 +578,8 @@ def main():
     ttf = None
     if not args.no_ttt_full:
         try:
-            ttf = time_to_tolerance_full(T, W, config["workload"], app, hier, dev, world, rank, nccl_id, pg)
+            ttf = time_to_tolerance_full(T, W, config["workload"], app, hier, dev, world, rank,
+                                         new_nccl_id(), pg)
             line["time_to_tolerance_full"] = ttf
         except Exception as e:  # reported, not fatal
             line["time_to_tolerance_full"] = {"unavailable": str(e)}
