@@ -324,6 +324,7 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double r_in, double shift
     // leading elements inside the row has q' = q - kappa p_b on them,
     // kappa = sum_{j >= real} (-c)^{j - M} gamma^{j + 1}: the thread holding
     // element n-1 folds kappa_b (powc row 2) into its sub-block c_b.
+#ifndef ATM_NO_SUBBLOCK
     if (!cyclic && L == 16) {
         constexpr int M = 8;
         const int S = L / M;
@@ -351,6 +352,7 @@ HeatLevelHost heat_level_host(int n, int pitch, int L, double r_in, double shift
             H.powc[2 * kMaxL + b] = static_cast<double>(kap);
         }
     }
+#endif
     return H;
 }
 
