@@ -83,6 +83,22 @@ def test_phi_matches_oracle(n, level):
     _check_phi(drv, orc, hier, n, level, 1, xs, 3 if level == 1 else 1)
 
 
+@pytest.mark.parametrize("n", [33, 100, 1000, 2051, 2053, 2056, 3003, 4090])
+def test_phi_sub_block_solver_matches_oracle(n, monkeypatch):
+    # ATM_HEAT_L=16 puts every level on the L = 16 kernels, i.e. the
+    # sub-block solve (tri_solve_sb): row ends at every position of a chunk's
+    # two 8-element sub-blocks (n % 16 = 1, 4, 8, 3, 5, 8, 11, 10), rows of one
+    # to 257 chunks, three sub-steps
+    monkeypatch.setenv("ATM_HEAT_L", "16")
+    args = _heat_case(n, substeps=3)
+    app, hier, cfg = device_objects(args)
+    drv = T.CycleDriver(app, hier, cfg)
+    orc = oracle_driver(args)
+    xs = np.stack([O.random_state(100 + j, n) for j in range(3)])
+    for level in (0, 1):
+        _check_phi(drv, orc, hier, n, level, 1, xs, 3 if level == 1 else 1)
+
+
 @pytest.mark.parametrize("n", [63, 257, 1025, 4095])
 @pytest.mark.parametrize("tf", [1.0 / 64, 1.0 / 4, 4.0])
 def test_phi_across_stiffness(n, tf):
