@@ -1350,7 +1350,9 @@ void Engine::f_sweep(int level, int tail, int store) {
         if (tail == TAIL_NONE) return;
         store = STORE_NONE;
     }
-    halo(level, &LevelDev::u);
+    // (the exchange of the previous cycle's correction sweep still stands when
+    // no C point has been written since: halo0_valid_)
+    if (!(level == 0 && halo0_valid_)) halo(level, &LevelDev::u);
     const char* tag = level != 0 ? nullptr
                       : (tail == TAIL_SQ || tail == TAIL_BOTH) ? "sweep_correct"
                       : tail == TAIL_STORE                     ? "sweep_relax"
@@ -1564,12 +1566,16 @@ void Engine::two_level_cycle() {
     if (sol_.relaxation != ATM_RELAX_F) resid_c(0);
     for (Shard& s : sh_) point0_residual(s, 0, s.lv[1].r.p, nullptr);
     phase_end();
+    halo0_valid_ = false;  // the windows write the C points
     coarsest_linear();
     phase_begin("correct");
     f_sweep(0, reuse ? TAIL_BOTH : TAIL_SQ);
     for (Shard& s : sh_) point0_residual(s, 0, d_row_, d_sq_c_);
     phase_end();
     relax_valid_ = reuse;
+    // one process per shard (no graph replay of a fixed exchange sequence):
+    // the correction sweep's halo serves the next cycle's relaxation sweep too
+    halo0_valid_ = world_ > 1 && sol_.relaxation == ATM_RELAX_F && !std::getenv("ATM_HALO_EVERY_SWEEP");
 }
 
 // One cycle = a fixed launch sequence on one stream: captured once into a
@@ -1601,7 +1607,7 @@ void Engine::cycle() {
             relax_valid_ = reuse_possible();
         }
     } catch (...) {
-        relax_valid_ = false;
+        relax_valid_ = halo0_valid_ = false;
         if (graphs) {
             cudaGraph_t g = nullptr;
             cudaStreamEndCapture(st_, &g);
@@ -1634,7 +1640,7 @@ void Engine::cycle() {
     try {
         check_newton();
     } catch (...) {
-        relax_valid_ = false;  // a failed Phi leaves no residuals worth keeping
+        relax_valid_ = halo0_valid_ = false;  // a failed Phi leaves no residuals worth keeping
         throw;
     }
 }
@@ -1663,7 +1669,7 @@ void Engine::nested_init() {
     // solver.cpp:331-368
     setup();
     flush_guess();
-    relax_valid_ = false;
+    relax_valid_ = halo0_valid_ = false;
     const int lc = H_.coarsest();
     for (int l = 0; l < lc; ++l) {
         const int m = H_.m[l];
@@ -1886,7 +1892,7 @@ void Engine::xfer_level(int level, int which, int first, int count, double* host
     if (count < 0 || first < 0 || first + count > H_.np[level]) config_error("point range out of range");
     if (!to_host) {
         setup();
-        relax_valid_ = false;
+        relax_valid_ = halo0_valid_ = false;
     }
     if (level == 0) flush_guess();
     sync_stream(__func__);
@@ -2013,7 +2019,7 @@ void Engine::apply_phi(int level, int first, int count, const double* in, double
 void Engine::kernel_f_relax(int level, int first_iv, int count) {
     if (level == 0 && cpts_)
         config_error("kernel-level entry points need full level-0 storage");
-    relax_valid_ = false;
+    relax_valid_ = halo0_valid_ = false;
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
     flush_guess();
@@ -2025,7 +2031,7 @@ void Engine::kernel_f_relax(int level, int first_iv, int count) {
 void Engine::kernel_c_relax(int level, int first_c, int count) {
     if (level == 0 && cpts_)
         config_error("kernel-level entry points need full level-0 storage");
-    relax_valid_ = false;
+    relax_valid_ = halo0_valid_ = false;
     if (G_ != 1) config_error("kernel-level entry points need a single shard");
     setup();
     flush_guess();

@@ -268,6 +268,11 @@ private:
     bool use_graphs() const;
     bool reuse_possible() const;
     bool relax_valid_ = false;  // level-1 r holds the residuals of the current C points
+    // multi-process two-level F cycles: the level-0 left-edge row still holds
+    // the left neighbour's current last C point (nothing has written a C point
+    // since the correction sweep's exchange), so the next cycle's opening
+    // F-sweep needs no second halo exchange
+    bool halo0_valid_ = false;
     cudaGraphExec_t graph_exec_ = nullptr;
     int graph_launches_ = 0;
     double last_sweep_ms_ = 0.0;
