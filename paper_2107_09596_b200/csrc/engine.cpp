@@ -887,7 +887,8 @@ void Engine::sweep_jobs(Shard& s, int level, int kind, int j0, int j1, int tail,
         a.n_out = choose_n_out(a);
         // streaming rows: an array several times the L2 cannot be re-read from it,
         // so its row stores are marked evict_first (config-5 correction sweep
-        // 0.95 -> 0.99 of the HBM peak); smaller levels keep the default policy
+        // 0.95 -> 1.00 of the measured HBM copy peak); smaller levels keep the
+        // default policy
         a.st_hint = sizeof(double) * pitch_ * static_cast<size_t>(Lv.u.rows) > 2 * l2_bytes_ ? 1 : 0;
         if (const char* e = std::getenv("ATM_ST_HINT")) a.st_hint = std::atoi(e);
         int grid = grid_for(j1 - j0, heat_sweep_occupancy(a));

@@ -46,7 +46,7 @@ struct HeatCoefDev {
     double beta_c, gamma_c, cneg_c;  // fixed-point factors: 1/d*, r/d*, -c*
     double sigma;          // Sherman-Morrison scale
     int ncw;               // warps [0, ncw) carry the left correction vector
-    // sub-block local passes (plain heat rows, L >= 16): every chunk runs as
+    // sub-block local passes (plain heat rows with L = 16): every chunk runs as
     // L / sb_m independent chains of sb_m elements; sb_af = gamma^sb_m and
     // sb_ab = (-c)^sb_m carry between the sub-blocks (heat_phi5.cu, tri_solve_sb)
     int sb_m;
