@@ -7,6 +7,12 @@ __global__ void st_kernel(double2* p, size_t n2) {
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (; i < n2; i += stride) p[i] = make_double2(1.0, 2.0);
 }
+// streaming stores (st.global.cs: evict-first)
+__global__ void st_cs_kernel(double2* p, size_t n2) {
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (; i < n2; i += stride) __stcs(p + i, make_double2(1.0, 2.0));
+}
 __global__ void ld_kernel(const double2* p, size_t n2, double* out) {
     size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -25,6 +31,8 @@ int main() {
         cudaEventElapsedTime(&ms, a, b); printf("memset write: %.1f GB/s\n", bytes / ms / 1e6);
         cudaEventRecord(a); st_kernel<<<148 * 8, 512>>>((double2*)p, bytes / 16); cudaEventRecord(b); cudaEventSynchronize(b);
         cudaEventElapsedTime(&ms, a, b); printf("st.global.v2 write: %.1f GB/s\n", bytes / ms / 1e6);
+        cudaEventRecord(a); st_cs_kernel<<<148 * 8, 512>>>((double2*)p, bytes / 16); cudaEventRecord(b); cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b); printf("st.global.cs.v2 write: %.1f GB/s\n", bytes / ms / 1e6);
         cudaEventRecord(a); ld_kernel<<<148 * 8, 512>>>((const double2*)p, bytes / 16, o); cudaEventRecord(b); cudaEventSynchronize(b);
         cudaEventElapsedTime(&ms, a, b); printf("ld read: %.1f GB/s\n", bytes / ms / 1e6);
         cudaEventRecord(a); cudaMemcpyAsync(p + bytes / 16, p, bytes / 2, cudaMemcpyDeviceToDevice); cudaEventRecord(b); cudaEventSynchronize(b);
