@@ -99,6 +99,21 @@ def test_phi_sub_block_solver_matches_oracle(n, monkeypatch):
         _check_phi(drv, orc, hier, n, level, 1, xs, 3 if level == 1 else 1)
 
 
+@pytest.mark.parametrize("n", [2053, 4090, 4096])
+@pytest.mark.parametrize("tf", [1e-9, 1e-4, 64.0])
+def test_phi_sub_block_solver_across_stiffness(n, tf, monkeypatch):
+    # dt/h^2 from ~1e-4 (gamma^8 ~ 1e-33: the kappa of a short sub-block is a
+    # large number times a tiny p_b) to ~1e7 (carries reach across the row)
+    monkeypatch.setenv("ATM_HEAT_L", "16")
+    args = dict(_heat_case(n, n_points=4097, m=16, k=8), tf=tf)
+    app, hier, cfg = device_objects(args)
+    drv = T.CycleDriver(app, hier, cfg)
+    orc = oracle_driver(args)
+    xs = np.stack([O.random_state(300 + j, n) for j in range(2)])
+    for level in (0, 1):
+        _check_phi(drv, orc, hier, n, level, 1, xs, 1)
+
+
 @pytest.mark.parametrize("n", [63, 257, 1025, 4095])
 @pytest.mark.parametrize("tf", [1.0 / 64, 1.0 / 4, 4.0])
 def test_phi_across_stiffness(n, tf):
