@@ -508,7 +508,8 @@ def main():
                          "peak_source": peak_src,
                          "note": "the peak is a device-to-device copy (half reads, half writes); this "
                                  "sweep is 94% writes stored with an L2 evict_first policy, so frac can "
-                                 "reach or slightly pass 1"},
+                                 "reach or slightly pass 1 (streaming stores alone: 6.67-6.70 TB/s on the "
+                                 "same pool, profiles/ubench_wbw_r02.txt)"},
             "roofline_fp64": {"bound": "fp64 (Phi-chain latency)", "peak": fpk, "unit": "TFLOP/s",
                               "peak_source": fpk_src, "kernels": fp64},
             "gpu_launches": launches * args.steps,
