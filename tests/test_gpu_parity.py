@@ -370,6 +370,24 @@ def test_config5_shape_bitwise_across_shard_counts():
         assert np.array_equal(u, base[1]), workers
 
 
+def test_config5_shape_l32_windows_and_store_policies_against_the_reference(monkeypatch):
+    # the config-5 shape (N_t = 2^14, k = 8) against the compiled reference's
+    # fixture with the coarsest level on the L = 32 window kernel (two stream
+    # buffers, emit by TMA reduce-add into the fine C row), and the level-0 row
+    # stores under every L2 policy (the policy cannot change a value: bitwise)
+    monkeypatch.setenv("ATM_WIN_L32", "1")
+    a = _golden_solve("config5r_k8")
+    monkeypatch.delenv("ATM_WIN_L32")
+    states = []
+    for hint in ("0", "1", "2"):
+        monkeypatch.setenv("ATM_ST_HINT", hint)
+        r = _golden_solve("config5r_k8")
+        states.append((np.array(r.report.residual_norms), np.asarray(r.state)))
+    for h, st in states[1:]:
+        assert np.array_equal(h, states[0][0]) and np.array_equal(st, states[0][1])
+    assert a.report.iterations == r.report.iterations
+
+
 @pytest.mark.parametrize("n", [2047, 2048, 2049, 2053, 2056, 3001, 4090, 4095, 4096])
 def test_two_level_solve_across_chunk_lengths(n):
     # n around the L = 16 / L = 32 switch (pitch > 2048) and the exact fit;
